@@ -1,0 +1,151 @@
+/*
+ * alphax_b200.h -- C ABI of the B200-native alpha-complex hot path.
+ *
+ * The reference package (alphax 0.1.0) has no FFI layer: its boundary for this
+ * path is the Python function compute_alpha_complex (reference
+ * pkg/src/alphax/pipeline.py:571-628) plus the standalone stage operations
+ * (pipeline.py:640-731, grid.py:105-144).  This header is the C-ABI a binding
+ * for that boundary would call; each entry point names the reference code it
+ * replaces.  Plain pointers and sizes only; no exceptions cross the ABI; every
+ * function returns an axb_status.  All device work is hand-written CUDA for
+ * sm_100a (paper_1908_05944_b200/csrc), launched on the context's stream.
+ *
+ * Memory: the caller owns all device memory.  Scratch comes from one caller-
+ * provided arena (axb_ctx_set_arena); when it is too small a call returns
+ * AXB_ERR_ARENA and axb_arena_needed() says how much would have been enough so
+ * far -- grow and call again.  Inputs/outputs are caller buffers.
+ */
+#ifndef ALPHAX_B200_H
+#define ALPHAX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum axb_status {
+    AXB_OK = 0,
+    AXB_ERR_BAD_ARG = 1,
+    AXB_ERR_CUDA = 2,          /* a CUDA runtime call failed; see axb_last_message */
+    AXB_ERR_ARENA = 3,         /* scratch arena too small; see axb_arena_needed    */
+    AXB_ERR_EMPTY = 4,         /* EmptyInput            (pipeline.py:226-227)      */
+    AXB_ERR_NONFINITE = 5,     /* NonFiniteCoordinate   (pipeline.py:235-237)      */
+    AXB_ERR_DUPLICATE = 6,     /* DuplicateCenter       (pipeline.py:238-244)      */
+    AXB_ERR_DEGENERATE = 7,    /* DegenerateSimplex     (pipeline.py:263-266)      */
+    AXB_ERR_BAD_SIDE = 8,      /* ValueError, non-positive squared cell side (grid.py:113-117) */
+    AXB_ERR_GRID_TOO_LARGE = 9,/* dense cell table would exceed the supported size */
+    AXB_ERR_DENSITY = 10,      /* a ball has more than AXB_MAX_PARTNERS potential-edge partners */
+    AXB_ERR_STATE = 11,        /* stages called out of order                       */
+    AXB_ERR_INTERNAL = 12
+} axb_status;
+
+#define AXB_MAX_PARTNERS 256
+
+typedef struct axb_ctx axb_ctx;
+
+/* run parameters: PipelineConfig + TolerancePolicy (pipeline.py:55-83, geometry.py:22-37) */
+typedef struct axb_params {
+    double alpha;          /* A^2, compared as size <= alpha + eps_abs */
+    double eps_abs;        /* TolerancePolicy.eps_abs      */
+    double eps_singular;   /* TolerancePolicy.eps_singular */
+    int32_t biomolecule;   /* PipelineConfig.biomolecule_mode */
+    int32_t reserved;
+} axb_params;
+
+/* grid geometry (grid.py:30-39) */
+typedef struct axb_grid_info {
+    double origin[3];
+    double cell_side;
+    int64_t dims[3];
+    int64_t n_cells;
+    int64_t n_balls;
+} axb_grid_info;
+
+/* what-selectors */
+enum { AXB_K0 = 0, AXB_K1 = 1, AXB_K2 = 2, AXB_K3 = 3, AXB_PE = 4, AXB_PT = 5, AXB_PQ = 6 };
+
+/* stage indices of axb_stage_ms: the reference's STAGE_NAMES (pipeline.py:43-52)
+ * with "io" replaced by prune_vertices (cli.py:210 folds it into prune_edges),
+ * plus this implementation's canonicalisation (count/scan/scatter) and export
+ * (in-bucket sort + int64 rows) stages. */
+enum {
+    AXB_ST_GRID = 0, AXB_ST_POT_EDGES, AXB_ST_POT_TRIANGLES, AXB_ST_POT_TETS,
+    AXB_ST_PRUNE_TETS, AXB_ST_PRUNE_TRIANGLES, AXB_ST_PRUNE_EDGES, AXB_ST_PRUNE_VERTICES,
+    AXB_ST_CANONICAL, AXB_ST_EXPORT, AXB_ST_COUNT
+};
+
+/* ---- context ---------------------------------------------------------- */
+int axb_version(void);
+const char *axb_status_name(int status);
+int axb_ctx_create(axb_ctx **out, int device);
+void axb_ctx_destroy(axb_ctx *ctx);
+int axb_ctx_set_stream(axb_ctx *ctx, void *cuda_stream);      /* cudaStream_t; NULL = default */
+int axb_ctx_set_arena(axb_ctx *ctx, void *dev_ptr, size_t bytes);
+size_t axb_arena_needed(const axb_ctx *ctx);
+size_t axb_arena_used(const axb_ctx *ctx);
+/* a conservative first guess for the arena size (bytes) */
+size_t axb_arena_hint(int64_t n, double alpha, double r_max);
+const char *axb_last_message(const axb_ctx *ctx);
+/* AXB_ERR_NONFINITE: verts[0]; AXB_ERR_DUPLICATE: verts[0..1];
+ * AXB_ERR_DEGENERATE: verts[0..nverts-1] ascending ball indices. */
+int axb_last_error(const axb_ctx *ctx, int *status, int64_t verts[4], int *nverts);
+
+/* ---- the hot path, stage by stage ------------------------------------- */
+/* validate_input + build_grid_arrays (pipeline.py:224-245, grid.py:105-144).
+ * d_xyz: n x 3 row-major f64, d_radii: n f64, both DEVICE pointers. */
+int axb_grid_build(axb_ctx *ctx, int64_t n, const double *d_xyz, const double *d_radii,
+                   const axb_params *params);
+int axb_grid_get_info(const axb_ctx *ctx, axb_grid_info *out);
+/* order / rank / ball_cells of the reference Grid as int64 DEVICE arrays (any may be NULL) */
+int axb_grid_export(axb_ctx *ctx, int64_t *d_order, int64_t *d_rank, int64_t *d_ball_cells);
+
+/* _chunk_potential_edges / _triangles / _tets (pipeline.py:316-479) for the
+ * generators at grid ranks [rank_lo, rank_hi); (0, n) is the whole input. */
+int axb_potential(axb_ctx *ctx, int64_t rank_lo, int64_t rank_hi);
+/* counts[0..2] = potential edges, triangles, tets */
+int axb_potential_counts(const axb_ctx *ctx, int64_t counts[3]);
+/* one potential level as the reference's PotentialLevel (pipeline.py:86-106):
+ * rows (m, dim+1) int64 ascending ball indices, lexicographically sorted,
+ * with cached centres (m,3) / sizes (m,) (either may be NULL).  DEVICE buffers. */
+int axb_potential_export(axb_ctx *ctx, int what, int64_t *d_rows, double *d_centers, double *d_sizes);
+
+/* _prune_levels (pipeline.py:482-527): AC2 at every ortho-centre, inheritance of faces */
+int axb_prune(axb_ctx *ctx);
+/* canonical sort + dedup (pipeline.py:611-614, _arrays.py:12-16); counts[d] = simplices of dimension d */
+int axb_canonicalize(axb_ctx *ctx, int64_t counts[4]);
+/* the four canonical int64 arrays of AlphaComplex (pipeline.py:117-130) into DEVICE buffers
+ * sized from axb_canonicalize's counts: (k0,), (k1,2), (k2,3), (k3,4) */
+int axb_export(axb_ctx *ctx, int64_t *d_vertices, int64_t *d_edges, int64_t *d_triangles, int64_t *d_tets);
+
+/* waits for the stream and reports deferred device-side flags (singular solves, internal checks);
+ * call it after axb_export before trusting DEVICE output buffers (axb_export_host does it itself) */
+int axb_sync_check(axb_ctx *ctx);
+
+/* ---- the hot path in one call ------------------------------------------ */
+/* compute_alpha_complex (pipeline.py:571-628, mode="grid") on DEVICE inputs:
+ * grid_build -> potential(0,n) -> prune -> canonicalize. */
+int axb_compute(axb_ctx *ctx, int64_t n, const double *d_xyz, const double *d_radii,
+                const axb_params *params, int64_t counts[4]);
+/* Same from HOST buffers: copies inputs to the arena, runs axb_compute. */
+int axb_compute_host(axb_ctx *ctx, int64_t n, const double *h_xyz, const double *h_radii,
+                     const axb_params *params, int64_t counts[4]);
+/* axb_export into HOST buffers (pinned or pageable). */
+int axb_export_host(axb_ctx *ctx, int64_t *h_vertices, int64_t *h_edges, int64_t *h_triangles, int64_t *h_tets);
+
+/* ---- measurement -------------------------------------------------------- */
+/* CUDA-event milliseconds per stage of the last run */
+int axb_stage_ms(const axb_ctx *ctx, float out[AXB_ST_COUNT]);
+/* number of kernels this library launched since the context was created */
+int64_t axb_kernel_launches(const axb_ctx *ctx);
+
+/* ---- predicate probes (unit tests of the device arithmetic) ------------- */
+/* geometry.py:161-181 on the device: pts (m,k,3), r2 (m,k), DEVICE pointers */
+int axb_ortho_batch(axb_ctx *ctx, int64_t m, int k, const double *d_pts, const double *d_r2,
+                    double eps_singular, double *d_centers, double *d_sizes, uint8_t *d_singular);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

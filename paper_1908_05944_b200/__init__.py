@@ -1,1 +1,48 @@
-"""B200-native alpha-complex hot path (drop-in for alphax.compute_alpha_complex)."""
+"""B200-native alpha-complex construction (arXiv 1908.05944) -- a drop-in for
+the hot path of the reference package ``alphax``:
+
+    from paper_1908_05944_b200 import Ball, PipelineConfig, compute_alpha_complex
+
+Python/PyTorch host code over hand-written sm_100a CUDA kernels behind a thin
+C-ABI (``include/alphax_b200.h``).  No CPU fallback: computing without the
+built library or without a GPU raises ``NativeLibraryMissing``.
+"""
+
+__version__ = "0.1.0"
+
+from .errors import (
+    AlphaxError,
+    DegenerateSimplex,
+    DuplicateCenter,
+    EmptyInput,
+    MalformedLine,
+    MalformedRecord,
+    NativeLibraryMissing,
+    NoAtoms,
+    NonFiniteCoordinate,
+    NonFiniteValue,
+    NonPositiveRadius,
+)
+from .types import DEFAULT_TOLERANCE, Ball, OrthoResult, SimplexKey, TolerancePolicy, simplex_compare
+from .pipeline import (
+    STAGE_NAMES,
+    AlphaComplex,
+    ComplexStats,
+    Engine,
+    PipelineConfig,
+    as_ball_arrays,
+    closure_ok,
+    complex_stats,
+    compute_alpha_complex,
+    compute_alpha_complex_arrays,
+    default_engine,
+)
+from . import synth
+
+__all__ = [
+    "AlphaComplex", "AlphaxError", "Ball", "ComplexStats", "DEFAULT_TOLERANCE", "DegenerateSimplex",
+    "DuplicateCenter", "EmptyInput", "Engine", "MalformedLine", "MalformedRecord", "NativeLibraryMissing",
+    "NoAtoms", "NonFiniteCoordinate", "NonFiniteValue", "NonPositiveRadius", "OrthoResult", "PipelineConfig",
+    "STAGE_NAMES", "SimplexKey", "TolerancePolicy", "as_ball_arrays", "closure_ok", "complex_stats",
+    "compute_alpha_complex", "compute_alpha_complex_arrays", "default_engine", "simplex_compare", "synth",
+]

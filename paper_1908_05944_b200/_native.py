@@ -1,0 +1,93 @@
+"""ctypes binding of libalphax_b200.so -- the C-ABI in include/alphax_b200.h.
+
+There is NO fallback: if the library is missing or CUDA is unavailable the
+calls raise ``NativeLibraryMissing``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import NativeLibraryMissing
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libalphax_b200.so")
+
+(OK, ERR_BAD_ARG, ERR_CUDA, ERR_ARENA, ERR_EMPTY, ERR_NONFINITE, ERR_DUPLICATE, ERR_DEGENERATE,
+ ERR_BAD_SIDE, ERR_GRID_TOO_LARGE, ERR_DENSITY, ERR_STATE, ERR_INTERNAL) = range(13)
+
+K0, K1, K2, K3, PE, PT, PQ = range(7)
+STAGE_KEYS = ("grid", "potential_edges", "potential_triangles", "potential_tets", "prune_tets",
+              "prune_triangles", "prune_edges", "prune_vertices", "canonical", "export")
+
+# every symbol include/alphax_b200.h declares
+SYMBOLS = (
+    "axb_version", "axb_status_name", "axb_ctx_create", "axb_ctx_destroy", "axb_ctx_set_stream",
+    "axb_ctx_set_arena", "axb_arena_needed", "axb_arena_used", "axb_arena_hint", "axb_last_message",
+    "axb_last_error", "axb_grid_build", "axb_grid_get_info", "axb_grid_export", "axb_potential",
+    "axb_potential_counts", "axb_potential_export", "axb_prune", "axb_canonicalize", "axb_export",
+    "axb_sync_check", "axb_compute", "axb_compute_host", "axb_export_host", "axb_stage_ms",
+    "axb_kernel_launches", "axb_ortho_batch",
+)
+
+
+class Params(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("eps_abs", C.c_double), ("eps_singular", C.c_double),
+                ("biomolecule", C.c_int32), ("reserved", C.c_int32)]
+
+
+class GridInfo(C.Structure):
+    _fields_ = [("origin", C.c_double * 3), ("cell_side", C.c_double), ("dims", C.c_int64 * 3),
+                ("n_cells", C.c_int64), ("n_balls", C.c_int64)]
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """dlopen the library and declare the prototypes (no CUDA call is made)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryMissing(
+            f"{LIB_PATH} is not built (run `python -m paper_1908_05944_b200.build`); "
+            "this package has no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, sz = C.c_void_p, C.c_int64, C.c_size_t
+    pi64 = C.POINTER(C.c_int64)
+    proto = {
+        "axb_version": (C.c_int, []),
+        "axb_status_name": (C.c_char_p, [C.c_int]),
+        "axb_ctx_create": (C.c_int, [C.POINTER(vp), C.c_int]),
+        "axb_ctx_destroy": (None, [vp]),
+        "axb_ctx_set_stream": (C.c_int, [vp, vp]),
+        "axb_ctx_set_arena": (C.c_int, [vp, vp, sz]),
+        "axb_arena_needed": (sz, [vp]),
+        "axb_arena_used": (sz, [vp]),
+        "axb_arena_hint": (sz, [i64, C.c_double, C.c_double]),
+        "axb_last_message": (C.c_char_p, [vp]),
+        "axb_last_error": (C.c_int, [vp, C.POINTER(C.c_int), pi64, C.POINTER(C.c_int)]),
+        "axb_grid_build": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params)]),
+        "axb_grid_get_info": (C.c_int, [vp, C.POINTER(GridInfo)]),
+        "axb_grid_export": (C.c_int, [vp, vp, vp, vp]),
+        "axb_potential": (C.c_int, [vp, i64, i64]),
+        "axb_potential_counts": (C.c_int, [vp, pi64]),
+        "axb_potential_export": (C.c_int, [vp, C.c_int, vp, vp, vp]),
+        "axb_prune": (C.c_int, [vp]),
+        "axb_canonicalize": (C.c_int, [vp, pi64]),
+        "axb_export": (C.c_int, [vp, vp, vp, vp, vp]),
+        "axb_sync_check": (C.c_int, [vp]),
+        "axb_compute": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params), pi64]),
+        "axb_compute_host": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params), pi64]),
+        "axb_export_host": (C.c_int, [vp, vp, vp, vp, vp]),
+        "axb_stage_ms": (C.c_int, [vp, C.POINTER(C.c_float)]),
+        "axb_kernel_launches": (i64, [vp]),
+        "axb_ortho_batch": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_double, vp, vp, vp]),
+    }
+    for name, (res, args) in proto.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L

@@ -1,0 +1,911 @@
+// alphax_b200.cu -- C-ABI entry points (include/alphax_b200.h) and host-side
+// orchestration of the CUDA kernels.  One translation unit; compile with
+//   nvcc -gencode arch=compute_100a,code=sm_100a -fmad=false -lineinfo ...
+// (-fmad=false is part of the contract: see predicates.cuh).
+#include "../../include/alphax_b200.h"
+
+#include "canon.cuh"
+#include "common.cuh"
+#include "estimate.cuh"
+#include "grid.cuh"
+#include "predicates.cuh"
+#include "prune.cuh"
+#include "scan.cuh"
+
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+
+using namespace axb;
+
+namespace {
+
+constexpr size_t ARENA_ALIGN = 256;
+constexpr int64_t MAX_CELLS = (int64_t)1 << 31;   // dense cell table limit (uint32 keys, 8 GiB of table)
+
+struct HostBlock {            // pinned; filled by async copies
+    Counters ctr;
+    BoundsPartial bounds;
+    uint32_t totals[4];
+    ErrRecord errs[ERR_CAP];
+    int2 dups[DUP_CAP];
+};
+
+enum State { S_NONE = 0, S_GRID = 1, S_POTENTIAL = 2, S_PRUNED = 3, S_CANON = 4 };
+
+}  // namespace
+
+struct axb_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    char *arena = nullptr;
+    size_t arena_bytes = 0, arena_used = 0, arena_needed = 0;
+    HostBlock *h = nullptr;
+    int state = S_NONE;
+    int last_status = AXB_OK;
+    int64_t err_verts[4] = {-1, -1, -1, -1};
+    int err_nverts = 0;
+    char msg[512] = {0};
+    int64_t launches = 0;
+    cudaEvent_t ev[AXB_ST_COUNT + 2] = {};      // stage boundaries 0..EXPORT, then export begin/end
+    bool ev_set[AXB_ST_COUNT + 2] = {};
+    float stage_ms[AXB_ST_COUNT] = {};
+
+    // run
+    axb_params prm = {};
+    int64_t n = 0;
+    const double *d_xyz = nullptr, *d_radii = nullptr;
+    axb_grid_info ginfo = {};
+    GridView g = {};
+    Tol tol = {};
+    int rank_lo = 0, rank_hi = 0;
+    // device arrays (arena)
+    Counters *ctr = nullptr;
+    ErrRecord *errs = nullptr;
+    int2 *dups = nullptr;
+    int *key_of_ball = nullptr, *key_of_rank = nullptr, *orig = nullptr, *rank = nullptr;
+    uint32_t *cell_start = nullptr;
+    Atom *atoms = nullptr;
+    double *reach = nullptr;
+    uint32_t *adj_off = nullptr;
+    int *deg = nullptr, *pe_u = nullptr, *pe_v = nullptr;
+    uint32_t pe_cap = 0, pt_cap = 0, pq_cap = 0;
+    int4 *pt = nullptr, *pq_r = nullptr;
+    int *pq_l = nullptr;
+    int W = 1;
+    unsigned long long *trimask = nullptr;
+    unsigned int *eflag = nullptr;
+    unsigned char *vflag = nullptr;
+    int4 *k3 = nullptr;
+    uint32_t *cnt1 = nullptr, *cnt2 = nullptr, *cnt3 = nullptr, *vkeep = nullptr;
+    uint32_t *off1 = nullptr, *off2 = nullptr, *off3 = nullptr, *voff = nullptr;
+    int2 *tmp1 = nullptr;
+    int4 *tmp2 = nullptr, *tmp3 = nullptr;
+    uint32_t n_pe = 0, n_pt = 0, n_pq = 0;
+    int64_t counts[4] = {0, 0, 0, 0};
+    size_t mark_after_grid = 0, mark_after_edges = 0;
+};
+
+namespace {
+
+int fail(axb_ctx *c, int status, const char *fmt, ...) __attribute__((format(printf, 3, 4)));
+int fail(axb_ctx *c, int status, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(c->msg, sizeof(c->msg), fmt, ap);
+    va_end(ap);
+    c->last_status = status;
+    return status;
+}
+
+#define CUDA_TRY(c, expr)                                                                           \
+    do {                                                                                            \
+        cudaError_t e_ = (expr);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail((c), AXB_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                        \
+    } while (0)
+
+#define LAUNCH_CHECK(c)                                                                                        \
+    do {                                                                                                       \
+        (c)->launches++;                                                                                       \
+        cudaError_t e_ = cudaGetLastError();                                                                   \
+        if (e_ != cudaSuccess)                                                                                 \
+            return fail((c), AXB_ERR_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                                             \
+    } while (0)
+
+template <class T>
+T *arena_alloc(axb_ctx *c, size_t count) {
+    size_t bytes = (count * sizeof(T) + ARENA_ALIGN - 1) / ARENA_ALIGN * ARENA_ALIGN;
+    if (bytes == 0) bytes = ARENA_ALIGN;
+    size_t want = c->arena_used + bytes;
+    if (want > c->arena_needed) c->arena_needed = want;
+    if (want > c->arena_bytes || c->arena == nullptr) return nullptr;
+    T *p = reinterpret_cast<T *>(c->arena + c->arena_used);
+    c->arena_used = want;
+    return p;
+}
+
+#define ARENA(c, ptr, T, count)                                                                         \
+    do {                                                                                                \
+        (ptr) = arena_alloc<T>((c), (count));                                                           \
+        if (!(ptr))                                                                                     \
+            return fail((c), AXB_ERR_ARENA, "scratch arena too small: need at least %zu bytes, have %zu", \
+                        (c)->arena_needed, (c)->arena_bytes);                                           \
+    } while (0)
+
+inline unsigned blocks_for(size_t items, int threads) { return (unsigned)std::max<size_t>(1, (items + threads - 1) / threads); }
+
+int mark_event(axb_ctx *c, int idx) {
+    CUDA_TRY(c, cudaEventRecord(c->ev[idx], c->stream));
+    c->ev_set[idx] = true;
+    return AXB_OK;
+}
+
+// exclusive scan of n uint32 (out has n + 1 entries, may alias in)
+int device_scan(axb_ctx *c, const uint32_t *in, size_t n, uint32_t *out) {
+    size_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (ntiles == 0) ntiles = 1;
+    uint32_t *sums;
+    ARENA(c, sums, uint32_t, ntiles + 1);
+    k_scan_tile_sums<<<(unsigned)ntiles, SCAN_THREADS, 0, c->stream>>>(in, n, sums);
+    LAUNCH_CHECK(c);
+    k_scan_of_sums<<<1, SCAN_THREADS, 0, c->stream>>>(sums, ntiles);
+    LAUNCH_CHECK(c);
+    k_scan_apply<<<(unsigned)ntiles, SCAN_THREADS, 0, c->stream>>>(in, n, sums, out);
+    LAUNCH_CHECK(c);
+    return AXB_OK;
+}
+
+int fetch_counters(axb_ctx *c) {
+    CUDA_TRY(c, cudaMemcpyAsync(&c->h->ctr, c->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return AXB_OK;
+}
+
+// counting sort of the balls by cell key + rank-space records (grid.cuh)
+int bin_balls(axb_ctx *c, double side, const double lo[3], const double hi[3]) {
+    const int n = (int)c->n;
+    int64_t dims[3];
+    for (int a = 0; a < 3; ++a) dims[a] = (int64_t)floor((hi[a] - lo[a]) / side) + 1;   // grid.py:121
+    // dims are at least 1; guard the product before multiplying
+    long double cells = (long double)dims[0] * (long double)dims[1] * (long double)dims[2];
+    if (cells >= (long double)MAX_CELLS)
+        return fail(c, AXB_ERR_GRID_TOO_LARGE,
+                    "grid of %lld x %lld x %lld cells exceeds the dense cell table limit (%lld cells)", (long long)dims[0],
+                    (long long)dims[1], (long long)dims[2], (long long)MAX_CELLS);
+    const int64_t G = dims[0] * dims[1] * dims[2];
+    c->ginfo.cell_side = side;
+    for (int a = 0; a < 3; ++a) { c->ginfo.origin[a] = lo[a]; c->ginfo.dims[a] = dims[a]; }
+    c->ginfo.n_cells = G;
+    c->ginfo.n_balls = c->n;
+    GridView &g = c->g;
+    g.ox = lo[0]; g.oy = lo[1]; g.oz = lo[2];
+    g.side = side;
+    g.dx = (int)dims[0]; g.dy = (int)dims[1]; g.dz = (int)dims[2];
+    g.n = n;
+
+    uint32_t *cell_count;
+    int *arrival;
+    ARENA(c, c->key_of_ball, int, n);
+    ARENA(c, c->cell_start, uint32_t, (size_t)G + 2);
+    ARENA(c, c->orig, int, n);
+    ARENA(c, c->rank, int, n);
+    ARENA(c, c->key_of_rank, int, n);
+    ARENA(c, c->atoms, Atom, n);
+    ARENA(c, c->reach, double, n);
+    const size_t mark = c->arena_used;          // everything below is scratch of this function
+    ARENA(c, cell_count, uint32_t, (size_t)G + 2);
+    ARENA(c, arrival, int, n);
+    g.cell_start = c->cell_start;
+
+    CUDA_TRY(c, cudaMemsetAsync(cell_count, 0, ((size_t)G + 2) * sizeof(uint32_t), c->stream));
+    k_cell_keys<<<blocks_for(n, 256), 256, 0, c->stream>>>(c->d_xyz, g, c->key_of_ball, cell_count);
+    LAUNCH_CHECK(c);
+    int st = device_scan(c, cell_count, (size_t)G + 1, c->cell_start);
+    if (st != AXB_OK) return st;
+    k_cell_scatter<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->key_of_ball, c->cell_start, cell_count, arrival);
+    LAUNCH_CHECK(c);
+    k_cell_finalize<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->d_xyz, c->d_radii, c->key_of_ball, c->cell_start,
+                                                             arrival, c->prm.alpha, c->prm.eps_abs, c->orig, c->rank,
+                                                             c->key_of_rank, c->atoms, c->reach, c->ctr, c->dups);
+    LAUNCH_CHECK(c);
+    // the scratch is dead once the stream has passed k_cell_finalize; later stages
+    // are ordered on the same stream, so it can be handed out again
+    c->arena_used = mark;
+    return AXB_OK;
+}
+
+// pick the duplicate pair the reference reports (pipeline.py:238-244): first adjacent equal
+// pair in lexsort (x, y, z) order == smallest centre, then the two smallest ball indices.
+int report_duplicate(axb_ctx *c, unsigned ndup) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->h->dups, c->dups, sizeof(int2) * std::min<unsigned>(ndup, DUP_CAP),
+                                cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    unsigned m = std::min<unsigned>(ndup, DUP_CAP);
+    int best = -1;
+    double bx[3] = {0, 0, 0};
+    for (unsigned q = 0; q < m; ++q) {
+        double p[3];
+        CUDA_TRY(c, cudaMemcpy(p, c->d_xyz + 3 * (size_t)c->h->dups[q].x, sizeof(p), cudaMemcpyDeviceToHost));
+        bool better = best < 0;
+        if (!better) {
+            if (p[0] != bx[0]) better = p[0] < bx[0];
+            else if (p[1] != bx[1]) better = p[1] < bx[1];
+            else if (p[2] != bx[2]) better = p[2] < bx[2];
+            else better = c->h->dups[q].x < c->h->dups[best].x;
+        }
+        if (better) { best = (int)q; bx[0] = p[0]; bx[1] = p[1]; bx[2] = p[2]; }
+    }
+    c->err_verts[0] = c->h->dups[best].x;
+    c->err_verts[1] = c->h->dups[best].y;
+    c->err_nverts = 2;
+    return fail(c, AXB_ERR_DUPLICATE, "balls %lld and %lld share the center (%.17g, %.17g, %.17g)",
+                (long long)c->err_verts[0], (long long)c->err_verts[1], bx[0], bx[1], bx[2]);
+}
+
+EstParams est_params(axb_ctx *c, unsigned long long report_key) {
+    EstParams P;
+    P.g = c->g; P.tol = c->tol;
+    P.atoms = c->atoms; P.reach = c->reach; P.orig = c->orig; P.key_of_rank = c->key_of_rank;
+    P.adj_off = c->adj_off; P.deg = c->deg; P.pe_v = c->pe_v; P.pe_u = c->pe_u; P.pe_cap = c->pe_cap;
+    P.pt = c->pt; P.pt_cap = c->pt_cap; P.pq_r = c->pq_r; P.pq_l = c->pq_l; P.pq_cap = c->pq_cap;
+    P.ctr = c->ctr; P.errs = c->errs; P.report_key = report_key;
+    return P;
+}
+
+PruneParams prune_params(axb_ctx *c) {
+    PruneParams P;
+    P.g = c->g; P.tol = c->tol;
+    P.atoms = c->atoms; P.orig = c->orig; P.adj_off = c->adj_off; P.deg = c->deg;
+    P.pe_u = c->pe_u; P.pe_v = c->pe_v; P.pt = c->pt; P.pq_r = c->pq_r; P.pq_l = c->pq_l;
+    P.pt_cap = c->pt_cap; P.pq_cap = c->pq_cap; P.pe_cap = c->pe_cap;
+    P.W = c->W; P.trimask = c->trimask; P.eflag = c->eflag; P.vflag = c->vflag; P.k3 = c->k3;
+    P.cnt1 = c->cnt1; P.cnt2 = c->cnt2; P.cnt3 = c->cnt3; P.vkeep = c->vkeep;
+    P.ctr = c->ctr; P.biomolecule = c->prm.biomolecule;
+    return P;
+}
+
+int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
+    EstParams P = est_params(c, report_key);
+    const int ngen = c->rank_hi - c->rank_lo;
+    const unsigned ntiles = (unsigned)((ngen + EST_TILE - 1) / EST_TILE);
+    if (c->W == 1) {
+        size_t smem = sizeof(TriWarpSmem<1>) * 8;
+        CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        unsigned grid = std::max(1u, std::min(ntiles, (unsigned)c->sm_count * 3u));
+        k_tri_tet<1><<<grid, 256, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
+    } else {
+        size_t smem = sizeof(TriWarpSmem<4>) * 4;
+        CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        unsigned grid = std::max(1u, std::min(ntiles, (unsigned)c->sm_count));
+        k_tri_tet<4><<<grid, 128, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
+    }
+    LAUNCH_CHECK(c);
+    return AXB_OK;
+}
+
+// turn the smallest singular key into the reference's DegenerateSimplex report
+int report_degenerate(axb_ctx *c) {
+    const unsigned long long key = c->h->ctr.err_key;
+    unsigned m = std::min<unsigned>(c->h->ctr.err_count, ERR_CAP);
+    CUDA_TRY(c, cudaMemcpyAsync(c->h->errs, c->errs, sizeof(ErrRecord) * std::max(1u, m), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    const ErrRecord *hit = nullptr;
+    for (unsigned q = 0; q < m && !hit; ++q)
+        if (c->h->errs[q].key == key) hit = &c->h->errs[q];
+    if (!hit) {
+        // more singular solves than record slots: replay the stage with only `key` reporting
+        const int stage = (int)(key >> 60);
+        if (stage == ST_EDGE) {
+            EstParams P = est_params(c, key);
+            P.pe_cap = 0;    // count only
+            const unsigned ntiles = (unsigned)((c->rank_hi - c->rank_lo + EST_TILE - 1) / EST_TILE);
+            k_edges<<<std::max(1u, std::min(ntiles, (unsigned)c->sm_count * 4u)), EST_WARPS * 32, 0, c->stream>>>(
+                P, c->rank_lo, c->rank_hi);
+            LAUNCH_CHECK(c);
+        } else {
+            uint32_t pt_cap = c->pt_cap, pq_cap = c->pq_cap;
+            c->pt_cap = 0; c->pq_cap = 0;
+            int st = launch_tri_tet(c, key);
+            c->pt_cap = pt_cap; c->pq_cap = pq_cap;
+            if (st != AXB_OK) return st;
+        }
+        CUDA_TRY(c, cudaMemcpyAsync(c->h->errs, c->errs, sizeof(ErrRecord), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        hit = &c->h->errs[0];
+    }
+    c->err_nverts = hit->nverts;
+    for (int a = 0; a < 4; ++a) c->err_verts[a] = a < hit->nverts ? hit->verts[a] : -1;
+    static const char *what[] = {"simplex", "edge", "edge", "triangle", "tetrahedron"};
+    const int stage = (int)(key >> 60);
+    char vs[128];
+    int w = 0;
+    for (int a = 0; a < hit->nverts; ++a) w += snprintf(vs + w, sizeof(vs) - w, a ? ", %d" : "%d", hit->verts[a]);
+    return fail(c, AXB_ERR_DEGENERATE, "%s (%s) has affinely dependent centers", what[stage <= 4 ? stage : 0], vs);
+}
+
+int check_run_flags(axb_ctx *c) {
+    const Counters &k = c->h->ctr;
+    if (k.err_key != ~0ull) return report_degenerate(c);
+    if (k.overflow & 1u)
+        return fail(c, AXB_ERR_DENSITY, "a ball has more than %d potential-edge partners", AXB_MAX_PARTNERS);
+    if (k.overflow & (1u << 3))
+        return fail(c, AXB_ERR_INTERNAL,
+                    "%u inherited faces have no row in their generator's partner list (cell-boundary corner case)",
+                    k.lookup_miss);
+    if (k.overflow & (1u << 5)) return fail(c, AXB_ERR_INTERNAL, "duplicate simplex inside an owner bucket");
+    return AXB_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+
+extern "C" int axb_version(void) { return 100; }
+
+extern "C" const char *axb_status_name(int s) {
+    static const char *names[] = {"AXB_OK", "AXB_ERR_BAD_ARG", "AXB_ERR_CUDA", "AXB_ERR_ARENA", "AXB_ERR_EMPTY",
+                                  "AXB_ERR_NONFINITE", "AXB_ERR_DUPLICATE", "AXB_ERR_DEGENERATE", "AXB_ERR_BAD_SIDE",
+                                  "AXB_ERR_GRID_TOO_LARGE", "AXB_ERR_DENSITY", "AXB_ERR_STATE", "AXB_ERR_INTERNAL"};
+    return (s >= 0 && s <= AXB_ERR_INTERNAL) ? names[s] : "AXB_ERR_UNKNOWN";
+}
+
+extern "C" int axb_ctx_create(axb_ctx **out, int device) {
+    if (!out) return AXB_ERR_BAD_ARG;
+    *out = nullptr;
+    axb_ctx *c = new (std::nothrow) axb_ctx();
+    if (!c) return AXB_ERR_INTERNAL;
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void **>(&c->h), sizeof(HostBlock), cudaHostAllocDefault);
+    for (int i = 0; e == cudaSuccess && i < AXB_ST_COUNT + 2; ++i) e = cudaEventCreate(&c->ev[i]);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "axb_ctx_create: %s\n", cudaGetErrorString(e));
+        delete c;
+        return AXB_ERR_CUDA;
+    }
+    *out = c;
+    return AXB_OK;
+}
+
+extern "C" void axb_ctx_destroy(axb_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (int i = 0; i < AXB_ST_COUNT + 2; ++i)
+        if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->h) cudaFreeHost(c->h);
+    delete c;
+}
+
+extern "C" int axb_ctx_set_stream(axb_ctx *c, void *s) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    c->stream = reinterpret_cast<cudaStream_t>(s);
+    return AXB_OK;
+}
+
+extern "C" int axb_ctx_set_arena(axb_ctx *c, void *p, size_t bytes) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (reinterpret_cast<uintptr_t>(p) % ARENA_ALIGN) return fail(c, AXB_ERR_BAD_ARG, "arena must be %zu-byte aligned", ARENA_ALIGN);
+    c->arena = static_cast<char *>(p);
+    c->arena_bytes = bytes;
+    c->arena_used = 0;
+    c->arena_needed = 0;
+    c->state = S_NONE;
+    return AXB_OK;
+}
+
+extern "C" size_t axb_arena_needed(const axb_ctx *c) { return c ? c->arena_needed : 0; }
+extern "C" size_t axb_arena_used(const axb_ctx *c) { return c ? c->arena_used : 0; }
+
+extern "C" size_t axb_arena_hint(int64_t n, double alpha, double r_max) {
+    // ~ one cell per ball at protein density plus the per-simplex lists; alpha widens everything
+    double widen = 1.0;
+    if (r_max > 0.0 && alpha > 0.0) widen = pow(1.0 + alpha / (r_max * r_max), 1.5);
+    double per_atom = 900.0 + 1400.0 * widen * widen;
+    double bytes = 64.0 * 1024 * 1024 + per_atom * (double)(n > 0 ? n : 1);
+    return (size_t)bytes;
+}
+
+extern "C" const char *axb_last_message(const axb_ctx *c) { return c ? c->msg : "null context"; }
+
+extern "C" int axb_last_error(const axb_ctx *c, int *status, int64_t verts[4], int *nverts) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (status) *status = c->last_status;
+    if (verts) for (int a = 0; a < 4; ++a) verts[a] = c->err_verts[a];
+    if (nverts) *nverts = c->err_nverts;
+    return AXB_OK;
+}
+
+extern "C" int64_t axb_kernel_launches(const axb_ctx *c) { return c ? c->launches : 0; }
+
+extern "C" int axb_stage_ms(const axb_ctx *cc, float out[AXB_ST_COUNT]) {
+    axb_ctx *c = const_cast<axb_ctx *>(cc);
+    if (!c || !out) return AXB_ERR_BAD_ARG;
+    for (int i = 0; i < AXB_ST_COUNT; ++i) {
+        out[i] = 0.f;
+        // stages 0..CANONICAL are delimited by ev[i], ev[i+1]; EXPORT by its own pair
+        const int a = i == AXB_ST_EXPORT ? AXB_ST_COUNT : i, b = a + 1;
+        if (c->ev_set[a] && c->ev_set[b]) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]) == cudaSuccess) out[i] = ms;
+        }
+    }
+    return AXB_OK;
+}
+
+// --------------------------------------------------------------------- grid
+
+extern "C" int axb_grid_build(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *prm) {
+    if (!c || !prm) return AXB_ERR_BAD_ARG;
+    c->state = S_NONE;
+    c->last_status = AXB_OK;
+    c->msg[0] = 0;
+    c->err_nverts = 0;
+    for (int a = 0; a < 4; ++a) c->err_verts[a] = -1;
+    for (int i = 0; i < AXB_ST_COUNT + 2; ++i) c->ev_set[i] = false;
+    c->arena_used = 0;
+    c->arena_needed = 0;
+    if (n <= 0) return fail(c, AXB_ERR_EMPTY, "at least one ball is required");
+    if (n >= ((int64_t)1 << 31) - 1) return fail(c, AXB_ERR_BAD_ARG, "more than 2^31 - 2 balls are not supported");
+    if (!d_xyz || !d_radii) return fail(c, AXB_ERR_BAD_ARG, "null input pointer");
+    if (!(prm->eps_abs > 0.0) || !(prm->eps_singular > 0.0) || !isfinite(prm->alpha))
+        return fail(c, AXB_ERR_BAD_ARG, "alpha must be finite and tolerances strictly positive");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    c->prm = *prm;
+    c->n = n;
+    c->d_xyz = d_xyz;
+    c->d_radii = d_radii;
+    c->tol.eps_abs = prm->eps_abs;
+    c->tol.eps_sing = prm->eps_singular;
+    c->tol.lim_a = prm->alpha + prm->eps_abs;
+
+    int st = mark_event(c, AXB_ST_GRID);
+    if (st != AXB_OK) return st;
+    ARENA(c, c->ctr, Counters, 1);
+    ARENA(c, c->errs, ErrRecord, ERR_CAP);
+    ARENA(c, c->dups, int2, DUP_CAP);
+    const unsigned nb = std::max(1u, std::min(blocks_for((size_t)n, BOUNDS_THREADS), (unsigned)c->sm_count * 4u));
+    BoundsPartial *partials, *bres;
+    unsigned int *done;
+    ARENA(c, partials, BoundsPartial, nb);
+    ARENA(c, bres, BoundsPartial, 1);
+    ARENA(c, done, unsigned int, 1);
+    memset(&c->h->ctr, 0, sizeof(Counters));
+    c->h->ctr.err_key = ~0ull;
+    c->h->ctr.first_bad = 0xffffffffu;
+    CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(done, 0, sizeof(unsigned int), c->stream));
+    k_bounds<<<nb, BOUNDS_THREADS, 0, c->stream>>>(d_xyz, d_radii, (int)n, partials, done, bres);
+    LAUNCH_CHECK(c);
+    CUDA_TRY(c, cudaMemcpyAsync(&c->h->bounds, bres, sizeof(BoundsPartial), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    const BoundsPartial &b = c->h->bounds;
+    if (b.first_bad != 0xffffffffu) {                     // pipeline.py:235-237
+        c->err_verts[0] = b.first_bad;
+        c->err_nverts = 1;
+        return fail(c, AXB_ERR_NONFINITE, "ball %u is not finite", b.first_bad);
+    }
+    const double side_sq = b.rmax * b.rmax + prm->alpha;   // grid.py:112-113
+    const bool bad_side = !(side_sq > 0.0);
+    double side = bad_side ? 0.0 : sqrt(side_sq);          // grid.py:118
+    if (bad_side) {
+        // the reference validates duplicates BEFORE it looks at the cell side (pipeline.py:583 then 594),
+        // so bin with a stand-in side just to find them
+        double span = std::max(b.hi[0] - b.lo[0], std::max(b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]));
+        side = span > 0.0 ? span / 128.0 : 1.0;
+    }
+    st = bin_balls(c, side, b.lo, b.hi);
+    if (st != AXB_OK) return st;
+    st = fetch_counters(c);
+    if (st != AXB_OK) return st;
+    if (c->h->ctr.dup_count) return report_duplicate(c, c->h->ctr.dup_count);
+    if (bad_side)
+        return fail(c, AXB_ERR_BAD_SIDE, "alpha=%.17g gives non-positive squared cell side (r_max=%.17g)", prm->alpha, b.rmax);
+    st = mark_event(c, AXB_ST_GRID + 1);
+    if (st != AXB_OK) return st;
+    c->mark_after_grid = c->arena_used;
+    c->state = S_GRID;
+    return AXB_OK;
+}
+
+extern "C" int axb_grid_get_info(const axb_ctx *c, axb_grid_info *out) {
+    if (!c || !out) return AXB_ERR_BAD_ARG;
+    if (c->state < S_GRID) return AXB_ERR_STATE;
+    *out = c->ginfo;
+    return AXB_OK;
+}
+
+extern "C" int axb_grid_export(axb_ctx *c, int64_t *d_order, int64_t *d_rank, int64_t *d_cells) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (c->state < S_GRID) return fail(c, AXB_ERR_STATE, "axb_grid_export before axb_grid_build");
+    k_grid_export<<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>((int)c->n, c->orig, c->rank, c->key_of_ball,
+                                                                       d_order, d_rank, d_cells);
+    LAUNCH_CHECK(c);
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return AXB_OK;
+}
+
+// ---------------------------------------------------------------- potential
+
+namespace {
+
+int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool sync_at_end) {
+    if (c->state < S_GRID) return fail(c, AXB_ERR_STATE, "axb_potential before axb_grid_build");
+    if (lo < 0 || hi > c->n || lo > hi) return fail(c, AXB_ERR_BAD_ARG, "bad rank range");
+    c->state = S_GRID;
+    c->arena_used = c->mark_after_grid;
+    c->rank_lo = (int)lo;
+    c->rank_hi = (int)hi;
+    const int n = (int)c->n;
+    const int ngen = (int)(hi - lo);
+    int st;
+    memset(&c->h->ctr, 0, sizeof(Counters));
+    c->h->ctr.err_key = ~0ull;
+    c->h->ctr.first_bad = 0xffffffffu;
+    CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
+    if ((st = mark_event(c, AXB_ST_POT_EDGES)) != AXB_OK) return st;
+    ARENA(c, c->adj_off, uint32_t, n);
+    ARENA(c, c->deg, int, n);
+    const size_t mark_pe = c->arena_used;
+    const unsigned ntiles = (unsigned)std::max(1, (ngen + EST_TILE - 1) / EST_TILE);
+    uint64_t want = (uint64_t)16 * (uint64_t)ngen + 4096;
+    for (int attempt = 0;; ++attempt) {
+        if (want > 0xfffffff0ull) return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential edges");
+        c->arena_used = mark_pe;
+        c->pe_cap = (uint32_t)want;
+        ARENA(c, c->pe_v, int, c->pe_cap);
+        ARENA(c, c->pe_u, int, c->pe_cap);
+        CUDA_TRY(c, cudaMemsetAsync(c->deg, 0, sizeof(int) * (size_t)n, c->stream));
+        if (attempt) {   // reset the counters the first attempt touched
+            c->h->ctr.n_pe = 0; c->h->ctr.max_deg = 0; c->h->ctr.pair_bound = 0; c->h->ctr.overflow = 0;
+            c->h->ctr.err_key = ~0ull; c->h->ctr.err_count = 0;
+            CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
+        }
+        EstParams P = est_params(c, 0);
+        k_edges<<<std::max(1u, std::min(ntiles, (unsigned)c->sm_count * 4u)), EST_WARPS * 32, 0, c->stream>>>(P, c->rank_lo, c->rank_hi);
+        LAUNCH_CHECK(c);
+        st = fetch_counters(c);
+        if (st != AXB_OK) return st;
+        if (c->h->ctr.n_pe <= c->pe_cap) break;
+        if (attempt >= 2) return fail(c, AXB_ERR_INTERNAL, "potential-edge buffer still too small after resize");
+        want = (uint64_t)c->h->ctr.n_pe + 1024;
+    }
+    st = mark_event(c, AXB_ST_POT_EDGES + 1);
+    if (st != AXB_OK) return st;
+    // singular edges are raised before any triangle is looked at (pipeline.py:357)
+    st = check_run_flags(c);
+    if (st != AXB_OK) return st;
+    c->n_pe = c->h->ctr.n_pe;
+    c->W = c->h->ctr.max_deg <= 64 ? 1 : 4;
+    c->mark_after_edges = c->arena_used;
+
+    uint64_t pt_want = c->h->ctr.pair_bound + 32;           // every potential triangle is a partner pair
+    uint64_t pq_want = c->h->ctr.pair_bound / 2 + 4096;     // first guess; re-run on overflow
+    for (int attempt = 0;; ++attempt) {
+        if (pt_want > 0xfffffff0ull || pq_want > 0xfffffff0ull)
+            return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential triangles or tetrahedra");
+        c->arena_used = c->mark_after_edges;
+        c->pt_cap = (uint32_t)pt_want;
+        c->pq_cap = (uint32_t)pq_want;
+        ARENA(c, c->pt, int4, c->pt_cap);
+        ARENA(c, c->pq_r, int4, c->pq_cap);
+        ARENA(c, c->pq_l, int, c->pq_cap);
+        if (attempt) {
+            c->h->ctr.n_pt = 0; c->h->ctr.n_pq = 0; c->h->ctr.overflow = 0;
+            c->h->ctr.err_key = ~0ull; c->h->ctr.err_count = 0;
+            CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
+        }
+        st = launch_tri_tet(c, 0);
+        if (st != AXB_OK) return st;
+        if (!sync_at_end && attempt == 0) {
+            // optimistic path of axb_compute: overflow and singular flags are checked at the next sync
+            break;
+        }
+        st = fetch_counters(c);
+        if (st != AXB_OK) return st;
+        if (c->h->ctr.n_pq <= c->pq_cap && c->h->ctr.n_pt <= c->pt_cap) break;
+        if (attempt >= 2) return fail(c, AXB_ERR_INTERNAL, "potential-tet buffer still too small after resize");
+        pq_want = (uint64_t)c->h->ctr.n_pq + 1024;
+        pt_want = std::max<uint64_t>(pt_want, (uint64_t)c->h->ctr.n_pt + 32);
+    }
+    st = mark_event(c, AXB_ST_POT_TRIANGLES + 1);
+    if (st != AXB_OK) return st;
+    st = mark_event(c, AXB_ST_POT_TETS + 1);     // triangles and tets are one fused kernel
+    if (st != AXB_OK) return st;
+    if (sync_at_end) {
+        st = check_run_flags(c);
+        if (st != AXB_OK) return st;
+        c->n_pt = c->h->ctr.n_pt;
+        c->n_pq = c->h->ctr.n_pq;
+    }
+    c->state = S_POTENTIAL;
+    return AXB_OK;
+}
+
+int run_prune(axb_ctx *c) {
+    if (c->state < S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_prune before axb_potential");
+    const int n = (int)c->n;
+    ARENA(c, c->trimask, unsigned long long, (size_t)std::max<uint32_t>(c->n_pe, 1) * c->W);
+    ARENA(c, c->eflag, unsigned int, std::max<uint32_t>(c->n_pe, 1));
+    ARENA(c, c->vflag, unsigned char, n);
+    ARENA(c, c->k3, int4, std::max<uint32_t>(c->pq_cap, 1));
+    ARENA(c, c->cnt1, uint32_t, (size_t)n + 1);
+    ARENA(c, c->cnt2, uint32_t, (size_t)n + 1);
+    ARENA(c, c->cnt3, uint32_t, (size_t)n + 1);
+    ARENA(c, c->vkeep, uint32_t, (size_t)n + 1);
+    CUDA_TRY(c, cudaMemsetAsync(c->trimask, 0, sizeof(unsigned long long) * (size_t)std::max<uint32_t>(c->n_pe, 1) * c->W, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->eflag, 0, sizeof(unsigned int) * std::max<uint32_t>(c->n_pe, 1), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->vflag, 0, (size_t)n, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->cnt1, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->cnt2, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->cnt3, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->vkeep, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(&c->ctr->n_k3, 0, sizeof(unsigned int), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(&c->ctr->lookup_miss, 0, sizeof(unsigned int), c->stream));
+    PruneParams P = prune_params(c);
+    const unsigned grid = (unsigned)c->sm_count * 8u;
+    int st;
+    k_prune_tets<<<grid, 256, 0, c->stream>>>(P);
+    LAUNCH_CHECK(c);
+    if ((st = mark_event(c, AXB_ST_PRUNE_TETS + 1)) != AXB_OK) return st;
+    k_prune_tris<<<grid, 256, 0, c->stream>>>(P);
+    LAUNCH_CHECK(c);
+    if ((st = mark_event(c, AXB_ST_PRUNE_TRIANGLES + 1)) != AXB_OK) return st;
+    k_prune_edges<<<grid, 256, 0, c->stream>>>(P);
+    LAUNCH_CHECK(c);
+    if ((st = mark_event(c, AXB_ST_PRUNE_EDGES + 1)) != AXB_OK) return st;
+    const int ngen = c->rank_hi - c->rank_lo;
+    if (ngen > 0) {
+        k_prune_vertices<<<blocks_for((size_t)ngen, 256), 256, 0, c->stream>>>(P, c->rank_lo, c->rank_hi);
+        LAUNCH_CHECK(c);
+    }
+    if ((st = mark_event(c, AXB_ST_PRUNE_VERTICES + 1)) != AXB_OK) return st;
+    c->state = S_PRUNED;
+    return AXB_OK;
+}
+
+int run_canonicalize(axb_ctx *c, int64_t counts[4]) {
+    if (c->state < S_PRUNED) return fail(c, AXB_ERR_STATE, "axb_canonicalize before axb_prune");
+    const size_t n = (size_t)c->n;
+    int st;
+    ARENA(c, c->off1, uint32_t, n + 2);
+    ARENA(c, c->off2, uint32_t, n + 2);
+    ARENA(c, c->off3, uint32_t, n + 2);
+    ARENA(c, c->voff, uint32_t, n + 2);
+    if ((st = device_scan(c, c->cnt1, n, c->off1)) != AXB_OK) return st;
+    if ((st = device_scan(c, c->cnt2, n, c->off2)) != AXB_OK) return st;
+    if ((st = device_scan(c, c->cnt3, n, c->off3)) != AXB_OK) return st;
+    if ((st = device_scan(c, c->vkeep, n, c->voff)) != AXB_OK) return st;
+    CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[0], c->voff + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[1], c->off1 + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[2], c->off2 + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[3], c->off3 + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    if ((st = fetch_counters(c)) != AXB_OK) return st;
+    // deferred checks of the optimistic potential stage
+    if (c->h->ctr.n_pq > c->pq_cap || c->h->ctr.n_pt > c->pt_cap) return AXB_ERR_ARENA + 1000;   // sentinel: caller re-runs
+    if ((st = check_run_flags(c)) != AXB_OK) return st;
+    c->n_pt = c->h->ctr.n_pt;
+    c->n_pq = c->h->ctr.n_pq;
+    for (int d = 0; d < 4; ++d) c->counts[d] = c->h->totals[d];
+    ARENA(c, c->tmp1, int2, std::max<int64_t>(c->counts[1], 1));
+    ARENA(c, c->tmp2, int4, std::max<int64_t>(c->counts[2], 1));
+    ARENA(c, c->tmp3, int4, std::max<int64_t>(c->counts[3], 1));
+    CanonParams P;
+    P.n = (int)n; P.orig = c->orig; P.adj_off = c->adj_off; P.pe_u = c->pe_u; P.pe_v = c->pe_v; P.pe_cap = c->pe_cap;
+    P.W = c->W; P.trimask = c->trimask; P.eflag = c->eflag; P.k3 = c->k3;
+    P.cnt1 = c->cnt1; P.cnt2 = c->cnt2; P.cnt3 = c->cnt3; P.off1 = c->off1; P.off2 = c->off2; P.off3 = c->off3;
+    P.tmp1 = c->tmp1; P.tmp2 = c->tmp2; P.tmp3 = c->tmp3; P.ctr = c->ctr;
+    const unsigned grid = (unsigned)c->sm_count * 8u;
+    k_scatter_edges_tris<<<grid, 256, 0, c->stream>>>(P);
+    LAUNCH_CHECK(c);
+    k_scatter_tets<<<grid, 256, 0, c->stream>>>(P);
+    LAUNCH_CHECK(c);
+    if ((st = mark_event(c, AXB_ST_CANONICAL + 1)) != AXB_OK) return st;
+    if (counts) for (int d = 0; d < 4; ++d) counts[d] = c->counts[d];
+    c->state = S_CANON;
+    return AXB_OK;
+}
+
+}  // namespace
+
+extern "C" int axb_potential(axb_ctx *c, int64_t lo, int64_t hi) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    return run_potential(c, lo, hi, true);
+}
+
+extern "C" int axb_potential_counts(const axb_ctx *c, int64_t counts[3]) {
+    if (!c || !counts) return AXB_ERR_BAD_ARG;
+    if (c->state < S_POTENTIAL) return AXB_ERR_STATE;
+    counts[0] = c->n_pe; counts[1] = c->n_pt; counts[2] = c->n_pq;
+    return AXB_OK;
+}
+
+namespace {
+
+// rows of one potential level as ascending ball indices + recomputed ortho data (generation order)
+__global__ void k_export_potential(int what, unsigned m, const Atom *__restrict__ atoms, const int *__restrict__ orig,
+                                   const int *__restrict__ pe_u, const int *__restrict__ pe_v,
+                                   const int4 *__restrict__ pt, const int4 *__restrict__ pq_r, double eps_sing,
+                                   int64_t *rows, double *centers, double *sizes) {
+    unsigned e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    int r[4] = {-1, -1, -1, -1};
+    int k;
+    if (what == AXB_PE) { r[0] = pe_u[e]; r[1] = pe_v[e]; k = 2; }
+    else if (what == AXB_PT) { int4 q = pt[e]; r[0] = q.x; r[1] = q.y; r[2] = q.z; k = 3; }
+    else { int4 q = pq_r[e]; r[0] = q.x; r[1] = q.y; r[2] = q.z; r[3] = q.w; k = 4; }
+    Atom a[4];
+    int o[4];
+    for (int i = 0; i < k; ++i) { a[i] = load_atom(atoms, r[i]); o[i] = orig[r[i]]; }
+    Ortho res;
+    if (k == 2) res = ortho_edge(o[0], a[0], o[1], a[1], eps_sing);
+    else if (k == 3) res = ortho_tri(o[0], a[0], o[1], a[1], o[2], a[2], eps_sing);
+    else res = ortho_tet(o[0], a[0], o[1], a[1], o[2], a[2], o[3], a[3], eps_sing);
+    for (int x = 1; x < k; ++x)
+        for (int y = x; y > 0 && o[y - 1] > o[y]; --y) { int t = o[y]; o[y] = o[y - 1]; o[y - 1] = t; }
+    if (rows) for (int i = 0; i < k; ++i) rows[(size_t)e * k + i] = o[i];
+    if (centers) { centers[3 * (size_t)e] = res.cx; centers[3 * (size_t)e + 1] = res.cy; centers[3 * (size_t)e + 2] = res.cz; }
+    if (sizes) sizes[e] = res.size;
+}
+
+}  // namespace
+
+extern "C" int axb_potential_export(axb_ctx *c, int what, int64_t *d_rows, double *d_centers, double *d_sizes) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (c->state < S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_potential_export before axb_potential");
+    if (what < AXB_PE || what > AXB_PQ) return fail(c, AXB_ERR_BAD_ARG, "what must be AXB_PE, AXB_PT or AXB_PQ");
+    unsigned m = what == AXB_PE ? c->n_pe : (what == AXB_PT ? c->n_pt : c->n_pq);
+    if (m) {
+        k_export_potential<<<blocks_for(m, 128), 128, 0, c->stream>>>(what, m, c->atoms, c->orig, c->pe_u, c->pe_v, c->pt,
+                                                                      c->pq_r, c->tol.eps_sing, d_rows, d_centers, d_sizes);
+        LAUNCH_CHECK(c);
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return AXB_OK;
+}
+
+extern "C" int axb_prune(axb_ctx *c) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    return run_prune(c);
+}
+
+extern "C" int axb_canonicalize(axb_ctx *c, int64_t counts[4]) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    int st = run_canonicalize(c, counts);
+    if (st == AXB_ERR_ARENA + 1000) return fail(c, AXB_ERR_INTERNAL, "potential buffers overflowed; call axb_potential again");
+    return st;
+}
+
+extern "C" int axb_export(axb_ctx *c, int64_t *d_v, int64_t *d_e, int64_t *d_t, int64_t *d_q) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (c->state < S_CANON) return fail(c, AXB_ERR_STATE, "axb_export before axb_canonicalize");
+    int st;
+    if ((st = mark_event(c, AXB_ST_COUNT)) != AXB_OK) return st;
+    if (d_v) {
+        k_emit_vertices<<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>((int)c->n, c->vkeep, c->voff, d_v);
+        LAUNCH_CHECK(c);
+    }
+    if (d_e && c->counts[1]) {
+        k_emit_edges<<<blocks_for((size_t)c->counts[1], 256), 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->counts[1], d_e, c->ctr);
+        LAUNCH_CHECK(c);
+    }
+    if (d_t && c->counts[2]) {
+        k_emit_tris<<<blocks_for((size_t)c->counts[2], 256), 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->counts[2], d_t, c->ctr);
+        LAUNCH_CHECK(c);
+    }
+    if (d_q && c->counts[3]) {
+        k_emit_tets<<<blocks_for((size_t)c->counts[3], 256), 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->counts[3], d_q, c->ctr);
+        LAUNCH_CHECK(c);
+    }
+    return mark_event(c, AXB_ST_COUNT + 1);
+}
+
+extern "C" int axb_sync_check(axb_ctx *c) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    int st = fetch_counters(c);
+    if (st != AXB_OK) return st;
+    return check_run_flags(c);
+}
+
+extern "C" int axb_compute(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *prm,
+                           int64_t counts[4]) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    int st = axb_grid_build(c, n, d_xyz, d_radii, prm);
+    if (st != AXB_OK) return st;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        st = run_potential(c, 0, n, attempt > 0);
+        if (st != AXB_OK) return st;
+        if (attempt == 0) {        // counts of the optimistic run are not on the host yet; prune sizes by capacity
+            c->n_pt = c->pt_cap;
+            c->n_pq = c->pq_cap;
+        }
+        st = run_prune(c);
+        if (st != AXB_OK) return st;
+        st = run_canonicalize(c, counts);
+        if (st != AXB_ERR_ARENA + 1000) return st;
+        // potential-tet buffer overflowed: second attempt sizes it exactly
+    }
+    return fail(c, AXB_ERR_INTERNAL, "potential buffers overflowed twice");
+}
+
+extern "C" int axb_compute_host(axb_ctx *c, int64_t n, const double *h_xyz, const double *h_radii, const axb_params *prm,
+                                int64_t counts[4]) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (n <= 0) return fail(c, AXB_ERR_EMPTY, "at least one ball is required");
+    if (!h_xyz || !h_radii) return fail(c, AXB_ERR_BAD_ARG, "null input pointer");
+    // inputs live at the END of the arena so the per-run bump allocator never touches them
+    size_t in_bytes = ((size_t)n * 4 * sizeof(double) + ARENA_ALIGN - 1) / ARENA_ALIGN * ARENA_ALIGN;
+    if (!c->arena || c->arena_bytes < in_bytes + ARENA_ALIGN) {
+        c->arena_needed = in_bytes + axb_arena_hint(n, prm ? prm->alpha : 0.0, 1.9);
+        return fail(c, AXB_ERR_ARENA, "scratch arena too small for the input copy");
+    }
+    double *d_in = reinterpret_cast<double *>(c->arena + c->arena_bytes - in_bytes);
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemcpyAsync(d_in, h_xyz, (size_t)n * 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(d_in + 3 * (size_t)n, h_radii, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    const size_t full = c->arena_bytes;
+    c->arena_bytes = full - in_bytes;
+    int st = axb_compute(c, n, d_in, d_in + 3 * (size_t)n, prm, counts);
+    c->arena_bytes = full;
+    if (st == AXB_ERR_ARENA) c->arena_needed += in_bytes;
+    return st;
+}
+
+extern "C" int axb_export_host(axb_ctx *c, int64_t *h_v, int64_t *h_e, int64_t *h_t, int64_t *h_q) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (c->state < S_CANON) return fail(c, AXB_ERR_STATE, "axb_export_host before axb_canonicalize");
+    const size_t mark = c->arena_used;
+    int64_t *d[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t *h[4] = {h_v, h_e, h_t, h_q};
+    for (int k = 0; k < 4; ++k)
+        if (h[k]) ARENA(c, d[k], int64_t, (size_t)std::max<int64_t>(c->counts[k], 1) * (k + 1));
+    int st = axb_export(c, d[0], d[1], d[2], d[3]);
+    if (st != AXB_OK) return st;
+    for (int k = 0; k < 4; ++k)
+        if (h[k] && c->counts[k])
+            CUDA_TRY(c, cudaMemcpyAsync(h[k], d[k], sizeof(int64_t) * (size_t)c->counts[k] * (k + 1), cudaMemcpyDeviceToHost, c->stream));
+    st = axb_sync_check(c);
+    c->arena_used = mark;
+    return st;
+}
+
+// ------------------------------------------------------------------- probes
+
+namespace {
+__global__ void k_ortho_batch(int64_t m, int k, const double *__restrict__ pts, const double *__restrict__ r2,
+                              double eps_sing, double *centers, double *sizes, uint8_t *singular) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= m) return;
+    Atom a[4];
+    for (int i = 0; i < k; ++i) {
+        a[i].x = pts[(s * k + i) * 3]; a[i].y = pts[(s * k + i) * 3 + 1]; a[i].z = pts[(s * k + i) * 3 + 2];
+        a[i].r2 = r2[s * k + i];
+    }
+    Ortho o;
+    if (k == 1) { o.cx = a[0].x; o.cy = a[0].y; o.cz = a[0].z; o.size = -a[0].r2; o.singular = false; }
+    else if (k == 2) o = ortho2(a[0], a[1], eps_sing);
+    else if (k == 3) { Atom p[3] = {a[0], a[1], a[2]}; o = orthoN<3>(p, eps_sing); }
+    else { Atom p[4] = {a[0], a[1], a[2], a[3]}; o = orthoN<4>(p, eps_sing); }
+    centers[3 * s] = o.cx; centers[3 * s + 1] = o.cy; centers[3 * s + 2] = o.cz;
+    sizes[s] = o.size;
+    singular[s] = o.singular ? 1 : 0;
+}
+}  // namespace
+
+extern "C" int axb_ortho_batch(axb_ctx *c, int64_t m, int k, const double *d_pts, const double *d_r2, double eps_sing,
+                               double *d_centers, double *d_sizes, uint8_t *d_singular) {
+    if (!c || k < 1 || k > 4 || m < 0) return AXB_ERR_BAD_ARG;
+    if (m == 0) return AXB_OK;
+    k_ortho_batch<<<blocks_for((size_t)m, 128), 128, 0, c->stream>>>(m, k, d_pts, d_r2, eps_sing, d_centers, d_sizes, d_singular);
+    LAUNCH_CHECK(c);
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return AXB_OK;
+}

@@ -1,0 +1,135 @@
+// canon.cuh -- canonical sort + dedup of the kept simplices
+// (reference pipeline.py:611-614 via _arrays.py:12-16: rows of ascending ball
+// indices, lexicographically sorted, duplicate-free, int64).
+//
+// No global sort: a canonical row starts with its minimum ball index, so rows
+// are bucketed by that "owner".  Bucket sizes were counted while pruning;
+// an exclusive scan turns them into the final row offsets, a scatter drops
+// every kept simplex into its owner's bucket, and a rank-sort inside the
+// (tiny) bucket writes the int64 rows straight to their final position.
+// Each simplex is represented exactly once (a kept-bit / kept-flag / kept-list
+// entry), so there is nothing to deduplicate; an equal pair inside a bucket
+// would be a logic error and is reported.
+#pragma once
+
+#include "common.cuh"
+
+namespace axb {
+
+struct CanonParams {
+    int n;
+    const int *orig;
+    const uint32_t *adj_off;
+    const int *pe_u;
+    const int *pe_v;
+    uint32_t pe_cap;
+    int W;
+    const unsigned long long *trimask;
+    const unsigned int *eflag;
+    const int4 *k3;
+    uint32_t *cnt1, *cnt2, *cnt3;          // consumed as cursors
+    const uint32_t *off1, *off2, *off3;    // (n + 1) exclusive offsets per owner
+    int2 *tmp1;                            // (owner, b)
+    int4 *tmp2;                            // (owner, b, c, -)
+    int4 *tmp3;                            // (owner, b, c, d)
+    Counters *ctr;
+};
+
+__global__ void __launch_bounds__(256) k_scatter_edges_tris(CanonParams P) {
+    const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
+    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pe; e += gridDim.x * blockDim.x) {
+        const int u = __ldg(P.pe_u + e), v = __ldg(P.pe_v + e);
+        const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + v);
+        if (P.eflag[e]) {
+            const int a = min(ou, ov), b = max(ou, ov);
+            const unsigned slot = atomicSub(P.cnt1 + a, 1u) - 1u;
+            P.tmp1[P.off1[a] + slot] = make_int2(a, b);
+        }
+        const unsigned bu = __ldg(P.adj_off + u);
+        for (int w = 0; w < P.W; ++w) {
+            unsigned long long m = P.trimask[(size_t)e * P.W + w];
+            while (m) {
+                const int j = 64 * w + __ffsll((long long)m) - 1;
+                m &= m - 1;
+                const int ow = __ldg(P.orig + __ldg(P.pe_v + bu + j));
+                int a = ou, b = ov, c = ow, t;
+                if (a > b) { t = a; a = b; b = t; }
+                if (b > c) { t = b; b = c; c = t; }
+                if (a > b) { t = a; a = b; b = t; }
+                const unsigned slot = atomicSub(P.cnt2 + a, 1u) - 1u;
+                P.tmp2[P.off2[a] + slot] = make_int4(a, b, c, 0);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_scatter_tets(CanonParams P) {
+    const unsigned n_k3 = P.ctr->n_k3;
+    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_k3; e += gridDim.x * blockDim.x) {
+        const int4 r = P.k3[e];
+        const unsigned slot = atomicSub(P.cnt3 + r.x, 1u) - 1u;
+        P.tmp3[P.off3[r.x] + slot] = r;
+    }
+}
+
+// One thread per bucket entry: its position inside the bucket is the number of
+// smaller entries; write the int64 row there.
+__global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp, const uint32_t *__restrict__ off,
+                                                    unsigned total, int64_t *__restrict__ out, Counters *ctr) {
+    unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= total) return;
+    const int2 me = tmp[s];
+    const unsigned lo = off[me.x], hi = off[me.x + 1];
+    unsigned pos = lo;
+    for (unsigned q = lo; q < hi; ++q) {
+        const int b = tmp[q].y;
+        if (b < me.y) ++pos;
+        else if (b == me.y && q != s) atomicOr(&ctr->overflow, 1u << 5);
+    }
+    out[2 * (size_t)pos] = me.x;
+    out[2 * (size_t)pos + 1] = me.y;
+}
+
+__global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
+                                                   unsigned total, int64_t *__restrict__ out, Counters *ctr) {
+    unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= total) return;
+    const int4 me = tmp[s];
+    const unsigned lo = off[me.x], hi = off[me.x + 1];
+    unsigned pos = lo;
+    for (unsigned q = lo; q < hi; ++q) {
+        const int4 o = tmp[q];
+        if (o.y < me.y || (o.y == me.y && o.z < me.z)) ++pos;
+        else if (o.y == me.y && o.z == me.z && q != s) atomicOr(&ctr->overflow, 1u << 5);
+    }
+    out[3 * (size_t)pos] = me.x;
+    out[3 * (size_t)pos + 1] = me.y;
+    out[3 * (size_t)pos + 2] = me.z;
+}
+
+__global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
+                                                   unsigned total, int64_t *__restrict__ out, Counters *ctr) {
+    unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= total) return;
+    const int4 me = tmp[s];
+    const unsigned lo = off[me.x], hi = off[me.x + 1];
+    unsigned pos = lo;
+    for (unsigned q = lo; q < hi; ++q) {
+        const int4 o = tmp[q];
+        if (o.y < me.y || (o.y == me.y && (o.z < me.z || (o.z == me.z && o.w < me.w)))) ++pos;
+        else if (o.y == me.y && o.z == me.z && o.w == me.w && q != s) atomicOr(&ctr->overflow, 1u << 5);
+    }
+    out[4 * (size_t)pos] = me.x;
+    out[4 * (size_t)pos + 1] = me.y;
+    out[4 * (size_t)pos + 2] = me.z;
+    out[4 * (size_t)pos + 3] = me.w;
+}
+
+__global__ void __launch_bounds__(256) k_emit_vertices(int n, const uint32_t *__restrict__ vkeep,
+                                                       const uint32_t *__restrict__ voff, int64_t *__restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (vkeep[i]) out[voff[i]] = i;
+}
+
+}  // namespace axb

@@ -1,0 +1,88 @@
+// common.cuh -- shared device-side types and warp helpers.
+//
+// Everything on the device lives in "rank space": atoms are stored in the
+// order of the reference's Grid.order (grid.py:128, sorted by (cell key, ball
+// index)), so a cell, a row of cells along x and therefore every (2r+1)^3
+// neighbourhood row is a contiguous range of ranks.  Ball indices of the
+// caller ("orig") only reappear when simplices are emitted.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace axb {
+
+struct __align__(32) Atom {   // one 32-byte sector per atom
+    double x, y, z, r2;
+};
+
+// Device view of the uniform grid (reference grid.py:30-39), dense cell table.
+struct GridView {
+    double ox, oy, oz;        // origin
+    double side;              // cell side sqrt(r_max^2 + alpha)
+    int dx, dy, dz;           // dims
+    int n;                    // balls
+    const uint32_t *cell_start;   // (n_cells + 1) exclusive prefix of per-cell counts
+};
+
+// Scalar run parameters needed by the predicate kernels.
+struct Tol {
+    double lim_a;             // alpha + eps_abs         (pipeline.py:358)
+    double eps_abs;
+    double eps_sing;
+};
+
+// Device-side counters / status block (one per context, zeroed per run).
+struct Counters {
+    unsigned long long err_key;        // min over (stage, generator rank, ordinal) of singular solves
+    unsigned long long pair_bound;     // sum over generators of C(deg, 2)
+    unsigned int n_pe;                 // potential edges
+    unsigned int n_pt;                 // potential triangles
+    unsigned int n_pq;                 // potential tets
+    unsigned int n_k3;                 // kept tets
+    unsigned int max_deg;
+    unsigned int err_count;            // singular records appended
+    unsigned int dup_count;            // duplicate-centre records appended
+    unsigned int overflow;             // bit0: partner cap, bit1: PT cap, bit2: PQ cap, bit3: lookup miss
+    unsigned int first_bad;            // first non-finite ball index (0xffffffff = none)
+    unsigned int lookup_miss;          // inherited faces whose generator row has no such partner
+    unsigned int pad[2];
+};
+
+constexpr int ERR_CAP = 1024;          // singular records kept per run
+constexpr int DUP_CAP = 4096;
+
+struct ErrRecord {
+    unsigned long long key;
+    int verts[4];                      // ball indices ascending, -1 padded
+    int nverts;
+    int pad;
+};
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(FULL, v, o);
+        if (lane_id() >= o) v += t;
+    }
+    return v;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// error key: stage (3 bits) | generator rank (36 bits) | ordinal (24 bits); smaller = raised first
+// by the reference when the whole input is one chunk (pipeline.py:357, 414, 419, 477).
+enum { ST_EDGE = 1, ST_VW = 2, ST_TRI = 3, ST_TET = 4 };
+__device__ __forceinline__ unsigned long long make_err_key(int stage, int gen_rank, unsigned ordinal) {
+    return ((unsigned long long)stage << 60) | ((unsigned long long)(unsigned)gen_rank << 24) | (ordinal & 0xffffffu);
+}
+
+}  // namespace axb

@@ -1,0 +1,218 @@
+// predicates.cuh -- fp64 geometric predicates with the reference's exact
+// operation order (reference geometry.py:122-181, pipeline.py:286-313).
+//
+// Compile with -fmad=false: every multiply/add below is separately rounded.
+// The ONLY fused operations are the explicit fma() calls of the Gram matrix,
+// which reproduce what np.matmul (BLAS) computes at geometry.py:176:
+//     G_ij = fma(D_i.z, D_j.z, fma(D_i.y, D_j.y, D_i.x * D_j.x)).
+// Functions are __host__ __device__ so the same arithmetic can be unit-tested
+// on the CPU against the golden vectors (tests/native/).
+#pragma once
+
+#include "common.cuh"
+
+#include <math.h>
+
+namespace axb {
+
+#define AXB_HD __host__ __device__ __forceinline__
+
+struct Ortho {
+    double cx, cy, cz;   // ortho-centre
+    double size;         // ortho-size
+    bool singular;       // some |pivot| <= eps_singular
+};
+
+// squared distance with the reference's summation order ((dx^2 + dy^2) + dz^2)
+AXB_HD double dist2(const Atom &a, const Atom &b) {
+    double dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+    return (dx * dx + dy * dy) + dz * dz;
+}
+
+// pipeline.py:343-344 / 400-401 / 460-461: reach pre-filter of a pair.
+// reach < 0 encodes "not viable" (pipeline.py:323), which only matters for
+// the edge stage; later stages only ever see viable balls.
+AXB_HD bool reach_pair(const Atom &a, double reach_a, const Atom &b, double reach_b) {
+    double lims = reach_a + reach_b;
+    return dist2(a, b) <= lims * lims;
+}
+
+// k = 2 (geometry.py:161-181 with d = 1).  p0 must be the lower ball index.
+AXB_HD Ortho ortho2(const Atom &p0, const Atom &p1, double eps_sing) {
+    Ortho o;
+    double Dx = p1.x - p0.x, Dy = p1.y - p0.y, Dz = p1.z - p0.z;
+    double g = fma(Dz, Dz, fma(Dy, Dy, Dx * Dx));
+    double a = 2.0 * g;
+    double b = (((Dx * Dx + Dy * Dy) + Dz * Dz) + p0.r2) - p1.r2;
+    o.singular = fabs(a) <= eps_sing;
+    double lam = b / (o.singular ? 1.0 : a);
+    o.cx = p0.x + lam * Dx;
+    o.cy = p0.y + lam * Dy;
+    o.cz = p0.z + lam * Dz;
+    double ex = o.cx - p0.x, ey = o.cy - p0.y, ez = o.cz - p0.z;
+    o.size = ((ex * ex + ey * ey) + ez * ez) - p0.r2;
+    return o;
+}
+
+// Generic d x d partial-pivot solve (geometry.py:122-158), d = 2 or 3, fully
+// unrolled so the matrix stays in registers (row swaps are predicated).
+template <int d>
+AXB_HD bool solve_pp(double (&A)[d][d], double (&b)[d], double (&x)[d], double eps_sing) {
+    bool sing = false;
+#pragma unroll
+    for (int col = 0; col < d; ++col) {
+        int piv = col;                       // first arg-max of |A[r][col]|, r >= col
+        double best = fabs(A[col][col]);
+#pragma unroll
+        for (int r = col + 1; r < d; ++r) {
+            double v = fabs(A[r][col]);
+            if (v > best) { best = v; piv = r; }
+        }
+#pragma unroll
+        for (int r = col + 1; r < d; ++r) {
+            if (piv == r) {
+#pragma unroll
+                for (int c = 0; c < d; ++c) { double t = A[r][c]; A[r][c] = A[col][c]; A[col][c] = t; }
+                double t = b[r]; b[r] = b[col]; b[col] = t;
+            }
+        }
+        double pv = A[col][col];
+        bool bad = fabs(pv) <= eps_sing;
+        sing = sing || bad;
+        double safe = bad ? 1.0 : pv;
+#pragma unroll
+        for (int r = col + 1; r < d; ++r) {
+            double f = A[r][col] / safe;
+#pragma unroll
+            for (int c = col; c < d; ++c) A[r][c] = A[r][c] - f * A[col][c];
+            b[r] = b[r] - f * b[col];
+        }
+    }
+#pragma unroll
+    for (int r = d - 1; r >= 0; --r) {
+        double acc = b[r];
+#pragma unroll
+        for (int c = r + 1; c < d; ++c) acc = acc - A[r][c] * x[c];
+        x[r] = acc / (sing ? 1.0 : A[r][r]);
+    }
+    return sing;
+}
+
+// k = 3 and k = 4.  p[0] must be the lowest ball index, the rest ascending.
+template <int k>
+AXB_HD Ortho orthoN(const Atom (&p)[k], double eps_sing) {
+    constexpr int d = k - 1;
+    double D[d][3], A[d][d], b[d], x[d];
+#pragma unroll
+    for (int i = 0; i < d; ++i) {
+        D[i][0] = p[i + 1].x - p[0].x;
+        D[i][1] = p[i + 1].y - p[0].y;
+        D[i][2] = p[i + 1].z - p[0].z;
+    }
+#pragma unroll
+    for (int i = 0; i < d; ++i)
+#pragma unroll
+        for (int j = i; j < d; ++j) {
+            double g = fma(D[i][2], D[j][2], fma(D[i][1], D[j][1], D[i][0] * D[j][0]));
+            A[i][j] = 2.0 * g;
+            A[j][i] = A[i][j];               // products commute, so the mirror is bit-identical
+        }
+#pragma unroll
+    for (int i = 0; i < d; ++i)
+        b[i] = (((D[i][0] * D[i][0] + D[i][1] * D[i][1]) + D[i][2] * D[i][2]) + p[0].r2) - p[i + 1].r2;
+    Ortho o;
+    o.singular = solve_pp<d>(A, b, x, eps_sing);
+    double sx = x[0] * D[0][0], sy = x[0] * D[0][1], sz = x[0] * D[0][2];
+#pragma unroll
+    for (int i = 1; i < d; ++i) {
+        sx = sx + x[i] * D[i][0];
+        sy = sy + x[i] * D[i][1];
+        sz = sz + x[i] * D[i][2];
+    }
+    o.cx = p[0].x + sx;
+    o.cy = p[0].y + sy;
+    o.cz = p[0].z + sz;
+    double ex = o.cx - p[0].x, ey = o.cy - p[0].y, ez = o.cz - p[0].z;
+    o.size = ((ex * ex + ey * ey) + ez * ez) - p[0].r2;
+    return o;
+}
+
+// conditional swap of (ball index, atom) pairs: sorting network building block
+AXB_HD void cswap(int &ia, Atom &a, int &ib, Atom &b) {
+    if (ia > ib) {
+        int t = ia; ia = ib; ib = t;
+        Atom s = a; a = b; b = s;
+    }
+}
+
+AXB_HD Ortho ortho_edge(int i0, Atom a0, int i1, Atom a1, double eps_sing) {
+    cswap(i0, a0, i1, a1);
+    return ortho2(a0, a1, eps_sing);
+}
+
+AXB_HD Ortho ortho_tri(int i0, Atom a0, int i1, Atom a1, int i2, Atom a2, double eps_sing) {
+    cswap(i0, a0, i1, a1);
+    cswap(i1, a1, i2, a2);
+    cswap(i0, a0, i1, a1);
+    Atom p[3] = {a0, a1, a2};
+    return orthoN<3>(p, eps_sing);
+}
+
+AXB_HD Ortho ortho_tet(int i0, Atom a0, int i1, Atom a1, int i2, Atom a2, int i3, Atom a3, double eps_sing) {
+    cswap(i0, a0, i1, a1);
+    cswap(i2, a2, i3, a3);
+    cswap(i0, a0, i2, a2);
+    cswap(i1, a1, i3, a3);
+    cswap(i1, a1, i2, a2);
+    Atom p[4] = {a0, a1, a2, a3};
+    return orthoN<4>(p, eps_sing);
+}
+
+// grid.py:64-67 / 122-126: clamped cell coordinate of one axis
+AXB_HD int cell_coord(double v, double origin, double side, int dim) {
+    double q = floor((v - origin) / side);
+    // clip in floating point first so absurd values cannot overflow the cast
+    if (!(q > 0.0)) return 0;
+    if (q >= (double)dim) return dim - 1;
+    return (int)q;
+}
+
+#ifdef __CUDACC__
+// pipeline.py:286-313 for one simplex: true iff no non-incident ball of the
+// 27-cell block around the ortho-centre has power distance < size - eps_abs.
+// inc0..inc3 are the RANKS of the incident balls (-1 = unused).
+__device__ __forceinline__ bool ac2_pass(const GridView &g, const Atom *__restrict__ atoms, double cx, double cy,
+                                         double cz, double thr, int inc0, int inc1, int inc2, int inc3) {
+    int ix = cell_coord(cx, g.ox, g.side, g.dx);
+    int iy = cell_coord(cy, g.oy, g.side, g.dy);
+    int iz = cell_coord(cz, g.oz, g.side, g.dz);
+    int x0 = max(ix - 1, 0), x1 = min(ix + 1, g.dx - 1);
+    int y0 = max(iy - 1, 0), y1 = min(iy + 1, g.dy - 1);
+    int z0 = max(iz - 1, 0), z1 = min(iz + 1, g.dz - 1);
+    for (int z = z0; z <= z1; ++z)
+        for (int y = y0; y <= y1; ++y) {
+            int row = g.dx * (y + g.dy * z);
+            int s = (int)__ldg(g.cell_start + row + x0);
+            int e = (int)__ldg(g.cell_start + row + x1 + 1);
+            for (int t = s; t < e; ++t) {
+                if (t == inc0 || t == inc1 || t == inc2 || t == inc3) continue;
+                const double2 *q = reinterpret_cast<const double2 *>(atoms + t);
+                double2 xy = __ldg(q), zr = __ldg(q + 1);
+                double ddx = xy.x - cx, ddy = xy.y - cy, ddz = zr.x - cz;
+                double dp = ((ddx * ddx + ddy * ddy) + ddz * ddz) - zr.y;
+                if (dp < thr) return false;
+            }
+        }
+    return true;
+}
+
+__device__ __forceinline__ Atom load_atom(const Atom *__restrict__ atoms, int t) {
+    const double2 *q = reinterpret_cast<const double2 *>(atoms + t);
+    double2 xy = __ldg(q), zr = __ldg(q + 1);
+    Atom a;
+    a.x = xy.x; a.y = xy.y; a.z = zr.x; a.r2 = zr.y;
+    return a;
+}
+#endif
+
+}  // namespace axb

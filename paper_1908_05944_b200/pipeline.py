@@ -1,0 +1,504 @@
+"""Host side of the drop-in boundary: ``compute_alpha_complex`` on a B200.
+
+Mirrors the reference's public interface for the hot path (reference
+pkg/src/alphax/pipeline.py): ``PipelineConfig`` (:55-83), ``AlphaComplex``
+(:117-187), ``complex_stats`` (:197-200), ``closure_ok`` (:203-211),
+``compute_alpha_complex(balls, cfg, stage_times=None)`` (:571-628).  All
+geometry runs in hand-written CUDA kernels behind the C-ABI of
+``include/alphax_b200.h``; this module only validates arguments, moves
+buffers (torch owns device memory and streams) and maps status codes back to
+the reference's exceptions.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Iterator, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .errors import (AlphaxError, DegenerateSimplex, DuplicateCenter, EmptyInput, NativeLibraryMissing,
+                     NonFiniteCoordinate)
+from .types import Ball, SimplexKey, TolerancePolicy
+
+STAGE_NAMES = ("grid", "potential_edges", "potential_triangles", "potential_tets",
+               "prune_tets", "prune_triangles", "prune_edges", "io")
+
+
+@dataclass(frozen=True)
+class PipelineConfig:
+    """Run configuration (reference pipeline.py:55-83).
+
+    ``alpha`` is in A^2 and compared as ``size <= alpha + eps_abs``.
+    ``chunk_size`` and ``workers`` are accepted for drop-in compatibility and
+    ignored: the result is provably independent of them (reference
+    T/test_acceptance.py:218-233) and the GPU schedules its own work.
+    """
+
+    alpha: float
+    mode: str = "grid"
+    chunk_size: int | None = None
+    workers: int = 1
+    biomolecule_mode: bool = False
+    tolerance: TolerancePolicy = field(default_factory=TolerancePolicy)
+
+    def __post_init__(self):
+        if not np.isfinite(self.alpha):
+            raise ValueError("alpha must be finite")
+        if self.mode not in ("grid", "naive"):
+            raise ValueError(f"mode must be 'grid' or 'naive', got {self.mode!r}")
+        if self.chunk_size is not None and self.chunk_size < 1:
+            raise ValueError("chunk_size must be positive")
+        if self.workers < 1:
+            raise ValueError("workers must be positive")
+        if self.biomolecule_mode and self.alpha < 0.0:
+            raise ValueError("biomolecule_mode requires alpha >= 0")
+
+
+def _rows_view(a: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    return a.view([("", np.int64)] * a.shape[1]).ravel()
+
+
+def _rows_isin(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    if a.shape[0] == 0 or b.shape[0] == 0:
+        return np.zeros(a.shape[0], dtype=bool)
+    return np.isin(_rows_view(a), _rows_view(b))
+
+
+def _canonical_rows(a, k: int) -> np.ndarray:
+    a = np.asarray(a, dtype=np.int64).reshape(-1, k)
+    return np.unique(a, axis=0) if a.shape[0] else a.copy()
+
+
+@dataclass(frozen=True, eq=False)
+class AlphaComplex:
+    """The result container of the reference (pipeline.py:117-187): vertices
+    (k0,) ascending; edges/triangles/tets (k, d+1) int64 rows, each strictly
+    increasing, rows in lexicographic order, no duplicates."""
+
+    vertices: np.ndarray
+    edges: np.ndarray
+    triangles: np.ndarray
+    tets: np.ndarray
+    alpha: float
+    ball_count: int
+
+    @classmethod
+    def from_rows(cls, vertices, edges, triangles, tets, alpha, ball_count) -> "AlphaComplex":
+        return cls(vertices=np.unique(np.asarray(vertices, dtype=np.int64)), edges=_canonical_rows(edges, 2),
+                   triangles=_canonical_rows(triangles, 3), tets=_canonical_rows(tets, 4),
+                   alpha=float(alpha), ball_count=int(ball_count))
+
+    def level(self, dim: int) -> np.ndarray:
+        if dim == 0:
+            return self.vertices.reshape(-1, 1)
+        return (self.edges, self.triangles, self.tets)[dim - 1]
+
+    def counts(self) -> tuple:
+        return tuple(int(self.level(d).shape[0]) for d in range(4))
+
+    @property
+    def total(self) -> int:
+        return sum(self.counts())
+
+    def simplex_keys(self, dim: int) -> list:
+        return [SimplexKey(tuple(int(v) for v in row)) for row in self.level(dim)]
+
+    def iter_simplices(self) -> Iterator[SimplexKey]:
+        for dim in range(4):
+            yield from self.simplex_keys(dim)
+
+    def contains(self, key: SimplexKey) -> bool:
+        probe = np.asarray([key.vertices], dtype=np.int64)
+        return bool(_rows_isin(probe, self.level(key.dim))[0])
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, AlphaComplex):
+            return NotImplemented
+        if self.ball_count != other.ball_count or self.alpha != other.alpha:
+            return False
+        return all(np.array_equal(self.level(d), other.level(d)) for d in range(4))
+
+    def symmetric_difference(self, other: "AlphaComplex") -> dict:
+        """dim -> (rows only in self, rows only in other)."""
+        diff = {}
+        for d in range(4):
+            mine, theirs = self.level(d), other.level(d)
+            diff[d] = (mine[~_rows_isin(mine, theirs)], theirs[~_rows_isin(theirs, mine)])
+        return diff
+
+    def is_subcomplex_of(self, other: "AlphaComplex") -> bool:
+        return all(bool(_rows_isin(self.level(d), other.level(d)).all()) for d in range(4))
+
+
+@dataclass(frozen=True)
+class ComplexStats:
+    counts: tuple
+    total: int
+    euler: int
+
+
+def complex_stats(k: AlphaComplex) -> ComplexStats:
+    c = k.counts()
+    return ComplexStats(counts=c, total=sum(c), euler=c[0] - c[1] + c[2] - c[3])
+
+
+def _facets(rows: np.ndarray) -> np.ndarray:
+    k = rows.shape[1]
+    return np.concatenate([np.delete(rows, drop, axis=1) for drop in range(k)], axis=0)
+
+
+def closure_ok(k: AlphaComplex) -> bool:
+    """Every facet of every simplex is a member (reference pipeline.py:203-211).
+    Host-side numpy check for tests and debugging; the device pipeline
+    guarantees closure by construction (kept simplices mark all their faces)."""
+    if k.tets.size and not _rows_isin(np.unique(_facets(k.tets), axis=0), k.triangles).all():
+        return False
+    if k.triangles.size and not _rows_isin(np.unique(_facets(k.triangles), axis=0), k.edges).all():
+        return False
+    if k.edges.size and not np.isin(np.unique(k.edges), k.vertices).all():
+        return False
+    return True
+
+
+# --------------------------------------------------------------------------- engine
+
+
+class Engine:
+    """One CUDA context of the native library on one GPU: owns the scratch
+    arena (a torch uint8 tensor) and maps status codes to exceptions."""
+
+    def __init__(self, device: int | None = None, arena_bytes: int = 0):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise NativeLibraryMissing("CUDA is not available; this package has no CPU fallback")
+        self.torch = torch
+        self.lib = N.load()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.handle = C.c_void_p()
+        st = self.lib.axb_ctx_create(C.byref(self.handle), self.device)
+        if st != N.OK:
+            raise AlphaxError(f"axb_ctx_create failed: {self.lib.axb_status_name(st).decode()}")
+        self.arena = None
+        self.last_stage_ms: dict = {}
+        if arena_bytes:
+            self._set_arena(arena_bytes)
+
+    def close(self):
+        if self.handle:
+            self.lib.axb_ctx_destroy(self.handle)
+            self.handle = C.c_void_p()
+        self.arena = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- plumbing
+    def _set_arena(self, nbytes: int):
+        torch = self.torch
+        self.arena = None          # free before growing
+        nbytes = (int(nbytes) + 4095) // 4096 * 4096
+        self.arena = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        st = self.lib.axb_ctx_set_arena(self.handle, self.arena.data_ptr(), nbytes)
+        if st != N.OK:
+            raise AlphaxError(self._message())
+
+    def _bind_stream(self):
+        stream = self.torch.cuda.current_stream(self.device)
+        self.lib.axb_ctx_set_stream(self.handle, C.c_void_p(stream.cuda_stream))
+
+    def _message(self) -> str:
+        return self.lib.axb_last_message(self.handle).decode(errors="replace")
+
+    def _params(self, cfg: PipelineConfig) -> N.Params:
+        return N.Params(float(cfg.alpha), float(cfg.tolerance.eps_abs), float(cfg.tolerance.eps_singular),
+                        1 if cfg.biomolecule_mode else 0, 0)
+
+    def _error_vertices(self):
+        verts = (C.c_int64 * 4)()
+        nv = C.c_int()
+        st = C.c_int()
+        self.lib.axb_last_error(self.handle, C.byref(st), verts, C.byref(nv))
+        return tuple(int(verts[i]) for i in range(nv.value))
+
+    def _raise(self, st: int, cfg: PipelineConfig, centers=None, radii=None):
+        """Status -> the exception the reference raises for the same input."""
+        if st == N.ERR_EMPTY:
+            raise EmptyInput("at least one ball is required")
+        if st == N.ERR_NONFINITE:
+            raise NonFiniteCoordinate(f"ball {self._error_vertices()[0]} is not finite")
+        if st == N.ERR_DUPLICATE:
+            i, j = self._error_vertices()
+            where = None
+            if centers is not None:
+                where = tuple(float(v) for v in _row_to_host(centers, i))
+            raise DuplicateCenter(f"balls {i} and {j} share the center {where}")
+        if st == N.ERR_DEGENERATE:
+            bad = self._error_vertices()
+            what = {2: "edge", 3: "triangle", 4: "tetrahedron"}.get(len(bad), "simplex")
+            raise DegenerateSimplex(f"{what} {bad} has affinely dependent centers", vertices=bad)
+        if st == N.ERR_BAD_SIDE:
+            r_max = float(_max_to_host(radii)) if radii is not None else float("nan")
+            raise ValueError(f"alpha={cfg.alpha} gives non-positive squared cell side (r_max={r_max})")
+        name = self.lib.axb_status_name(st).decode()
+        raise AlphaxError(f"{name}: {self._message()}")
+
+    def _with_arena(self, n: int, cfg: PipelineConfig, call):
+        """Run ``call()`` (returns a status), growing the arena on AXB_ERR_ARENA."""
+        if self.arena is None:
+            self._set_arena(self.lib.axb_arena_hint(n, float(cfg.alpha), 1.9))
+        for _ in range(12):
+            st = call()
+            if st != N.ERR_ARENA:
+                return st
+            need = int(self.lib.axb_arena_needed(self.handle))
+            have = self.arena.numel()
+            self._set_arena(max(int(need * 1.3) + (64 << 20), int(have * 1.5)))
+        raise AlphaxError("scratch arena kept overflowing: " + self._message())
+
+    def _collect_stage_ms(self):
+        ms = (C.c_float * len(N.STAGE_KEYS))()
+        self.lib.axb_stage_ms(self.handle, ms)
+        self.last_stage_ms = {k: float(ms[i]) for i, k in enumerate(N.STAGE_KEYS)}
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self.lib.axb_kernel_launches(self.handle))
+
+    # -- the hot path
+    def compute_host(self, centers: np.ndarray, radii: np.ndarray, cfg: PipelineConfig, pinned_out: bool = True):
+        """Host arrays in, four host int64 arrays out (H2D and D2H inside)."""
+        torch = self.torch
+        centers = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 3)
+        radii = np.ascontiguousarray(radii, dtype=np.float64).reshape(-1)
+        n = centers.shape[0]
+        if radii.shape[0] != n:
+            raise ValueError("centers and radii disagree in length")
+        if n == 0:
+            raise EmptyInput("at least one ball is required")
+        prm = self._params(cfg)
+        counts = (C.c_int64 * 4)()
+        outs: list = []
+
+        def run():
+            st = self.lib.axb_compute_host(self.handle, n, centers.ctypes.data, radii.ctypes.data, C.byref(prm), counts)
+            if st != N.OK:
+                return st
+            outs.clear()
+            for d in range(4):
+                shape = (int(counts[d]),) if d == 0 else (int(counts[d]), d + 1)
+                if pinned_out and counts[d]:
+                    outs.append(torch.empty(shape, dtype=torch.int64, pin_memory=True).numpy())
+                else:
+                    outs.append(np.empty(shape, dtype=np.int64))
+            # an arena overflow here re-runs the whole computation with a larger arena
+            return self.lib.axb_export_host(self.handle, *(o.ctypes.data if o.size else None for o in outs))
+
+        with torch.cuda.device(self.device):
+            self._bind_stream()
+            st = self._with_arena(n, cfg, run)
+            if st != N.OK:
+                self._raise(st, cfg, centers, radii)
+            self._collect_stage_ms()
+        return outs
+
+    def compute_device(self, centers, radii, cfg: PipelineConfig):
+        """CUDA tensors in (centers (n,3) f64, radii (n,) f64), four CUDA int64 tensors out."""
+        torch = self.torch
+        centers = centers.to(dtype=torch.float64).contiguous().reshape(-1, 3)
+        radii = radii.to(dtype=torch.float64).contiguous().reshape(-1)
+        n = centers.shape[0]
+        if n == 0:
+            raise EmptyInput("at least one ball is required")
+        prm = self._params(cfg)
+        counts = (C.c_int64 * 4)()
+        dev = f"cuda:{self.device}"
+        with torch.cuda.device(self.device):
+            self._bind_stream()
+            st = self._with_arena(n, cfg, lambda: self.lib.axb_compute(
+                self.handle, n, centers.data_ptr(), radii.data_ptr(), C.byref(prm), counts))
+            if st != N.OK:
+                self._raise(st, cfg, centers, radii)
+            outs = [torch.empty((int(counts[d]),) if d == 0 else (int(counts[d]), d + 1), dtype=torch.int64, device=dev)
+                    for d in range(4)]
+            st = self.lib.axb_export(self.handle, *(o.data_ptr() if o.numel() else None for o in outs))
+            if st == N.OK:
+                st = self.lib.axb_sync_check(self.handle)
+            if st != N.OK:
+                self._raise(st, cfg, centers, radii)
+            self._collect_stage_ms()
+        return outs
+
+
+    # -- stage-by-stage access (the reference's standalone stage operations, pipeline.py:640-731).
+    # The arena must already be large enough: growing it would drop the state of earlier stages.
+    def _check(self, st, cfg, centers=None, radii=None):
+        if st != N.OK:
+            self._raise(st, cfg, centers, radii)
+
+    def stage_grid(self, centers, radii, cfg: PipelineConfig, arena_factor: float = 4.0):
+        """validate_input + build_grid_arrays on CUDA tensors; returns the grid geometry."""
+        torch = self.torch
+        self._stage_inputs = (centers.to(dtype=torch.float64).contiguous().reshape(-1, 3),
+                              radii.to(dtype=torch.float64).contiguous().reshape(-1))
+        self._stage_cfg = cfg
+        n = self._stage_inputs[0].shape[0]
+        want = int(self.lib.axb_arena_hint(max(n, 1), float(cfg.alpha), 1.9) * arena_factor)
+        if self.arena is None or self.arena.numel() < want:
+            self._set_arena(want)
+        prm = self._params(cfg)
+        with torch.cuda.device(self.device):
+            self._bind_stream()
+            st = self.lib.axb_grid_build(self.handle, n, self._stage_inputs[0].data_ptr(),
+                                         self._stage_inputs[1].data_ptr(), C.byref(prm))
+        self._check(st, cfg, *self._stage_inputs)
+        info = N.GridInfo()
+        self.lib.axb_grid_get_info(self.handle, C.byref(info))
+        return dict(origin=np.array(list(info.origin)), cell_side=float(info.cell_side),
+                    dims=tuple(int(d) for d in info.dims), n_cells=int(info.n_cells), n_balls=int(info.n_balls))
+
+    def stage_grid_export(self):
+        torch = self.torch
+        n = self._stage_inputs[0].shape[0]
+        out = [torch.empty(n, dtype=torch.int64, device=f"cuda:{self.device}") for _ in range(3)]
+        self._check(self.lib.axb_grid_export(self.handle, *(o.data_ptr() for o in out)), self._stage_cfg)
+        return out      # order, rank, ball_cells
+
+    def stage_potential(self, lo: int = 0, hi: int | None = None):
+        n = self._stage_inputs[0].shape[0]
+        st = self.lib.axb_potential(self.handle, int(lo), int(n if hi is None else hi))
+        self._check(st, self._stage_cfg, *self._stage_inputs)
+        counts = (C.c_int64 * 3)()
+        self.lib.axb_potential_counts(self.handle, counts)
+        return tuple(int(v) for v in counts)
+
+    def stage_potential_export(self, dim: int):
+        """(rows, centres, sizes) of one potential level as CUDA tensors, in generation order."""
+        torch = self.torch
+        counts = (C.c_int64 * 3)()
+        self.lib.axb_potential_counts(self.handle, counts)
+        m = int(counts[dim - 1])
+        dev = f"cuda:{self.device}"
+        rows = torch.empty((m, dim + 1), dtype=torch.int64, device=dev)
+        cen = torch.empty((m, 3), dtype=torch.float64, device=dev)
+        siz = torch.empty(m, dtype=torch.float64, device=dev)
+        st = self.lib.axb_potential_export(self.handle, N.PE + dim - 1, rows.data_ptr() if m else None,
+                                           cen.data_ptr() if m else None, siz.data_ptr() if m else None)
+        self._check(st, self._stage_cfg)
+        return rows, cen, siz
+
+    def stage_prune(self):
+        self._check(self.lib.axb_prune(self.handle), self._stage_cfg, *self._stage_inputs)
+
+    def stage_canonicalize(self):
+        counts = (C.c_int64 * 4)()
+        self._check(self.lib.axb_canonicalize(self.handle, counts), self._stage_cfg, *self._stage_inputs)
+        return tuple(int(v) for v in counts)
+
+    def stage_export(self, counts):
+        torch = self.torch
+        dev = f"cuda:{self.device}"
+        outs = [torch.empty((int(counts[d]),) if d == 0 else (int(counts[d]), d + 1), dtype=torch.int64, device=dev)
+                for d in range(4)]
+        st = self.lib.axb_export(self.handle, *(o.data_ptr() if o.numel() else None for o in outs))
+        if st == N.OK:
+            st = self.lib.axb_sync_check(self.handle)
+        self._check(st, self._stage_cfg, *self._stage_inputs)
+        self._collect_stage_ms()
+        return outs
+
+    def ortho_batch(self, points, r2, eps_singular: float = 1e-12):
+        """Device probe of the predicate arithmetic: (m,k,3),(m,k) numpy -> centres, sizes, singular."""
+        torch = self.torch
+        dev = f"cuda:{self.device}"
+        p = torch.as_tensor(np.ascontiguousarray(points, dtype=np.float64), device=dev)
+        q = torch.as_tensor(np.ascontiguousarray(r2, dtype=np.float64), device=dev)
+        m, k = q.shape
+        cen = torch.empty((m, 3), dtype=torch.float64, device=dev)
+        siz = torch.empty(m, dtype=torch.float64, device=dev)
+        sg = torch.zeros(m, dtype=torch.uint8, device=dev)
+        with torch.cuda.device(self.device):
+            self._bind_stream()
+            st = self.lib.axb_ortho_batch(self.handle, m, k, p.data_ptr(), q.data_ptr(), float(eps_singular),
+                                          cen.data_ptr(), siz.data_ptr(), sg.data_ptr())
+        if st != N.OK:
+            raise AlphaxError(self._message())
+        return cen.cpu().numpy(), siz.cpu().numpy(), sg.cpu().numpy().astype(bool)
+
+
+def _row_to_host(a, i):
+    if isinstance(a, np.ndarray):
+        return a[i]
+    return a[i].detach().cpu().numpy()
+
+
+def _max_to_host(a):
+    if isinstance(a, np.ndarray):
+        return a.max()
+    return a.max().item()
+
+
+_ENGINES: dict = {}
+
+
+def default_engine(device: int | None = None) -> Engine:
+    """Process-wide engine per GPU (keeps the scratch arena warm between calls)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeLibraryMissing("CUDA is not available; this package has no CPU fallback")
+    dev = torch.cuda.current_device() if device is None else int(device)
+    eng = _ENGINES.get(dev)
+    if eng is None:
+        eng = _ENGINES[dev] = Engine(dev)
+    return eng
+
+
+# --------------------------------------------------------------------------- boundary
+
+
+def as_ball_arrays(balls: Sequence[Ball]):
+    centers = np.array([b.center for b in balls], dtype=np.float64).reshape(-1, 3)
+    radii = np.array([b.radius for b in balls], dtype=np.float64)
+    return centers, radii
+
+
+def _accumulate_stage_times(stage_times, stage_ms: dict):
+    if stage_times is None:
+        return
+    for key, ms in stage_ms.items():
+        stage_times[key] = stage_times.get(key, 0.0) + ms * 1e-3
+
+
+def compute_alpha_complex_arrays(centers, radii, cfg: PipelineConfig, stage_times: dict | None = None,
+                                 device: int | None = None) -> AlphaComplex:
+    """Array fast path of ``compute_alpha_complex``: ``centers`` (n,3) and
+    ``radii`` (n,) as numpy arrays (ball i = row i).  Same result, no ``Ball``
+    objects (building 10^6 of them costs seconds of Python)."""
+    if cfg.mode == "naive":
+        raise NotImplementedError("mode='naive' (the exhaustive reference oracle) is not part of the B200 build")
+    eng = default_engine(device)
+    n = int(np.asarray(radii).shape[0])
+    v, e, t, q = eng.compute_host(centers, radii, cfg)
+    _accumulate_stage_times(stage_times, eng.last_stage_ms)
+    return AlphaComplex(vertices=v, edges=e, triangles=t, tets=q, alpha=cfg.alpha, ball_count=n)
+
+
+def compute_alpha_complex(balls: Sequence[Ball], cfg: PipelineConfig, stage_times: dict | None = None) -> AlphaComplex:
+    """Alpha complex of a ball set -- drop-in for the reference entry point
+    (pipeline.py:571-628).  ``balls[i].index`` must equal ``i``."""
+    if len(balls) == 0:
+        raise EmptyInput("at least one ball is required")
+    for position, ball in enumerate(balls):
+        if ball.index != position:
+            raise ValueError(f"ball at position {position} carries index {ball.index}; "
+                             "indices must be the stable input ordinals")
+    centers, radii = as_ball_arrays(balls)
+    return compute_alpha_complex_arrays(centers, radii, cfg, stage_times)
