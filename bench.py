@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the alpha-complex hot path (BASELINE.json metric: alpha-complex
+atoms/sec on B200, % of HBM roofline, CPU reference beside it).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--atoms-per-gpu M] [--alpha A]
+
+One "step" = one full pass of the hot path (grid binning -> potential edges /
+triangles / tets -> pruning -> canonical int64 simplex lists) over one
+synthetic protein-density point set (generator G2 of SURVEY.md 8(d)).
+
+Workload at N=1: SURVEY.md 8(d) config 3 -- 1,000,000 atoms, seed 0, alpha 0.
+At N>1 every rank owns one z-slab of 1,000,000 atoms of an N x 1,000,000-atom
+set (weak scaling; N=8 is an 8M-atom assembly; `--atoms-per-gpu 1250000` gives
+the 10M-atom config 4), halo atoms replicated, no data-path collective; the
+only collective is the final gather of counts.
+
+Prints ONE JSON line (see the task contract): `value` = device-resident
+throughput (inputs already in HBM, outputs left in HBM), `e2e` = the same
+through the public host API with pinned host buffers (H2D + D2H inside the
+timed region), `roofline` for the dominant kernel, `cpu_baseline` = the CPU
+oracle (a C port of the reference algorithm, oracle/) on the host cores.
+`--impl reference` times that CPU implementation alone.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "alpha_complex_atoms_per_sec"
+UNIT = "atoms/s"
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        try:
+            return float(json.load(open(path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def algorithmic_bytes(n, G, E, T, Q, K):
+    """compulsory traffic per stage (each distinct input read once, each output written
+    once; fp64 coordinates/centres/sizes, int32 intermediate indices, int64 final rows)."""
+    K0, K1, K2, K3 = K
+    kept32 = 4 * K0 + 8 * K1 + 12 * K2 + 16 * K3
+    kept64 = 2 * kept32
+    S = {
+        "grid": 32 * n + 32 * n + 8 * n + 4 * (G + 1),
+        "potential_edges": 32 * n + 4 * G + 40 * E,
+        "potential_triangles": (32 * n + 8 * E + 44 * T) + (32 * n + 8 * E + 12 * T + 48 * Q),   # fused with tets
+        "prune_tets": 32 * n + 4 * G + 48 * Q + 16 * K3,
+        "prune_triangles": 32 * n + 4 * G + 44 * T + 12 * K2,
+        "prune_edges": 32 * n + 4 * G + 40 * E + 8 * K1,
+        "prune_vertices": 32 * n + 4 * G + 4 * K0,
+        "canonical": kept32 + kept32,
+        "export": kept32 + kept64,
+    }
+    total = (S["grid"] + S["potential_edges"] + S["potential_triangles"]
+             + (32 * n + 4 * G + 40 * E + 44 * T + 48 * Q + kept32) + kept32 + kept64)
+    return S, total
+
+
+KERNEL_OF_STAGE = {
+    "grid": "k_bounds+k_cell_keys+scan+k_cell_scatter+k_cell_finalize",
+    "potential_edges": "k_edges",
+    "potential_triangles": "k_tri_tet",
+    "prune_tets": "k_prune_tets",
+    "prune_triangles": "k_prune_tris",
+    "prune_edges": "k_prune_edges",
+    "prune_vertices": "k_prune_vertices",
+    "canonical": "scan+k_scatter_edges_tris+k_scatter_tets",
+    "export": "k_emit_edges+k_emit_tris+k_emit_tets+k_emit_vertices",
+}
+
+
+def make_workload(n_total, seed=0):
+    from paper_1908_05944_b200 import synth
+
+    return synth.jittered_lattice(n_total, seed)
+
+
+def run_cpu(centers, radii, alpha, eps_sing, threads):
+    import oracle
+
+    n = len(radii)
+    t0 = time.perf_counter()
+    res = oracle.compute(centers, radii, alpha, eps_singular=eps_sing, threads=threads,
+                         chunk=max(1, n // (8 * threads)))
+    dt = time.perf_counter() - t0
+    if res.status != oracle.OK:
+        raise RuntimeError(f"oracle failed with status {res.status}")
+    return dt, res
+
+
+def bench_reference(args, rank, world):
+    """The CPU implementation of the path (oracle port of the reference algorithm) on all host threads."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n = args.atoms_per_gpu          # bounded sample: one GPU's share of the workload
+    centers, radii = make_workload(n)
+    for _ in range(min(args.warmup, 1)):
+        run_cpu(centers, radii, args.alpha, args.eps_singular, threads)
+    times = []
+    for _ in range(args.steps):
+        dt, res = run_cpu(centers, radii, args.alpha, args.eps_singular, threads)
+        times.append(dt)
+    total = sum(times)
+    value = n * args.steps / total
+    sample = f"G2 jittered lattice n={n} seed=0 alpha={args.alpha}, {args.steps} full passes"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, n),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "simplices_per_sec": sum(res.counts()) * args.steps / total,
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+
+
+def workload_config(args, n_local):
+    return {"workload": f"SURVEY 8(d) config 3: G2 jittered lattice, {n_local} atoms per GPU, seed 0, "
+                        f"1 atom/12 A^3, radii U[1.2,1.9] A, alpha={args.alpha} A^2",
+            "atoms_per_gpu": n_local, "alpha": args.alpha, "eps_singular": args.eps_singular,
+            "l2": "flushed (256 MiB write) between timed steps; per-step working set ~1.5 GB also exceeds L2",
+            "sharding": "one z-slab per rank, 2-cell halo replicated" if args.gpus > 1 else "single GPU"}
+
+
+def bench_b200(args, rank, world, local_rank):
+    import torch
+
+    import paper_1908_05944_b200 as ax
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    eng = ax.default_engine(local_rank)
+    tol = ax.TolerancePolicy(1e-9, args.eps_singular)
+    cfg = ax.PipelineConfig(alpha=args.alpha, tolerance=tol)
+    n = args.atoms_per_gpu
+
+    if world == 1:
+        centers, radii = make_workload(n)
+    else:
+        from paper_1908_05944_b200.sharding import slab_for_rank
+
+        full_c, full_r = make_workload(n * world)
+        centers, radii = slab_for_rank(full_c, full_r, args.alpha, rank, world)
+        n = len(radii)
+    d_c = torch.as_tensor(centers, device="cuda")
+    d_r = torch.as_tensor(radii, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident throughput
+    for _ in range(args.warmup):
+        outs = eng.compute_device(d_c, d_r, cfg)
+    counts = tuple(int(o.shape[0]) for o in outs)
+    stage_acc = {}
+    launches0 = eng.kernel_launches
+    sampler = ClockSampler(local_rank)
+    if rank == 0:
+        sampler.start()
+    barrier()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)                      # evict L2 between timed iterations
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        outs = eng.compute_device(d_c, d_r, cfg)
+        e1.record()
+        torch.cuda.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        for k, v in eng.last_stage_ms.items():
+            stage_acc[k] = stage_acc.get(k, 0.0) + v
+    barrier()
+    clocks = sampler.stop() if rank == 0 else None
+    launches = eng.kernel_launches - launches0
+    dev_ms = float(sum(step_ms))
+    if dist is not None:
+        t = torch.tensor([dev_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+        tot = torch.tensor([n, sum(counts)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tot)
+        n_all, simplices_all = int(tot[0].item()), int(tot[1].item())
+    else:
+        n_all, simplices_all = n, sum(counts)
+    del outs
+
+    # ---- end to end through the public host API (pinned host inputs, host int64 outputs)
+    h_c = torch.as_tensor(centers).pin_memory()
+    h_r = torch.as_tensor(radii).pin_memory()
+    hc_np, hr_np = h_c.numpy(), h_r.numpy()
+    for _ in range(max(1, min(args.warmup, 2))):
+        k = ax.compute_alpha_complex_arrays(hc_np, hr_np, cfg, device=local_rank)
+    d2h = sum(a.nbytes for a in (k.vertices, k.edges, k.triangles, k.tets))
+    del k
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        k = ax.compute_alpha_complex_arrays(hc_np, hr_np, cfg, device=local_rank)
+        del k
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (CUDA-event stage times recorded inside the library)
+    pot = (C_int64 * 3)()
+    eng.lib.axb_potential_counts(eng.handle, pot)
+    info = ax._native.GridInfo()
+    eng.lib.axb_grid_get_info(eng.handle, __import__("ctypes").byref(info))
+    S, b_total = algorithmic_bytes(n, int(info.n_cells), int(pot[0]), int(pot[1]), int(pot[2]), counts)
+    stage_ms = {k: v / args.steps for k, v in stage_acc.items()}
+    kernel_stages = [k for k in stage_ms if k in S and k not in ("grid", "canonical", "export")]
+    top = max(kernel_stages, key=lambda k: stage_ms[k])
+    peak, peak_src = measured_peak()
+    achieved = S[top] / (stage_ms[top] * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(KERNEL_OF_STAGE[top])
+        except Exception:
+            traffic = None
+    ms_per_step = dev_ms / args.steps
+    line = {
+        "metric": METRIC, "value": n_all * args.steps / (dev_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, args.atoms_per_gpu),
+        "simplices_per_sec": simplices_all * args.steps / (dev_ms * 1e-3),
+        "counts": list(counts),
+        "e2e": {"value": n_all * args.steps / e2e_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_s / args.steps,
+                "h2d_bytes_per_step": int(hc_np.nbytes + hr_np.nbytes), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": KERNEL_OF_STAGE[top], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": int(S[top]), "kernel_ms": stage_ms[top],
+                     "pipeline": {"algorithmic_bytes": int(b_total), "bytes_per_atom": b_total / n,
+                                  "achieved": b_total / (ms_per_step * 1e-3) / 1e9,
+                                  "frac": b_total / (ms_per_step * 1e-3) / 1e9 / peak},
+                     "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+                     "stage_gbs": {k: round(S[k] / (stage_ms[k] * 1e-3) / 1e9, 1) for k in S if stage_ms.get(k, 0) > 0}},
+        "clocks": clocks,
+    }
+    # ---- CPU baseline beside it (rank 0, N=1 only): the oracle port on the host cores, same workload
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        dt, res = run_cpu(centers, radii, args.alpha, args.eps_singular, threads)
+        same = all(np.array_equal(a, b) for a, b in zip(
+            [o for o in eng.compute_host(centers, radii, cfg)], (res.vertices, res.edges, res.triangles, res.tets)))
+        line["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"the full step workload once ({n} atoms, alpha={args.alpha}): {dt:.2f} s",
+                                "gpu_output_bit_exact_with_cpu": bool(same)}
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--atoms-per-gpu", type=int, default=1_000_000)
+    ap.add_argument("--alpha", type=float, default=0.0)
+    ap.add_argument("--eps-singular", type=float, default=1e-12)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.eps_singular == 1e-12:
+        args.eps_singular = 1e-300      # large sets trip the default pivot threshold in BOTH implementations
+    if args.impl == "reference":
+        bench_reference(args, rank, world)
+    else:
+        bench_b200(args, rank, world, local_rank)
+
+
+from ctypes import c_int64 as C_int64  # noqa: E402
+
+if __name__ == "__main__":
+    main()

@@ -472,7 +472,7 @@ extern "C" int axb_grid_build(axb_ctx *c, int64_t n, const double *d_xyz, const 
     ARENA(c, c->ctr, Counters, 1);
     ARENA(c, c->errs, ErrRecord, ERR_CAP);
     ARENA(c, c->dups, int2, DUP_CAP);
-    const unsigned nb = std::max(1u, std::min(blocks_for((size_t)n, BOUNDS_THREADS), (unsigned)c->sm_count * 4u));
+    const unsigned nb = std::max(1u, std::min(blocks_for((size_t)n, BOUNDS_THREADS * 4), (unsigned)c->sm_count * 2u));
     BoundsPartial *partials, *bres;
     unsigned int *done;
     ARENA(c, partials, BoundsPartial, nb);
@@ -588,7 +588,7 @@ int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool sync_at_end) {
     c->mark_after_edges = c->arena_used;
 
     uint64_t pt_want = c->h->ctr.pair_bound + 32;           // every potential triangle is a partner pair
-    uint64_t pq_want = c->h->ctr.pair_bound / 2 + 4096;     // first guess; re-run on overflow
+    uint64_t pq_want = c->h->ctr.pair_bound + 4096;         // first guess; re-run on overflow
     for (int attempt = 0;; ++attempt) {
         if (pt_want > 0xfffffff0ull || pq_want > 0xfffffff0ull)
             return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential triangles or tetrahedra");

@@ -75,21 +75,39 @@ __global__ void __launch_bounds__(BOUNDS_THREADS) k_bounds(const double *__restr
         s_last = (ticket == gridDim.x - 1);
     }
     __syncthreads();
-    if (s_last && threadIdx.x == 0) {
+    if (s_last) {
+        // the last block folds all partials: threads stride over them, then the same two-level reduction
         __threadfence();
         const volatile BoundsPartial *vp = partials;
-        BoundsPartial p;
-        for (int c = 0; c < 3; ++c) { p.lo[c] = vp[0].lo[c]; p.hi[c] = vp[0].hi[c]; }
-        p.rmax = vp[0].rmax;
-        p.first_bad = vp[0].first_bad;
-        for (unsigned k = 1; k < gridDim.x; ++k) {
-            for (int c = 0; c < 3; ++c) { p.lo[c] = fmin(p.lo[c], vp[k].lo[c]); p.hi[c] = fmax(p.hi[c], vp[k].hi[c]); }
-            p.rmax = fmax(p.rmax, vp[k].rmax);
-            p.first_bad = min(p.first_bad, vp[k].first_bad);
+        double l2[3] = {INFINITY, INFINITY, INFINITY}, h2[3] = {-INFINITY, -INFINITY, -INFINITY}, rm = -INFINITY;
+        unsigned int fb = 0xffffffffu;
+        for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) {
+            for (int c = 0; c < 3; ++c) { l2[c] = fmin(l2[c], vp[k].lo[c]); h2[c] = fmax(h2[c], vp[k].hi[c]); }
+            rm = fmax(rm, vp[k].rmax);
+            fb = min(fb, vp[k].first_bad);
         }
-        p.pad = 0;
-        *result = p;
-        *done_counter = 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { l2[c] = warp_min_d(l2[c]); h2[c] = warp_max_d(h2[c]); }
+        rm = warp_max_d(rm);
+        fb = __reduce_min_sync(FULL, fb);
+        __syncthreads();
+        if (lane_id() == 0) {
+            for (int c = 0; c < 3; ++c) { s_part[w].lo[c] = l2[c]; s_part[w].hi[c] = h2[c]; }
+            s_part[w].rmax = rm;
+            s_part[w].first_bad = fb;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            BoundsPartial p = s_part[0];
+            for (int k = 1; k < BOUNDS_THREADS / 32; ++k) {
+                for (int c = 0; c < 3; ++c) { p.lo[c] = fmin(p.lo[c], s_part[k].lo[c]); p.hi[c] = fmax(p.hi[c], s_part[k].hi[c]); }
+                p.rmax = fmax(p.rmax, s_part[k].rmax);
+                p.first_bad = min(p.first_bad, s_part[k].first_bad);
+            }
+            p.pad = 0;
+            *result = p;
+            *done_counter = 0;
+        }
     }
 }
 

@@ -1,0 +1,239 @@
+"""GPU parity tests: the CUDA path (through the Python boundary and the C-ABI)
+against (a) the golden outputs of the real reference and (b) the CPU oracle on
+the same seeded inputs.  Bit-exact everywhere: integer rows and the cached
+fp64 ortho data."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1908_05944_b200 as ax
+from paper_1908_05944_b200 import synth
+
+from conftest import GOLD
+from helpers import canonical_text, digest_arrays
+
+pytestmark = pytest.mark.gpu
+
+
+def arrays_of(k):
+    return (k.vertices, k.edges, k.triangles, k.tets)
+
+
+def assert_same_complex(k, ref, tag=""):
+    for d, (got, want) in enumerate(zip(arrays_of(k), (ref.vertices, ref.edges, ref.triangles, ref.tets))):
+        assert got.dtype == np.int64
+        assert np.array_equal(got, want), f"{tag}: dimension {d} differs"
+
+
+def lexsorted(rows, *carry):
+    if rows.shape[0] == 0:
+        return (rows,) + carry
+    perm = np.lexsort(tuple(rows[:, c] for c in range(rows.shape[1] - 1, -1, -1)))
+    return (rows[perm],) + tuple(a[perm] for a in carry)
+
+
+def test_device_ortho_matches_reference_bitwise():
+    eng = ax.default_engine()
+    d = np.load(os.path.join(GOLD, "ortho_vectors.npz"))
+    for k in (1, 2, 3, 4):
+        for eps in ("1e-12", "1e-300"):
+            cen, siz, sg = eng.ortho_batch(d[f"k{k}_points"], d[f"k{k}_r2"], float(eps))
+            want_sg = d[f"k{k}_eps{eps}_singular"]
+            assert np.array_equal(sg, want_sg)
+            ok = ~want_sg
+            assert np.array_equal(cen[ok].view(np.uint64), d[f"k{k}_eps{eps}_centers"][ok].view(np.uint64))
+            assert np.array_equal(siz[ok].view(np.uint64), d[f"k{k}_eps{eps}_sizes"][ok].view(np.uint64))
+
+
+def test_small_cases_against_reference_golden(gold_small):
+    for name, rec in gold_small.items():
+        m = rec["meta"]
+        cfg = ax.PipelineConfig(alpha=m["alpha"], biomolecule_mode=m["biomolecule"],
+                                tolerance=ax.TolerancePolicy(m["eps_abs"], m["eps_singular"]))
+        k = ax.compute_alpha_complex_arrays(rec["centers"], rec["radii"], cfg)
+        assert list(k.counts()) == m["counts"], name
+        for d, got in enumerate(arrays_of(k)):
+            assert np.array_equal(got, rec[f"k{d}"].reshape(got.shape)), (name, d)
+        text = canonical_text(*arrays_of(k), len(rec["radii"]), m["alpha"])
+        assert hashlib.sha256(text.encode()).hexdigest() == m["sha256_complex"], name
+        assert k.ball_count == len(rec["radii"]) and k.alpha == m["alpha"]
+
+
+def test_config1_through_ball_boundary(gold_config1):
+    data, meta = gold_config1
+    balls = [ax.Ball(tuple(c), float(r), i) for i, (c, r) in enumerate(zip(data["centers"], data["radii"]))]
+    for tag, m in meta.items():
+        st = {}
+        k = ax.compute_alpha_complex(balls, ax.PipelineConfig(alpha=m["alpha"], biomolecule_mode=m["biomolecule"],
+                                                              workers=3, chunk_size=37), stage_times=st)
+        assert list(k.counts()) == m["counts"]
+        for d, got in enumerate(arrays_of(k)):
+            assert np.array_equal(got, data[f"{tag}__k{d}"].reshape(got.shape))
+        text = canonical_text(*arrays_of(k), 1000, m["alpha"])
+        assert hashlib.sha256(text.encode()).hexdigest() == m["sha256_complex"]
+        for key in ("grid", "potential_edges", "potential_triangles", "potential_tets", "prune_tets",
+                    "prune_triangles", "prune_edges", "prune_vertices"):
+            assert key in st and st[key] >= 0.0
+        assert ax.closure_ok(k)
+        assert ax.complex_stats(k).total == sum(m["counts"])
+
+
+def test_stagewise_against_oracle():
+    """grid order, potential levels (rows + cached ortho data bitwise) and the complex, stage by stage."""
+    import torch
+
+    eng = ax.default_engine()
+    cases = [synth.jittered_lattice(20_000, 11) + (0.0, 1e-12), synth.jittered_lattice(20_000, 11) + (1.4, 1e-12),
+             synth.adversarial_density(20_000, 5) + (0.0, 1e-300),
+             synth.random_globule(300, 21, 0.4, (0.3, 2.2), 0.5) + (0.7, 1e-300)]
+    for c, r, alpha, eps_sing in cases:
+        cfg = ax.PipelineConfig(alpha=alpha, tolerance=ax.TolerancePolicy(1e-9, eps_sing))
+        ref = oracle.compute(c, r, alpha, eps_singular=eps_sing, keep_potentials=True, threads=os.cpu_count(), chunk=2000)
+        assert ref.status == oracle.OK
+        info = eng.stage_grid(torch.as_tensor(c, device="cuda"), torch.as_tensor(r, device="cuda"), cfg)
+        st, g = oracle.grid_build(c, r, alpha)
+        assert info["dims"] == g.dims and info["cell_side"] == g.side and np.array_equal(info["origin"], g.origin)
+        order, rank, cells = (t.cpu().numpy() for t in eng.stage_grid_export())
+        assert np.array_equal(order, g.order) and np.array_equal(rank, g.rank) and np.array_equal(cells, g.cells)
+        eng.stage_potential()
+        for dim in (1, 2, 3):
+            rows, cen, siz = lexsorted(*(t.cpu().numpy() for t in eng.stage_potential_export(dim)))
+            wrows, wcen, wsiz = ref.potentials[dim]
+            assert np.array_equal(rows, wrows), dim
+            assert np.array_equal(cen.view(np.uint64), wcen.view(np.uint64)), dim
+            assert np.array_equal(siz.view(np.uint64), wsiz.view(np.uint64)), dim
+        eng.stage_prune()
+        counts = eng.stage_canonicalize()
+        outs = [t.cpu().numpy() for t in eng.stage_export(counts)]
+        for got, want in zip(outs, (ref.vertices, ref.edges, ref.triangles, ref.tets)):
+            assert np.array_equal(got, want)
+
+
+def test_error_parity(gold_errors):
+    """Same exception type, vertices and message as the reference on its failing inputs."""
+    kinds = {"DegenerateSimplex": ax.DegenerateSimplex, "DuplicateCenter": ax.DuplicateCenter,
+             "NonFiniteCoordinate": ax.NonFiniteCoordinate, "ValueError": ValueError}
+    for name, rec in gold_errors.items():
+        c = np.array(rec["centers"], dtype=np.float64)
+        r = np.array(rec["radii"], dtype=np.float64)
+        cfg = ax.PipelineConfig(alpha=rec["alpha"], tolerance=ax.TolerancePolicy(1e-9, rec["eps_singular"]))
+        if rec["error"] is None:
+            ax.compute_alpha_complex_arrays(c, r, cfg)
+            continue
+        with pytest.raises(kinds[rec["error"]]) as err:
+            ax.compute_alpha_complex_arrays(c, r, cfg)
+        assert str(err.value) == rec["message"], name
+        if rec["error"] == "DegenerateSimplex":
+            assert list(err.value.vertices) == rec["vertices"], name
+    with pytest.raises(ax.EmptyInput):
+        ax.compute_alpha_complex([], ax.PipelineConfig(alpha=0.0))
+    with pytest.raises(ax.NonFiniteCoordinate, match="ball 1 is not finite"):
+        ax.compute_alpha_complex_arrays(np.array([[0, 0, 0], [np.inf, 0, 0]]), np.ones(2), ax.PipelineConfig(alpha=0.0))
+    with pytest.raises(ValueError, match="stable input ordinals"):
+        ax.compute_alpha_complex([ax.Ball((0, 0, 0), 1, 0), ax.Ball((3, 0, 0), 1, 2)], ax.PipelineConfig(alpha=0.0))
+    with pytest.raises(NotImplementedError):
+        ax.compute_alpha_complex_arrays(np.zeros((1, 3)), np.ones(1), ax.PipelineConfig(alpha=0.0, mode="naive"))
+
+
+def test_many_singular_solves_report_the_first():
+    """More singular candidates than record slots: the replay path must still name the reference's simplex."""
+    g = np.stack(np.meshgrid(np.arange(14.0), np.arange(14.0), np.arange(14.0), indexing="ij"), -1).reshape(-1, 3) * 1.5
+    r = np.full(g.shape[0], 1.2)
+    ref = oracle.compute(g, r, 1.0)
+    assert ref.status == oracle.DEGENERATE
+    with pytest.raises(ax.DegenerateSimplex) as err:
+        ax.compute_alpha_complex_arrays(g, r, ax.PipelineConfig(alpha=1.0))
+    assert err.value.vertices == ref.error_vertices
+
+
+def test_config2_50k_against_reference_golden(gold_large):
+    for name in ("g2_50k_a0", "g2_50k_a14"):
+        m = gold_large[name]
+        c, r = synth.jittered_lattice(m["n"], m["seed"])
+        k = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=m["alpha"]))
+        assert list(k.counts()) == m["counts"]
+        assert digest_arrays(*arrays_of(k)) == m["sha256_arrays"]
+    # alpha sweep is monotone: K(0) is a subcomplex of K(1.4)
+    c, r = synth.jittered_lattice(20_000, 0)
+    k0 = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=0.0))
+    k1 = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=1.4))
+    assert k0.is_subcomplex_of(k1) and ax.closure_ok(k0) and ax.closure_ok(k1)
+
+
+def test_config3_1m_against_oracle_and_reference_golden(gold_large):
+    """1,000,000 atoms, alpha 0 -- full-size bit-exact comparison."""
+    c, r = synth.jittered_lattice(1_000_000, 0)
+    k = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=0.0))
+    assert k.counts() == (1000000, 4607698, 3483769, 510141)          # measured with the reference
+    if "g2_1m_a0" in gold_large:
+        assert list(k.counts()) == gold_large["g2_1m_a0"]["counts"]
+        assert digest_arrays(*arrays_of(k)) == gold_large["g2_1m_a0"]["sha256_arrays"]
+    ref = oracle.compute(c, r, 0.0, threads=os.cpu_count(), chunk=4000)
+    assert ref.status == oracle.OK
+    assert_same_complex(k, ref, "1M")
+    # rows strictly increasing and lexicographically sorted without duplicates (size-independent properties)
+    for rows in (k.edges, k.triangles, k.tets):
+        assert (np.diff(rows, axis=1) > 0).all()
+        a, b = rows[:-1], rows[1:]
+        less = np.zeros(a.shape[0], dtype=bool)
+        equal = np.ones(a.shape[0], dtype=bool)
+        for col in range(rows.shape[1]):
+            less |= equal & (a[:, col] < b[:, col])
+            equal &= a[:, col] == b[:, col]
+        assert less.all()
+    assert (np.diff(k.vertices) > 0).all()
+
+
+def test_alpha14_200k_tiny_eps_against_oracle():
+    c, r = synth.jittered_lattice(200_000, 0)
+    tol = ax.TolerancePolicy(1e-9, 1e-300)
+    k = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=1.4, tolerance=tol))
+    ref = oracle.compute(c, r, 1.4, eps_singular=1e-300, threads=os.cpu_count(), chunk=4000)
+    assert_same_complex(k, ref, "200k a1.4")
+
+
+def test_adversarial_density_against_oracle():
+    """Config 5 (reduced to 300k atoms so the CPU oracle stays quick): voids + 3x-dense cores, shuffled indices."""
+    c, r = synth.adversarial_density(300_000, 0, shuffle=True)
+    tol = ax.TolerancePolicy(1e-9, 1e-300)
+    k = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=0.0, tolerance=tol))
+    ref = oracle.compute(c, r, 0.0, eps_singular=1e-300, threads=os.cpu_count(), chunk=4000)
+    assert ref.status == oracle.OK
+    assert_same_complex(k, ref, "adversarial")
+
+
+def test_device_path_equals_host_path_and_is_deterministic():
+    import torch
+
+    eng = ax.default_engine()
+    c, r = synth.jittered_lattice(100_000, 2)
+    cfg = ax.PipelineConfig(alpha=0.5)
+    host = eng.compute_host(c, r, cfg)
+    for _ in range(2):
+        dev = [t.cpu().numpy() for t in eng.compute_device(torch.as_tensor(c, device="cuda"),
+                                                           torch.as_tensor(r, device="cuda"), cfg)]
+        for a, b in zip(host, dev):
+            assert np.array_equal(a, b)
+    before = eng.kernel_launches
+    eng.compute_host(c, r, cfg)
+    assert eng.kernel_launches - before >= 20        # the CUDA kernels did run
+
+
+def test_permutation_of_input_indices():
+    """Relabelling the balls relabels the complex (ownership by grid rank must not leak into the output)."""
+    c, r = synth.jittered_lattice(30_000, 4)
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(len(r))
+    cfg = ax.PipelineConfig(alpha=0.8)
+    k = ax.compute_alpha_complex_arrays(c, r, cfg)
+    kp = ax.compute_alpha_complex_arrays(c[perm], r[perm], cfg)
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(len(perm))
+    # ball i of the original is ball inv[i] of the permuted input
+    relabelled = ax.AlphaComplex.from_rows(inv[k.vertices], np.sort(inv[k.edges], axis=1),
+                                           np.sort(inv[k.triangles], axis=1), np.sort(inv[k.tets], axis=1),
+                                           cfg.alpha, len(r))
+    assert relabelled == kp
