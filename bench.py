@@ -211,16 +211,19 @@ def bench_b200(args, rank, world, local_rank):
     cfg = ax.PipelineConfig(alpha=args.alpha, tolerance=tol)
     n = args.atoms_per_gpu
 
+    job = None
     if world == 1:
         centers, radii = make_workload(n)
+        n_total = n
     else:
-        from paper_1908_05944_b200.sharding import slab_for_rank
+        from paper_1908_05944_b200.sharding import ShardedJob
 
-        full_c, full_r = make_workload(n * world)
-        centers, radii = slab_for_rank(full_c, full_r, args.alpha, rank, world)
-        n = len(radii)
-    d_c = torch.as_tensor(centers, device="cuda")
-    d_r = torch.as_tensor(radii, device="cuda")
+        n_total = n * world
+        centers, radii = make_workload(n_total)
+        job = ShardedJob(centers, radii, cfg, rank, world, eng, dist)
+    if job is None:
+        d_c = torch.as_tensor(centers, device="cuda")
+        d_r = torch.as_tensor(radii, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -228,10 +231,14 @@ def bench_b200(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def device_step():
+        # N=1: the whole input on this GPU.  N>1: this rank's slab, then the gather + merge on rank 0.
+        return eng.compute_device(d_c, d_r, cfg) if job is None else job.step()
+
     # ---- device-resident throughput
     for _ in range(args.warmup):
-        outs = eng.compute_device(d_c, d_r, cfg)
-    counts = tuple(int(o.shape[0]) for o in outs)
+        outs = device_step()
+    counts = tuple(int(o.shape[0]) for o in outs) if outs is not None else (0, 0, 0, 0)
     stage_acc = {}
     launches0 = eng.kernel_launches
     sampler = ClockSampler(local_rank)
@@ -244,7 +251,7 @@ def bench_b200(args, rank, world, local_rank):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        outs = eng.compute_device(d_c, d_r, cfg)
+        outs = device_step()
         e1.record()
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
@@ -258,26 +265,42 @@ def bench_b200(args, rank, world, local_rank):
         t = torch.tensor([dev_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
-        tot = torch.tensor([n, sum(counts)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tot)
-        n_all, simplices_all = int(tot[0].item()), int(tot[1].item())
-    else:
-        n_all, simplices_all = n, sum(counts)
+    n_all, simplices_all = n_total, sum(counts)      # counts live on rank 0 (the merged complex)
     del outs
 
-    # ---- end to end through the public host API (pinned host inputs, host int64 outputs)
-    h_c = torch.as_tensor(centers).pin_memory()
-    h_r = torch.as_tensor(radii).pin_memory()
-    hc_np, hr_np = h_c.numpy(), h_r.numpy()
+    # ---- end to end: pinned host inputs -> H2D -> hot path -> D2H of the int64 rows, every step
+    if job is None:
+        h_c = torch.as_tensor(centers).pin_memory()
+        h_r = torch.as_tensor(radii).pin_memory()
+        hc_np, hr_np = h_c.numpy(), h_r.numpy()
+        h2d = int(hc_np.nbytes + hr_np.nbytes)
+
+        def e2e_step():
+            k = ax.compute_alpha_complex_arrays(hc_np, hr_np, cfg, device=local_rank)   # the public API call
+            return sum(a.nbytes for a in (k.vertices, k.edges, k.triangles, k.tets))
+    else:
+        slab = job.slab
+        pins = [torch.as_tensor(a).pin_memory() for a in (slab.centers, slab.radii, slab.global_index)] if slab else []
+        h2d = int(sum(p.numel() * p.element_size() for p in pins))
+
+        def e2e_step():
+            if slab is not None:
+                job.d_c.copy_(pins[0], non_blocking=True)
+                job.d_r.copy_(pins[1], non_blocking=True)
+                job.d_g.copy_(pins[2], non_blocking=True)
+            merged = job.step()
+            if merged is None:
+                return 0
+            host = [torch.empty(m.shape, dtype=m.dtype, pin_memory=True).copy_(m, non_blocking=True) for m in merged]
+            torch.cuda.synchronize()
+            return sum(h.numel() * 8 for h in host)
+
     for _ in range(max(1, min(args.warmup, 2))):
-        k = ax.compute_alpha_complex_arrays(hc_np, hr_np, cfg, device=local_rank)
-    d2h = sum(a.nbytes for a in (k.vertices, k.edges, k.triangles, k.tets))
-    del k
+        d2h = e2e_step()
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        k = ax.compute_alpha_complex_arrays(hc_np, hr_np, cfg, device=local_rank)
-        del k
+        e2e_step()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist is not None:
@@ -291,11 +314,14 @@ def bench_b200(args, rank, world, local_rank):
         return
 
     # ---- roofline of the dominant kernel (CUDA-event stage times recorded inside the library)
+    if job is not None:
+        job.local()            # the merge on rank 0 dropped the slab state; redo the slab so its counts can be read
     pot = (C_int64 * 3)()
     eng.lib.axb_potential_counts(eng.handle, pot)
     info = ax._native.GridInfo()
     eng.lib.axb_grid_get_info(eng.handle, __import__("ctypes").byref(info))
-    S, b_total = algorithmic_bytes(n, int(info.n_cells), int(pot[0]), int(pot[1]), int(pot[2]), counts)
+    n_local = n if job is None else (len(job.slab.radii) if job.slab is not None else 0)
+    S, b_total = algorithmic_bytes(n_local, int(info.n_cells), int(pot[0]), int(pot[1]), int(pot[2]), counts)
     stage_ms = {k: v / args.steps for k, v in stage_acc.items()}
     kernel_stages = [k for k in stage_ms if k in S and k not in ("grid", "canonical", "export")]
     top = max(kernel_stages, key=lambda k: stage_ms[k])
@@ -317,7 +343,7 @@ def bench_b200(args, rank, world, local_rank):
         "simplices_per_sec": simplices_all * args.steps / (dev_ms * 1e-3),
         "counts": list(counts),
         "e2e": {"value": n_all * args.steps / e2e_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_s / args.steps,
-                "h2d_bytes_per_step": int(hc_np.nbytes + hr_np.nbytes), "d2h_bytes_per_step": int(d2h)},
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": KERNEL_OF_STAGE[top], "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

@@ -63,6 +63,15 @@ typedef struct axb_grid_info {
     int64_t n_balls;
 } axb_grid_info;
 
+/* one z-slab of a global grid (multi-GPU sharding): geometry of the GLOBAL grid
+ * (grid.py:112-121 evaluated on the whole input) and the loaded cell layers [z_lo, z_hi) */
+typedef struct axb_slab {
+    double origin[3];
+    double cell_side;
+    int64_t dims[3];
+    int64_t z_lo, z_hi;
+} axb_slab;
+
 /* what-selectors */
 enum { AXB_K0 = 0, AXB_K1 = 1, AXB_K2 = 2, AXB_K3 = 3, AXB_PE = 4, AXB_PT = 5, AXB_PQ = 6 };
 
@@ -97,6 +106,15 @@ int axb_last_error(const axb_ctx *ctx, int *status, int64_t verts[4], int *nvert
  * d_xyz: n x 3 row-major f64, d_radii: n f64, both DEVICE pointers. */
 int axb_grid_build(axb_ctx *ctx, int64_t n, const double *d_xyz, const double *d_radii,
                    const axb_params *params);
+/* Same for ONE SLAB of a larger input: the caller fixes the global grid geometry and passes only
+ * the balls whose cell layer lies in [z_lo, z_hi), in ascending global ball index;
+ * d_global_index (n int64, may be NULL) renames them in the exported rows.  This is the paper's
+ * partition strategy (PAPER 4.6) / the reference's chunk ownership (pipeline.py:10-15) across GPUs. */
+int axb_grid_build_slab(axb_ctx *ctx, int64_t n, const double *d_xyz, const double *d_radii,
+                        const int64_t *d_global_index, const axb_params *params, const axb_slab *slab);
+/* grid ranks [rank_lo, rank_hi) of the balls in cell layers [z_own_lo, z_own_hi) -- the generator
+ * range to pass to axb_potential for the layers this slab OWNS (the rest is halo) */
+int axb_slab_rank_range(axb_ctx *ctx, int64_t z_own_lo, int64_t z_own_hi, int64_t *rank_lo, int64_t *rank_hi);
 int axb_grid_get_info(const axb_ctx *ctx, axb_grid_info *out);
 /* order / rank / ball_cells of the reference Grid as int64 DEVICE arrays (any may be NULL) */
 int axb_grid_export(axb_ctx *ctx, int64_t *d_order, int64_t *d_rank, int64_t *d_ball_cells);
@@ -133,6 +151,14 @@ int axb_compute_host(axb_ctx *ctx, int64_t n, const double *h_xyz, const double 
                      const axb_params *params, int64_t counts[4]);
 /* axb_export into HOST buffers (pinned or pageable). */
 int axb_export_host(axb_ctx *ctx, int64_t *h_vertices, int64_t *h_edges, int64_t *h_triangles, int64_t *h_tets);
+
+/* ---- merge of per-slab results ------------------------------------------- */
+/* Sorted, duplicate-free union of m canonical rows of width k (1..4) with indices in [0, n_index):
+ * the final np.unique of the reference (pipeline.py:611-614) for lists gathered from several slabs.
+ * d_rows (m, k) and d_out (capacity m rows) are DEVICE int64; *count_out = rows written.
+ * Reuses the scratch arena from the start (drops the state of a previous run). */
+int axb_merge_rows(axb_ctx *ctx, int k, int64_t n_index, const int64_t *d_rows, int64_t m, int64_t *d_out,
+                   int64_t *count_out);
 
 /* ---- measurement -------------------------------------------------------- */
 /* CUDA-event milliseconds per stage of the last run */

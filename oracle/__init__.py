@@ -49,6 +49,9 @@ def lib() -> C.CDLL:
         L.axo_compute.argtypes = [C.c_int64, pd, pd, C.c_double, C.c_double, C.c_double,
                                   C.c_int, C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.axo_compute.restype = C.c_int
+        L.axo_compute_range.argtypes = [C.c_int64, pd, pd, C.c_double, C.c_double, C.c_double,
+                                        C.c_int, C.c_int64, C.c_int64, C.POINTER(C.c_void_p)]
+        L.axo_compute_range.restype = C.c_int
         L.axo_status.argtypes = [C.c_void_p]
         L.axo_status.restype = C.c_int
         L.axo_error.argtypes = [C.c_void_p, p64, C.POINTER(C.c_int)]
@@ -134,16 +137,21 @@ class OracleResult:
 
 def compute(centers: np.ndarray, radii: np.ndarray, alpha: float, *, eps_abs: float = 1e-9,
             eps_singular: float = 1e-12, biomolecule: bool = False, chunk: int | None = None,
-            threads: int = 1, keep_potentials: bool = False) -> OracleResult:
-    """The whole hot path on the CPU (reference pipeline.py:571-628, mode="grid")."""
+            threads: int = 1, keep_potentials: bool = False, rank_range: tuple | None = None) -> OracleResult:
+    """The whole hot path on the CPU (reference pipeline.py:571-628, mode="grid").
+    ``rank_range=(lo, hi)`` computes a single ``_chunk_pass`` over those grid ranks instead."""
     centers = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 3)
     radii = np.ascontiguousarray(radii, dtype=np.float64)
     n = centers.shape[0]
     L = lib()
     h = C.c_void_p()
-    st = L.axo_compute(n, _pd(centers), _pd(radii), float(alpha), float(eps_abs), float(eps_singular),
-                       int(bool(biomolecule)), int(chunk or 0), int(threads), int(bool(keep_potentials)),
-                       C.byref(h))
+    if rank_range is not None:
+        st = L.axo_compute_range(n, _pd(centers), _pd(radii), float(alpha), float(eps_abs), float(eps_singular),
+                                 int(bool(biomolecule)), int(rank_range[0]), int(rank_range[1]), C.byref(h))
+    else:
+        st = L.axo_compute(n, _pd(centers), _pd(radii), float(alpha), float(eps_abs), float(eps_singular),
+                           int(bool(biomolecule)), int(chunk or 0), int(threads), int(bool(keep_potentials)),
+                           C.byref(h))
     try:
         verts = (C.c_int64 * 4)()
         nv = C.c_int()

@@ -711,10 +711,10 @@ static int cmp_perm(const void *a, const void *b, void *cp) {
     return cmp_rows(pc->rows + (size_t)i * pc->k, pc->rows + (size_t)j * pc->k, (void *)&pc->k);
 }
 
-int axo_compute(int64_t n, const double *xyz, const double *radii,
+static int compute_impl(int64_t n, const double *xyz, const double *radii,
                 double alpha, double eps_abs, double eps_singular,
                 int biomolecule, int64_t chunk, int threads,
-                int keep_potentials, axo_result **out) {
+                int keep_potentials, int64_t range_lo, int64_t range_hi, axo_result **out) {
     axo_result *r = (axo_result *)calloc(1, sizeof(axo_result));
     if (!r) return AXO_NOMEM;
     *out = r;
@@ -743,6 +743,7 @@ int axo_compute(int64_t n, const double *xyz, const double *radii,
 
     if (chunk <= 0 || chunk > n) chunk = n;            /* pipe:598 */
     int64_t nchunks = (n + chunk - 1) / chunk;
+    if (range_lo >= 0) nchunks = 1;                    /* one explicit _chunk_pass(lo, hi), pipe:530 */
     chunk_out *parts = (chunk_out *)calloc((size_t)nchunks, sizeof(chunk_out));
     if (threads < 1) threads = 1;
 #ifdef _OPENMP
@@ -750,6 +751,7 @@ int axo_compute(int64_t n, const double *xyz, const double *radii,
 #endif
     for (int64_t ci = 0; ci < nchunks; ++ci) {
         int64_t lo = ci * chunk, hi = lo + chunk < n ? lo + chunk : n;
+        if (range_lo >= 0) { lo = range_lo; hi = range_hi < n ? range_hi : n; }
         chunk_pass(&c, lo, hi, &parts[ci]);
     }
 
@@ -815,4 +817,19 @@ int axo_compute(int64_t n, const double *xyz, const double *radii,
     free(c.r2); free(c.reach); free(c.viable);
     grid_free(&c.grid);
     return r->status;
+}
+
+int axo_compute(int64_t n, const double *xyz, const double *radii,
+                double alpha, double eps_abs, double eps_singular,
+                int biomolecule, int64_t chunk, int threads,
+                int keep_potentials, axo_result **out) {
+    return compute_impl(n, xyz, radii, alpha, eps_abs, eps_singular, biomolecule, chunk, threads,
+                        keep_potentials, -1, -1, out);
+}
+
+int axo_compute_range(int64_t n, const double *xyz, const double *radii,
+                      double alpha, double eps_abs, double eps_singular,
+                      int biomolecule, int64_t rank_lo, int64_t rank_hi, axo_result **out) {
+    if (rank_lo < 0) rank_lo = 0;
+    return compute_impl(n, xyz, radii, alpha, eps_abs, eps_singular, biomolecule, 0, 1, 0, rank_lo, rank_hi, out);
 }

@@ -67,6 +67,12 @@ int axo_compute(int64_t n, const double *xyz, const double *radii,
                 int biomolecule, int64_t chunk, int threads,
                 int keep_potentials, axo_result **out);
 
+/* pipeline.py:530-555: ONE _chunk_pass over grid ranks [rank_lo, rank_hi) of the whole input (the
+ * unit the reference hands to a worker; what one GPU slab computes).  Rows are sorted-unique. */
+int axo_compute_range(int64_t n, const double *xyz, const double *radii,
+                      double alpha, double eps_abs, double eps_singular,
+                      int biomolecule, int64_t rank_lo, int64_t rank_hi, axo_result **out);
+
 int axo_status(const axo_result *r);
 /* for AXO_NONFINITE: verts[0] = ball; AXO_DUPLICATE: verts[0..1];
  * AXO_DEGENERATE: verts[0..nverts-1] (sorted ball indices). */

@@ -89,6 +89,8 @@ struct axb_ctx {
     uint32_t n_pe = 0, n_pt = 0, n_pq = 0;
     int64_t counts[4] = {0, 0, 0, 0};
     size_t mark_after_grid = 0, mark_after_edges = 0;
+    bool slab_mode = false;               // grid geometry fixed by the caller (one z-slab of a global grid)
+    const int64_t *gidx = nullptr;        // slab mode: global ball index per local ball (ascending)
 };
 
 namespace {
@@ -169,18 +171,18 @@ int fetch_counters(axb_ctx *c) {
     return AXB_OK;
 }
 
-// counting sort of the balls by cell key + rank-space records (grid.cuh)
-int bin_balls(axb_ctx *c, double side, const double lo[3], const double hi[3]) {
+// counting sort of the balls by cell key + rank-space records (grid.cuh).
+// dims = dims of the GLOBAL grid; [z_lo, z_hi) = loaded z layers (the whole grid unless this is a slab).
+int bin_balls(axb_ctx *c, double side, const double lo[3], const int64_t dims[3], int64_t z_lo, int64_t z_hi) {
     const int n = (int)c->n;
-    int64_t dims[3];
-    for (int a = 0; a < 3; ++a) dims[a] = (int64_t)floor((hi[a] - lo[a]) / side) + 1;   // grid.py:121
-    // dims are at least 1; guard the product before multiplying
-    long double cells = (long double)dims[0] * (long double)dims[1] * (long double)dims[2];
-    if (cells >= (long double)MAX_CELLS)
+    const int64_t zc = z_hi - z_lo;
+    // guard the product before multiplying
+    long double cells = (long double)dims[0] * (long double)dims[1] * (long double)zc;
+    if (cells >= (long double)MAX_CELLS || dims[0] >= MAX_CELLS || dims[1] >= MAX_CELLS || dims[2] >= MAX_CELLS)
         return fail(c, AXB_ERR_GRID_TOO_LARGE,
                     "grid of %lld x %lld x %lld cells exceeds the dense cell table limit (%lld cells)", (long long)dims[0],
-                    (long long)dims[1], (long long)dims[2], (long long)MAX_CELLS);
-    const int64_t G = dims[0] * dims[1] * dims[2];
+                    (long long)dims[1], (long long)zc, (long long)MAX_CELLS);
+    const int64_t G = dims[0] * dims[1] * zc;
     c->ginfo.cell_side = side;
     for (int a = 0; a < 3; ++a) { c->ginfo.origin[a] = lo[a]; c->ginfo.dims[a] = dims[a]; }
     c->ginfo.n_cells = G;
@@ -188,7 +190,9 @@ int bin_balls(axb_ctx *c, double side, const double lo[3], const double hi[3]) {
     GridView &g = c->g;
     g.ox = lo[0]; g.oy = lo[1]; g.oz = lo[2];
     g.side = side;
-    g.dx = (int)dims[0]; g.dy = (int)dims[1]; g.dz = (int)dims[2];
+    g.dx = (int)dims[0]; g.dy = (int)dims[1]; g.dz = (int)zc;
+    g.z_lo = (int)z_lo;
+    g.dz_glob = (int)dims[2];
     g.n = n;
 
     uint32_t *cell_count;
@@ -269,6 +273,7 @@ PruneParams prune_params(axb_ctx *c) {
     P.W = c->W; P.trimask = c->trimask; P.eflag = c->eflag; P.vflag = c->vflag; P.k3 = c->k3;
     P.cnt1 = c->cnt1; P.cnt2 = c->cnt2; P.cnt3 = c->cnt3; P.vkeep = c->vkeep;
     P.ctr = c->ctr; P.biomolecule = c->prm.biomolecule;
+    P.rank_lo = c->rank_lo; P.rank_hi = c->rank_hi;
     return P;
 }
 
@@ -306,9 +311,10 @@ int report_degenerate(axb_ctx *c) {
         if (stage == ST_EDGE) {
             EstParams P = est_params(c, key);
             P.pe_cap = 0;    // count only
-            const unsigned ntiles = (unsigned)((c->rank_hi - c->rank_lo + EST_TILE - 1) / EST_TILE);
+            const int edge_hi = c->slab_mode ? (int)c->n : c->rank_hi;
+            const unsigned ntiles = (unsigned)std::max(1, (edge_hi - c->rank_lo + EST_TILE - 1) / EST_TILE);
             k_edges<<<std::max(1u, std::min(ntiles, (unsigned)c->sm_count * 4u)), EST_WARPS * 32, 0, c->stream>>>(
-                P, c->rank_lo, c->rank_hi);
+                P, c->rank_lo, edge_hi);
             LAUNCH_CHECK(c);
         } else {
             uint32_t pt_cap = c->pt_cap, pq_cap = c->pq_cap;
@@ -443,7 +449,11 @@ extern "C" int axb_stage_ms(const axb_ctx *cc, float out[AXB_ST_COUNT]) {
 
 // --------------------------------------------------------------------- grid
 
-extern "C" int axb_grid_build(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *prm) {
+namespace {
+
+// shared body of axb_grid_build / axb_grid_build_slab
+int grid_build_common(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *prm,
+                      const axb_slab *slab, const int64_t *d_gidx) {
     if (!c || !prm) return AXB_ERR_BAD_ARG;
     c->state = S_NONE;
     c->last_status = AXB_OK;
@@ -453,11 +463,16 @@ extern "C" int axb_grid_build(axb_ctx *c, int64_t n, const double *d_xyz, const 
     for (int i = 0; i < AXB_ST_COUNT + 2; ++i) c->ev_set[i] = false;
     c->arena_used = 0;
     c->arena_needed = 0;
+    c->slab_mode = slab != nullptr;
+    c->gidx = d_gidx;
     if (n <= 0) return fail(c, AXB_ERR_EMPTY, "at least one ball is required");
     if (n >= ((int64_t)1 << 31) - 1) return fail(c, AXB_ERR_BAD_ARG, "more than 2^31 - 2 balls are not supported");
     if (!d_xyz || !d_radii) return fail(c, AXB_ERR_BAD_ARG, "null input pointer");
     if (!(prm->eps_abs > 0.0) || !(prm->eps_singular > 0.0) || !isfinite(prm->alpha))
         return fail(c, AXB_ERR_BAD_ARG, "alpha must be finite and tolerances strictly positive");
+    if (slab && (!(slab->cell_side > 0.0) || slab->dims[0] < 1 || slab->dims[1] < 1 || slab->dims[2] < 1 ||
+                 slab->z_lo < 0 || slab->z_hi > slab->dims[2] || slab->z_lo >= slab->z_hi))
+        return fail(c, AXB_ERR_BAD_ARG, "bad slab geometry");
     CUDA_TRY(c, cudaSetDevice(c->device));
     c->prm = *prm;
     c->n = n;
@@ -493,16 +508,27 @@ extern "C" int axb_grid_build(axb_ctx *c, int64_t n, const double *d_xyz, const 
         c->err_nverts = 1;
         return fail(c, AXB_ERR_NONFINITE, "ball %u is not finite", b.first_bad);
     }
-    const double side_sq = b.rmax * b.rmax + prm->alpha;   // grid.py:112-113
-    const bool bad_side = !(side_sq > 0.0);
-    double side = bad_side ? 0.0 : sqrt(side_sq);          // grid.py:118
-    if (bad_side) {
-        // the reference validates duplicates BEFORE it looks at the cell side (pipeline.py:583 then 594),
-        // so bin with a stand-in side just to find them
-        double span = std::max(b.hi[0] - b.lo[0], std::max(b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]));
-        side = span > 0.0 ? span / 128.0 : 1.0;
+    bool bad_side = false;
+    if (slab) {
+        st = bin_balls(c, slab->cell_side, slab->origin, slab->dims, slab->z_lo, slab->z_hi);
+    } else {
+        const double side_sq = b.rmax * b.rmax + prm->alpha;   // grid.py:112-113
+        bad_side = !(side_sq > 0.0);
+        double side = bad_side ? 0.0 : sqrt(side_sq);          // grid.py:118
+        if (bad_side) {
+            // the reference validates duplicates BEFORE it looks at the cell side (pipeline.py:583 then 594),
+            // so bin with a stand-in side just to find them
+            double span = std::max(b.hi[0] - b.lo[0], std::max(b.hi[1] - b.lo[1], b.hi[2] - b.lo[2]));
+            side = span > 0.0 ? span / 128.0 : 1.0;
+        }
+        int64_t dims[3];
+        for (int a = 0; a < 3; ++a) {
+            double q = floor((b.hi[a] - b.lo[a]) / side) + 1.0;   // grid.py:121
+            if (!(q < 9.0e18)) return fail(c, AXB_ERR_GRID_TOO_LARGE, "grid dimension overflows");
+            dims[a] = (int64_t)q;
+        }
+        st = bin_balls(c, side, b.lo, dims, 0, dims[2]);
     }
-    st = bin_balls(c, side, b.lo, b.hi);
     if (st != AXB_OK) return st;
     st = fetch_counters(c);
     if (st != AXB_OK) return st;
@@ -513,6 +539,34 @@ extern "C" int axb_grid_build(axb_ctx *c, int64_t n, const double *d_xyz, const 
     if (st != AXB_OK) return st;
     c->mark_after_grid = c->arena_used;
     c->state = S_GRID;
+    return AXB_OK;
+}
+
+}  // namespace
+
+extern "C" int axb_grid_build(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *prm) {
+    return grid_build_common(c, n, d_xyz, d_radii, prm, nullptr, nullptr);
+}
+
+extern "C" int axb_grid_build_slab(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii,
+                                   const int64_t *d_global_index, const axb_params *prm, const axb_slab *slab) {
+    if (!slab) return AXB_ERR_BAD_ARG;
+    return grid_build_common(c, n, d_xyz, d_radii, prm, slab, d_global_index);
+}
+
+extern "C" int axb_slab_rank_range(axb_ctx *c, int64_t z_own_lo, int64_t z_own_hi, int64_t *rank_lo, int64_t *rank_hi) {
+    if (!c || !rank_lo || !rank_hi) return AXB_ERR_BAD_ARG;
+    if (c->state < S_GRID) return fail(c, AXB_ERR_STATE, "axb_slab_rank_range before axb_grid_build");
+    const GridView &g = c->g;
+    int64_t a = std::min<int64_t>(std::max<int64_t>(z_own_lo - g.z_lo, 0), g.dz);
+    int64_t b = std::min<int64_t>(std::max<int64_t>(z_own_hi - g.z_lo, 0), g.dz);
+    uint32_t v[2];
+    const size_t layer = (size_t)g.dx * g.dy;
+    CUDA_TRY(c, cudaMemcpyAsync(&v[0], c->cell_start + layer * (size_t)a, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(&v[1], c->cell_start + layer * (size_t)b, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    *rank_lo = v[0];
+    *rank_hi = v[1];
     return AXB_OK;
 }
 
@@ -556,7 +610,7 @@ int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool sync_at_end) {
     ARENA(c, c->deg, int, n);
     const size_t mark_pe = c->arena_used;
     const unsigned ntiles = (unsigned)std::max(1, (ngen + EST_TILE - 1) / EST_TILE);
-    uint64_t want = (uint64_t)16 * (uint64_t)ngen + 4096;
+    uint64_t want = (uint64_t)16 * (uint64_t)(c->slab_mode ? n - (int)lo : ngen) + 4096;
     for (int attempt = 0;; ++attempt) {
         if (want > 0xfffffff0ull) return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential edges");
         c->arena_used = mark_pe;
@@ -570,7 +624,10 @@ int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool sync_at_end) {
             CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
         }
         EstParams P = est_params(c, 0);
-        k_edges<<<std::max(1u, std::min(ntiles, (unsigned)c->sm_count * 4u)), EST_WARPS * 32, 0, c->stream>>>(P, c->rank_lo, c->rank_hi);
+        // a slab also needs the partner rows of its upper halo: inherited faces of owned tets land there
+        const int edge_hi = c->slab_mode ? n : c->rank_hi;
+        const unsigned etiles = (unsigned)std::max(1, (edge_hi - c->rank_lo + EST_TILE - 1) / EST_TILE);
+        k_edges<<<std::max(1u, std::min(etiles, (unsigned)c->sm_count * 4u)), EST_WARPS * 32, 0, c->stream>>>(P, c->rank_lo, edge_hi);
         LAUNCH_CHECK(c);
         st = fetch_counters(c);
         if (st != AXB_OK) return st;
@@ -662,11 +719,8 @@ int run_prune(axb_ctx *c) {
     k_prune_edges<<<grid, 256, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_EDGES + 1)) != AXB_OK) return st;
-    const int ngen = c->rank_hi - c->rank_lo;
-    if (ngen > 0) {
-        k_prune_vertices<<<blocks_for((size_t)ngen, 256), 256, 0, c->stream>>>(P, c->rank_lo, c->rank_hi);
-        LAUNCH_CHECK(c);
-    }
+    k_prune_vertices<<<blocks_for((size_t)n, 256), 256, 0, c->stream>>>(P, c->rank_lo, c->rank_hi);
+    LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_VERTICES + 1)) != AXB_OK) return st;
     c->state = S_PRUNED;
     return AXB_OK;
@@ -790,19 +844,19 @@ extern "C" int axb_export(axb_ctx *c, int64_t *d_v, int64_t *d_e, int64_t *d_t, 
     int st;
     if ((st = mark_event(c, AXB_ST_COUNT)) != AXB_OK) return st;
     if (d_v) {
-        k_emit_vertices<<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>((int)c->n, c->vkeep, c->voff, d_v);
+        k_emit_vertices<<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>((int)c->n, c->vkeep, c->voff, c->gidx, d_v);
         LAUNCH_CHECK(c);
     }
     if (d_e && c->counts[1]) {
-        k_emit_edges<<<blocks_for((size_t)c->counts[1], 256), 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->counts[1], d_e, c->ctr);
+        k_emit_edges<<<blocks_for((size_t)c->counts[1], 256), 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->counts[1], c->gidx, d_e, c->ctr);
         LAUNCH_CHECK(c);
     }
     if (d_t && c->counts[2]) {
-        k_emit_tris<<<blocks_for((size_t)c->counts[2], 256), 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->counts[2], d_t, c->ctr);
+        k_emit_tris<<<blocks_for((size_t)c->counts[2], 256), 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->counts[2], c->gidx, d_t, c->ctr);
         LAUNCH_CHECK(c);
     }
     if (d_q && c->counts[3]) {
-        k_emit_tets<<<blocks_for((size_t)c->counts[3], 256), 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->counts[3], d_q, c->ctr);
+        k_emit_tets<<<blocks_for((size_t)c->counts[3], 256), 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->counts[3], c->gidx, d_q, c->ctr);
         LAUNCH_CHECK(c);
     }
     return mark_event(c, AXB_ST_COUNT + 1);
@@ -875,6 +929,54 @@ extern "C" int axb_export_host(axb_ctx *c, int64_t *h_v, int64_t *h_e, int64_t *
     st = axb_sync_check(c);
     c->arena_used = mark;
     return st;
+}
+
+// -------------------------------------------------------------------- merge
+
+extern "C" int axb_merge_rows(axb_ctx *c, int k, int64_t n_index, const int64_t *d_rows, int64_t m, int64_t *d_out,
+                              int64_t *count_out) {
+    if (!c || k < 1 || k > 4 || n_index < 1 || m < 0 || !count_out) return AXB_ERR_BAD_ARG;
+    if (n_index >= ((int64_t)1 << 31) - 1 || m >= ((int64_t)1 << 32) - 16) return fail(c, AXB_ERR_BAD_ARG, "merge input too large");
+    c->state = S_NONE;          // the arena is reused from the start
+    c->arena_used = 0;
+    c->arena_needed = 0;
+    *count_out = 0;
+    if (m == 0) return AXB_OK;
+    if (!d_rows || !d_out) return fail(c, AXB_ERR_BAD_ARG, "null pointer");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    uint32_t *cnt, *off, *ucnt, *uoff;
+    int4 *tmp;
+    unsigned char *dup;
+    ARENA(c, c->ctr, Counters, 1);
+    ARENA(c, cnt, uint32_t, (size_t)n_index + 2);
+    ARENA(c, off, uint32_t, (size_t)n_index + 2);
+    ARENA(c, ucnt, uint32_t, (size_t)n_index + 2);
+    ARENA(c, uoff, uint32_t, (size_t)n_index + 2);
+    ARENA(c, tmp, int4, (size_t)m);
+    ARENA(c, dup, unsigned char, (size_t)m);
+    CUDA_TRY(c, cudaMemsetAsync(c->ctr, 0, sizeof(Counters), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * ((size_t)n_index + 2), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(ucnt, 0, sizeof(uint32_t) * ((size_t)n_index + 2), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(tmp, 0xff, sizeof(int4) * (size_t)m, c->stream));   // owner -1 = skipped
+    const unsigned nb = blocks_for((size_t)m, 256);
+    k_merge_count<<<nb, 256, 0, c->stream>>>(d_rows, (unsigned)m, k, (unsigned)n_index, cnt, c->ctr);
+    LAUNCH_CHECK(c);
+    int st = device_scan(c, cnt, (size_t)n_index, off);
+    if (st != AXB_OK) return st;
+    k_merge_scatter<<<nb, 256, 0, c->stream>>>(d_rows, (unsigned)m, k, (unsigned)n_index, cnt, off, tmp);
+    LAUNCH_CHECK(c);
+    k_merge_mark<<<nb, 256, 0, c->stream>>>(tmp, off, (unsigned)m, ucnt, dup);
+    LAUNCH_CHECK(c);
+    st = device_scan(c, ucnt, (size_t)n_index, uoff);
+    if (st != AXB_OK) return st;
+    k_merge_emit<<<nb, 256, 0, c->stream>>>(tmp, off, uoff, dup, (unsigned)m, k, d_out);
+    LAUNCH_CHECK(c);
+    CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[0], uoff + n_index, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    st = fetch_counters(c);
+    if (st != AXB_OK) return st;
+    if (c->h->ctr.overflow) return fail(c, AXB_ERR_BAD_ARG, "merge input holds an index outside [0, n_index)");
+    *count_out = c->h->totals[0];
+    return AXB_OK;
 }
 
 // ------------------------------------------------------------------- probes

@@ -74,8 +74,12 @@ __global__ void __launch_bounds__(256) k_scatter_tets(CanonParams P) {
 
 // One thread per bucket entry: its position inside the bucket is the number of
 // smaller entries; write the int64 row there.
+// `map` (optional) renames local ball indices to global ones; it is ascending, so order is preserved.
+__device__ __forceinline__ int64_t mapped(const int64_t *__restrict__ map, int v) { return map ? map[v] : (int64_t)v; }
+
 __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp, const uint32_t *__restrict__ off,
-                                                    unsigned total, int64_t *__restrict__ out, Counters *ctr) {
+                                                    unsigned total, const int64_t *__restrict__ map,
+                                                    int64_t *__restrict__ out, Counters *ctr) {
     unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= total) return;
     const int2 me = tmp[s];
@@ -86,12 +90,13 @@ __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp
         if (b < me.y) ++pos;
         else if (b == me.y && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
-    out[2 * (size_t)pos] = me.x;
-    out[2 * (size_t)pos + 1] = me.y;
+    out[2 * (size_t)pos] = mapped(map, me.x);
+    out[2 * (size_t)pos + 1] = mapped(map, me.y);
 }
 
 __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
-                                                   unsigned total, int64_t *__restrict__ out, Counters *ctr) {
+                                                   unsigned total, const int64_t *__restrict__ map,
+                                                   int64_t *__restrict__ out, Counters *ctr) {
     unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= total) return;
     const int4 me = tmp[s];
@@ -102,13 +107,14 @@ __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp,
         if (o.y < me.y || (o.y == me.y && o.z < me.z)) ++pos;
         else if (o.y == me.y && o.z == me.z && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
-    out[3 * (size_t)pos] = me.x;
-    out[3 * (size_t)pos + 1] = me.y;
-    out[3 * (size_t)pos + 2] = me.z;
+    out[3 * (size_t)pos] = mapped(map, me.x);
+    out[3 * (size_t)pos + 1] = mapped(map, me.y);
+    out[3 * (size_t)pos + 2] = mapped(map, me.z);
 }
 
 __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
-                                                   unsigned total, int64_t *__restrict__ out, Counters *ctr) {
+                                                   unsigned total, const int64_t *__restrict__ map,
+                                                   int64_t *__restrict__ out, Counters *ctr) {
     unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= total) return;
     const int4 me = tmp[s];
@@ -119,17 +125,84 @@ __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp,
         if (o.y < me.y || (o.y == me.y && (o.z < me.z || (o.z == me.z && o.w < me.w)))) ++pos;
         else if (o.y == me.y && o.z == me.z && o.w == me.w && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
-    out[4 * (size_t)pos] = me.x;
-    out[4 * (size_t)pos + 1] = me.y;
-    out[4 * (size_t)pos + 2] = me.z;
-    out[4 * (size_t)pos + 3] = me.w;
+    out[4 * (size_t)pos] = mapped(map, me.x);
+    out[4 * (size_t)pos + 1] = mapped(map, me.y);
+    out[4 * (size_t)pos + 2] = mapped(map, me.z);
+    out[4 * (size_t)pos + 3] = mapped(map, me.w);
 }
 
 __global__ void __launch_bounds__(256) k_emit_vertices(int n, const uint32_t *__restrict__ vkeep,
-                                                       const uint32_t *__restrict__ voff, int64_t *__restrict__ out) {
+                                                       const uint32_t *__restrict__ voff,
+                                                       const int64_t *__restrict__ map, int64_t *__restrict__ out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    if (vkeep[i]) out[voff[i]] = i;
+    if (vkeep[i]) out[voff[i]] = mapped(map, i);
+}
+
+// ---- merge of canonical row lists from several slabs / chunks (reference pipeline.py:611-614):
+// sorted union with duplicates removed.  Same owner-bucket scheme as above, plus a "first of its
+// equals" mark so every distinct row is written once.
+__device__ __forceinline__ int4 load_row4(const int64_t *__restrict__ rows, unsigned s, int k) {
+    int4 r = make_int4(-1, -1, -1, -1);
+    r.x = (int)rows[(size_t)s * k];
+    if (k > 1) r.y = (int)rows[(size_t)s * k + 1];
+    if (k > 2) r.z = (int)rows[(size_t)s * k + 2];
+    if (k > 3) r.w = (int)rows[(size_t)s * k + 3];
+    return r;
+}
+
+__device__ __forceinline__ bool row_less(const int4 &a, const int4 &b) {   // same owner (x)
+    return a.y < b.y || (a.y == b.y && (a.z < b.z || (a.z == b.z && a.w < b.w)));
+}
+__device__ __forceinline__ bool row_equal(const int4 &a, const int4 &b) { return a.y == b.y && a.z == b.z && a.w == b.w; }
+
+__global__ void __launch_bounds__(256) k_merge_count(const int64_t *__restrict__ rows, unsigned m, int k, unsigned n_index,
+                                                     uint32_t *__restrict__ cnt, Counters *ctr) {
+    unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= m) return;
+    const int64_t a = rows[(size_t)s * k];
+    if (a < 0 || a >= (int64_t)n_index) { atomicOr(&ctr->overflow, 1u << 6); return; }
+    atomicAdd(cnt + a, 1u);
+}
+
+__global__ void __launch_bounds__(256) k_merge_scatter(const int64_t *__restrict__ rows, unsigned m, int k, unsigned n_index,
+                                                       uint32_t *__restrict__ cnt, const uint32_t *__restrict__ off,
+                                                       int4 *__restrict__ tmp) {
+    unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= m) return;
+    const int4 r = load_row4(rows, s, k);
+    if (r.x < 0 || (unsigned)r.x >= n_index) return;
+    const unsigned slot = atomicSub(cnt + r.x, 1u) - 1u;
+    tmp[off[r.x] + slot] = r;
+}
+
+__global__ void __launch_bounds__(256) k_merge_mark(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
+                                                    unsigned m, uint32_t *__restrict__ ucnt, unsigned char *__restrict__ dup) {
+    unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= m) return;
+    const int4 me = tmp[s];
+    if (me.x < 0) { dup[s] = 1; return; }
+    const unsigned lo = off[me.x];
+    bool d = false;
+    for (unsigned q = lo; q < s && !d; ++q) d = row_equal(tmp[q], me);
+    dup[s] = d ? 1 : 0;
+    if (!d) atomicAdd(ucnt + me.x, 1u);
+}
+
+__global__ void __launch_bounds__(256) k_merge_emit(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
+                                                    const uint32_t *__restrict__ uoff, const unsigned char *__restrict__ dup,
+                                                    unsigned m, int k, int64_t *__restrict__ out) {
+    unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= m || dup[s]) return;
+    const int4 me = tmp[s];
+    const unsigned lo = off[me.x], hi = off[me.x + 1];
+    unsigned pos = uoff[me.x];
+    for (unsigned q = lo; q < hi; ++q)
+        if (!dup[q] && row_less(tmp[q], me)) ++pos;
+    out[(size_t)pos * k] = me.x;
+    if (k > 1) out[(size_t)pos * k + 1] = me.y;
+    if (k > 2) out[(size_t)pos * k + 2] = me.z;
+    if (k > 3) out[(size_t)pos * k + 3] = me.w;
 }
 
 }  // namespace axb

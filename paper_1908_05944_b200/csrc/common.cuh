@@ -20,7 +20,9 @@ struct __align__(32) Atom {   // one 32-byte sector per atom
 struct GridView {
     double ox, oy, oz;        // origin
     double side;              // cell side sqrt(r_max^2 + alpha)
-    int dx, dy, dz;           // dims
+    int dx, dy, dz;           // dims of the LOCAL table (dz = loaded z layers)
+    int z_lo;                 // first loaded z layer of the global grid (0 unless this is a slab)
+    int dz_glob;              // z layers of the global grid (== dz unless this is a slab)
     int n;                    // balls
     const uint32_t *cell_start;   // (n_cells + 1) exclusive prefix of per-cell counts
 };

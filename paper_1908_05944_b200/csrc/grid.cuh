@@ -118,7 +118,7 @@ __global__ void k_cell_keys(const double *__restrict__ xyz, GridView g, int *__r
     if (i >= g.n) return;
     int cx = cell_coord(xyz[3 * (size_t)i], g.ox, g.side, g.dx);
     int cy = cell_coord(xyz[3 * (size_t)i + 1], g.oy, g.side, g.dy);
-    int cz = cell_coord(xyz[3 * (size_t)i + 2], g.oz, g.side, g.dz);
+    int cz = cell_coord_z(xyz[3 * (size_t)i + 2], g);
     int key = cx + g.dx * (cy + g.dy * cz);
     key_of_ball[i] = key;
     atomicAdd(cell_count + key, 1u);

@@ -177,6 +177,13 @@ AXB_HD int cell_coord(double v, double origin, double side, int dim) {
     return (int)q;
 }
 
+// z layer inside the local table: global layer (clamped to the global grid exactly like the
+// reference) minus the slab offset, clamped into the loaded range
+AXB_HD int cell_coord_z(double v, const GridView &g) {
+    int iz = cell_coord(v, g.oz, g.side, g.dz_glob) - g.z_lo;
+    return iz < 0 ? 0 : (iz >= g.dz ? g.dz - 1 : iz);
+}
+
 #ifdef __CUDACC__
 // pipeline.py:286-313 for one simplex: true iff no non-incident ball of the
 // 27-cell block around the ortho-centre has power distance < size - eps_abs.
@@ -185,7 +192,7 @@ __device__ __forceinline__ bool ac2_pass(const GridView &g, const Atom *__restri
                                          double cz, double thr, int inc0, int inc1, int inc2, int inc3) {
     int ix = cell_coord(cx, g.ox, g.side, g.dx);
     int iy = cell_coord(cy, g.oy, g.side, g.dy);
-    int iz = cell_coord(cz, g.oz, g.side, g.dz);
+    int iz = cell_coord_z(cz, g);
     int x0 = max(ix - 1, 0), x1 = min(ix + 1, g.dx - 1);
     int y0 = max(iy - 1, 0), y1 = min(iy + 1, g.dy - 1);
     int z0 = max(iz - 1, 0), z1 = min(iz + 1, g.dz - 1);

@@ -414,6 +414,73 @@ class Engine:
         self._collect_stage_ms()
         return outs
 
+    # -- multi-GPU building blocks (sharding.py)
+    def compute_slab_device(self, centers, radii, global_index, cfg: PipelineConfig, plan, slab):
+        """One z-slab of a global grid: CUDA tensors of the loaded balls (ascending global index) in,
+        the four row lists in GLOBAL ball indices out (what this rank contributes to the union)."""
+        torch = self.torch
+        n = int(radii.shape[0])
+        prm = self._params(cfg)
+        geo = N.Slab((C.c_double * 3)(*[float(v) for v in plan.origin]), float(plan.cell_side),
+                     (C.c_int64 * 3)(*[int(v) for v in plan.dims]), int(slab.z_lo), int(slab.z_hi))
+        dev = f"cuda:{self.device}"
+        outs: list = []
+
+        def run():
+            lib, h = self.lib, self.handle
+            st = lib.axb_grid_build_slab(h, n, centers.data_ptr(), radii.data_ptr(), global_index.data_ptr(),
+                                         C.byref(prm), C.byref(geo))
+            if st != N.OK:
+                return st
+            lo, hi = C.c_int64(), C.c_int64()
+            st = lib.axb_slab_rank_range(h, int(slab.z_own_lo), int(slab.z_own_hi), C.byref(lo), C.byref(hi))
+            if st != N.OK:
+                return st
+            for call in (lambda: lib.axb_potential(h, lo.value, hi.value), lambda: lib.axb_prune(h)):
+                st = call()
+                if st != N.OK:
+                    return st
+            counts = (C.c_int64 * 4)()
+            st = lib.axb_canonicalize(h, counts)
+            if st != N.OK:
+                return st
+            outs.clear()
+            outs.extend(torch.empty((int(counts[d]),) if d == 0 else (int(counts[d]), d + 1), dtype=torch.int64,
+                                    device=dev) for d in range(4))
+            st = lib.axb_export(h, *(o.data_ptr() if o.numel() else None for o in outs))
+            return st if st != N.OK else lib.axb_sync_check(h)
+
+        with torch.cuda.device(self.device):
+            self._bind_stream()
+            st = self._with_arena(n, cfg, run)
+        if st != N.OK:
+            self._raise(st, cfg, centers, radii)
+        self._collect_stage_ms()
+        return outs
+
+    def merge_rows(self, rows, k: int, n_index: int):
+        """Sorted duplicate-free union of canonical rows (CUDA int64 tensor (m,k) or (m,) for k=1)."""
+        torch = self.torch
+        rows = rows.contiguous().reshape(-1, k)
+        m = int(rows.shape[0])
+        out = torch.empty((m, k), dtype=torch.int64, device=rows.device)
+        count = C.c_int64()
+
+        class _Cfg:      # only what _with_arena needs
+            alpha = 0.0
+
+        def run():
+            return self.lib.axb_merge_rows(self.handle, k, int(n_index), rows.data_ptr() if m else None, m,
+                                           out.data_ptr() if m else None, C.byref(count))
+
+        with torch.cuda.device(self.device):
+            self._bind_stream()
+            st = self._with_arena(max(m, n_index) // 8 + 1, _Cfg, run)
+        if st != N.OK:
+            raise AlphaxError(f"{self.lib.axb_status_name(st).decode()}: {self._message()}")
+        out = out[: count.value]
+        return out.reshape(-1) if k == 1 else out
+
     def ortho_batch(self, points, r2, eps_singular: float = 1e-12):
         """Device probe of the predicate arithmetic: (m,k,3),(m,k) numpy -> centres, sizes, singular."""
         torch = self.torch

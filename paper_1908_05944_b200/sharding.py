@@ -1,0 +1,190 @@
+"""Multi-GPU sharding of the hot path by grid slabs.
+
+One process per GPU.  The GLOBAL grid geometry (reference grid.py:112-127) is
+evaluated once on the host; ranks own contiguous z cell layers balanced by
+atom count, load their layers plus a 2-layer halo on each side, and generate
+exactly the simplices whose minimum-rank vertex they own -- the reference's
+chunk ownership (pipeline.py:10-15: a chunk is a contiguous range of the
+grid-sorted order, and z layers ARE contiguous rank ranges) mapped onto
+GPUs.  Why 2 layers suffice with no exchange: every simplex incident to an
+owned ball has all vertices within 2 cells of it, its ortho-centre within 1
+cell, and the domination candidates within 1 cell of the centre
+(pipeline.py:288-289, 316-320).  Like a reference chunk, a slab also emits the
+faces its kept simplices inherit even when a neighbour owns them, so the only
+collective is the final gather of counts and rows to rank 0, which takes the
+sorted duplicate-free union (pipeline.py:611-614) on its GPU.
+
+`local_compute` / `merge` are injectable so the plumbing is testable on CPU
+with the gloo backend (tests/test_sharding.py).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+HALO_LAYERS = 2
+
+
+@dataclass
+class SlabPlan:
+    origin: np.ndarray          # (3,) global grid origin
+    cell_side: float
+    dims: tuple                 # global (dx, dy, dz)
+    layer: np.ndarray           # (n,) z cell layer of every ball
+    owned: list                 # per rank: (z_own_lo, z_own_hi)
+    rank_ranges: list           # per rank: (lo, hi) in the global grid-sorted order
+
+    @property
+    def world(self) -> int:
+        return len(self.owned)
+
+
+def plan_slabs(centers: np.ndarray, radii: np.ndarray, alpha: float, world: int) -> SlabPlan:
+    """Global grid geometry + contiguous z-layer ownership balanced by atom count."""
+    centers = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 3)
+    radii = np.ascontiguousarray(radii, dtype=np.float64)
+    n = centers.shape[0]
+    if n == 0:
+        raise ValueError("cannot shard an empty input")
+    r_max = float(radii.max())
+    side_sq = r_max * r_max + alpha                         # grid.py:112-113
+    if side_sq <= 0.0:
+        raise ValueError(f"alpha={alpha} gives non-positive squared cell side (r_max={r_max})")
+    side = math.sqrt(side_sq)
+    origin = centers.min(axis=0)
+    span = centers.max(axis=0) - origin
+    dims = tuple(int(d) for d in (np.floor(span / side).astype(np.int64) + 1))      # grid.py:121
+    layer = np.clip(np.floor((centers[:, 2] - origin[2]) / side).astype(np.int64), 0, dims[2] - 1)   # grid.py:122-126
+    hist = np.bincount(layer, minlength=dims[2])
+    cum = np.concatenate([[0], np.cumsum(hist)])           # cum[z] = balls in layers < z = first grid rank of layer z
+    cuts = [0]
+    for r in range(1, world):
+        z = int(np.searchsorted(cum, r * n / world, side="left"))
+        cuts.append(min(max(z, cuts[-1]), dims[2]))
+    cuts.append(dims[2])
+    owned = [(cuts[r], cuts[r + 1]) for r in range(world)]
+    rank_ranges = [(int(cum[a]), int(cum[b])) for a, b in owned]
+    return SlabPlan(origin=origin, cell_side=side, dims=dims, layer=layer, owned=owned, rank_ranges=rank_ranges)
+
+
+@dataclass
+class SlabInput:
+    centers: np.ndarray         # balls of the loaded layers, ascending global index
+    radii: np.ndarray
+    global_index: np.ndarray    # (n_local,) int64
+    z_lo: int                   # loaded layers [z_lo, z_hi)
+    z_hi: int
+    z_own_lo: int
+    z_own_hi: int
+
+
+def slab_input(plan: SlabPlan, centers: np.ndarray, radii: np.ndarray, rank: int):
+    """The balls rank `rank` loads (owned layers + halo), or None if it owns no layer."""
+    own_lo, own_hi = plan.owned[rank]
+    if own_lo >= own_hi:
+        return None
+    z_lo = max(own_lo - HALO_LAYERS, 0)
+    z_hi = min(own_hi + HALO_LAYERS, plan.dims[2])
+    gidx = np.flatnonzero((plan.layer >= z_lo) & (plan.layer < z_hi)).astype(np.int64)
+    return SlabInput(centers=np.ascontiguousarray(centers[gidx]), radii=np.ascontiguousarray(radii[gidx]),
+                     global_index=gidx, z_lo=z_lo, z_hi=z_hi, z_own_lo=own_lo, z_own_hi=own_hi)
+
+
+def numpy_merge(parts: list, k: int) -> np.ndarray:
+    """Sorted duplicate-free union of row lists (host stand-in for Engine.merge_rows in CPU tests)."""
+    rows = [np.asarray(p, dtype=np.int64).reshape(-1, k) for p in parts]
+    cat = np.concatenate(rows, axis=0) if rows else np.empty((0, k), dtype=np.int64)
+    out = np.unique(cat, axis=0) if cat.shape[0] else cat
+    return out.reshape(-1) if k == 1 else out
+
+
+def gather_rows(local: list, dist, group=None, device="cpu"):
+    """Gather the four row lists of every rank on rank 0 (counts first, then padded rows).
+    `local` = [vertices (k0,), edges (k1,2), triangles (k2,3), tets (k3,4)] torch int64 tensors.
+    Returns on rank 0: list over dims of lists over ranks; elsewhere None."""
+    import torch
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    counts = torch.tensor([int(t.shape[0]) for t in local], dtype=torch.int64, device=device)
+    all_counts = [torch.empty_like(counts) for _ in range(world)]
+    dist.all_gather(all_counts, counts, group=group)           # the collective on counts
+    all_counts = torch.stack(all_counts).cpu().numpy()         # (world, 4)
+    gathered = []
+    for d in range(4):
+        width = d + 1
+        cap = int(all_counts[:, d].max())
+        pad = torch.zeros((max(cap, 1), width), dtype=torch.int64, device=device)
+        mine = local[d].reshape(-1, width)
+        pad[: mine.shape[0]] = mine
+        bins = [torch.empty_like(pad) for _ in range(world)] if rank == 0 else None
+        dist.gather(pad, bins, dst=0, group=group)             # the collective on rows
+        if rank == 0:
+            gathered.append([bins[r][: int(all_counts[r, d])] for r in range(world)])
+    return gathered if rank == 0 else None
+
+
+class ShardedJob:
+    """One rank's share of a sharded run: owns the local inputs on its GPU; step() computes the
+    slab, gathers everything on rank 0 and merges there."""
+
+    def __init__(self, centers, radii, cfg, rank: int, world: int, engine, dist=None, group=None):
+        import torch
+
+        self.torch = torch
+        self.cfg = cfg
+        self.rank, self.world = rank, world
+        self.engine = engine
+        self.dist, self.group = dist, group
+        self.n_global = int(np.asarray(radii).shape[0])
+        self.plan = plan_slabs(centers, radii, cfg.alpha, world)
+        self.slab = slab_input(self.plan, centers, radii, rank)
+        dev = f"cuda:{engine.device}"
+        self.device = dev
+        if self.slab is not None:
+            self.d_c = torch.as_tensor(self.slab.centers, device=dev)
+            self.d_r = torch.as_tensor(self.slab.radii, device=dev)
+            self.d_g = torch.as_tensor(self.slab.global_index, device=dev)
+
+    @property
+    def n_owned(self) -> int:
+        lo, hi = self.plan.rank_ranges[self.rank]
+        return hi - lo
+
+    def local(self):
+        torch = self.torch
+        if self.slab is None:
+            return [torch.empty((0,) if d == 0 else (0, d + 1), dtype=torch.int64, device=self.device) for d in range(4)]
+        return self.engine.compute_slab_device(self.d_c, self.d_r, self.d_g, self.cfg, self.plan, self.slab)
+
+    def step(self):
+        """Returns the four merged CUDA tensors on rank 0, None elsewhere."""
+        outs = self.local()
+        if self.world == 1:
+            parts = [[o] for o in outs]
+        else:
+            parts = gather_rows(outs, self.dist, self.group, device=self.device)
+            if parts is None:
+                return None
+        torch = self.torch
+        merged = []
+        for d in range(4):
+            cat = torch.cat([p.reshape(-1, d + 1) for p in parts[d]], dim=0)
+            merged.append(self.engine.merge_rows(cat, d + 1, self.n_global))
+        return merged
+
+
+def compute_sharded_single_gpu(centers, radii, cfg, world: int, engine):
+    """All `world` slabs one after the other on ONE GPU, then the merge: the sharded algorithm
+    without the transport (used to validate slab ownership where only one GPU is available)."""
+    import torch
+
+    jobs = [ShardedJob(centers, radii, cfg, r, world, engine) for r in range(world)]
+    per_rank = [j.local() for j in jobs]
+    merged = []
+    for d in range(4):
+        cat = torch.cat([outs[d].reshape(-1, d + 1) for outs in per_rank], dim=0)
+        merged.append(engine.merge_rows(cat, d + 1, len(radii)))
+    return merged, per_rank
