@@ -7,6 +7,7 @@
 #include "canon.cuh"
 #include "common.cuh"
 #include "estimate.cuh"
+#include "estimate2.cuh"
 #include "grid.cuh"
 #include "predicates.cuh"
 #include "prune.cuh"
@@ -15,6 +16,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -280,6 +282,21 @@ PruneParams prune_params(axb_ctx *c) {
 int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
     EstParams P = est_params(c, report_key);
     const int ngen = c->rank_hi - c->rank_lo;
+    static const bool use_v1 = getenv("AXB_TRITET_V1") != nullptr;      // A/B switch: warp-per-generator kernel
+    if (!use_v1) {
+        const unsigned ntiles = (unsigned)std::max(1, (ngen + T2_GENS - 1) / T2_GENS);
+        if (c->W == 1) {
+            const size_t smem = sizeof(T2Smem<1>);
+            CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_tri_tet2<1><<<std::min(ntiles, (unsigned)c->sm_count * 2u), T2_THREADS, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
+        } else {
+            const size_t smem = sizeof(T2Smem<4>);
+            CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_tri_tet2<4><<<std::min(ntiles, (unsigned)c->sm_count), T2_THREADS, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
+        }
+        LAUNCH_CHECK(c);
+        return AXB_OK;
+    }
     const unsigned ntiles = (unsigned)((ngen + EST_TILE - 1) / EST_TILE);
     if (c->W == 1) {
         size_t smem = sizeof(TriWarpSmem<1>) * 8;
