@@ -44,7 +44,8 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
     nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
     if not os.path.exists(nvcc):
         raise RuntimeError("nvcc not found; cannot build libalphax_b200.so")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB, os.path.join(CSRC, "alphax_b200.cu")]
+    extra = os.environ.get("AXB_NVCC_EXTRA", "").split()       # e.g. -DAXB_AC2_VARIANT=2 for A/B builds
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", LIB, os.path.join(CSRC, "alphax_b200.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -76,7 +76,7 @@ struct axb_ctx {
     double *reach = nullptr;
     uint32_t *adj_off = nullptr;
     int *deg = nullptr, *pe_u = nullptr, *pe_v = nullptr;
-    uint32_t pe_cap = 0, pt_cap = 0, pq_cap = 0;
+    uint32_t pe_cap = 0, pt_cap = 0, pq_cap = 0, k3_cap = 0;
     int4 *pt = nullptr, *pq_r = nullptr;
     int *pq_l = nullptr;
     int W = 1;
@@ -276,7 +276,15 @@ PruneParams prune_params(axb_ctx *c) {
     P.cnt1 = c->cnt1; P.cnt2 = c->cnt2; P.cnt3 = c->cnt3; P.vkeep = c->vkeep;
     P.ctr = c->ctr; P.biomolecule = c->prm.biomolecule;
     P.rank_lo = c->rank_lo; P.rank_hi = c->rank_hi;
+    P.k3_cap = c->k3_cap;
     return P;
+}
+
+int launch_edges(axb_ctx *c, const EstParams &P, int lo, int hi) {
+    const unsigned ntiles = (unsigned)std::max(1, (hi - lo + EST_TILE - 1) / EST_TILE);
+    k_edges<<<std::min(ntiles, (unsigned)c->sm_count * 4u), EST_WARPS * 32, 0, c->stream>>>(P, lo, hi);
+    LAUNCH_CHECK(c);
+    return AXB_OK;
 }
 
 int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
@@ -329,10 +337,8 @@ int report_degenerate(axb_ctx *c) {
             EstParams P = est_params(c, key);
             P.pe_cap = 0;    // count only
             const int edge_hi = c->slab_mode ? (int)c->n : c->rank_hi;
-            const unsigned ntiles = (unsigned)std::max(1, (edge_hi - c->rank_lo + EST_TILE - 1) / EST_TILE);
-            k_edges<<<std::max(1u, std::min(ntiles, (unsigned)c->sm_count * 4u)), EST_WARPS * 32, 0, c->stream>>>(
-                P, c->rank_lo, edge_hi);
-            LAUNCH_CHECK(c);
+            int st = launch_edges(c, P, c->rank_lo, edge_hi);
+            if (st != AXB_OK) return st;
         } else {
             uint32_t pt_cap = c->pt_cap, pq_cap = c->pq_cap;
             c->pt_cap = 0; c->pq_cap = 0;
@@ -608,7 +614,8 @@ extern "C" int axb_grid_export(axb_ctx *c, int64_t *d_order, int64_t *d_rank, in
 
 namespace {
 
-int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool sync_at_end) {
+// potential edges for generators [lo, hi) (+ the upper halo rows of a slab); synchronises once
+int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
     if (c->state < S_GRID) return fail(c, AXB_ERR_STATE, "axb_potential before axb_grid_build");
     if (lo < 0 || hi > c->n || lo > hi) return fail(c, AXB_ERR_BAD_ARG, "bad rank range");
     c->state = S_GRID;
@@ -626,7 +633,6 @@ int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool sync_at_end) {
     ARENA(c, c->adj_off, uint32_t, n);
     ARENA(c, c->deg, int, n);
     const size_t mark_pe = c->arena_used;
-    const unsigned ntiles = (unsigned)std::max(1, (ngen + EST_TILE - 1) / EST_TILE);
     uint64_t want = (uint64_t)16 * (uint64_t)(c->slab_mode ? n - (int)lo : ngen) + 4096;
     for (int attempt = 0;; ++attempt) {
         if (want > 0xfffffff0ull) return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential edges");
@@ -643,9 +649,8 @@ int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool sync_at_end) {
         EstParams P = est_params(c, 0);
         // a slab also needs the partner rows of its upper halo: inherited faces of owned tets land there
         const int edge_hi = c->slab_mode ? n : c->rank_hi;
-        const unsigned etiles = (unsigned)std::max(1, (edge_hi - c->rank_lo + EST_TILE - 1) / EST_TILE);
-        k_edges<<<std::max(1u, std::min(etiles, (unsigned)c->sm_count * 4u)), EST_WARPS * 32, 0, c->stream>>>(P, c->rank_lo, edge_hi);
-        LAUNCH_CHECK(c);
+        st = launch_edges(c, P, c->rank_lo, edge_hi);
+        if (st != AXB_OK) return st;
         st = fetch_counters(c);
         if (st != AXB_OK) return st;
         if (c->h->ctr.n_pe <= c->pe_cap) break;
@@ -660,7 +665,12 @@ int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool sync_at_end) {
     c->n_pe = c->h->ctr.n_pe;
     c->W = c->h->ctr.max_deg <= 64 ? 1 : 4;
     c->mark_after_edges = c->arena_used;
+    return AXB_OK;
+}
 
+// potential triangles + tets into global lists (the standalone stage path); synchronises
+int run_tri_tet_lists(axb_ctx *c) {
+    int st;
     uint64_t pt_want = c->h->ctr.pair_bound + 32;           // every potential triangle is a partner pair
     uint64_t pq_want = c->h->ctr.pair_bound + 4096;         // first guess; re-run on overflow
     for (int attempt = 0;; ++attempt) {
@@ -679,10 +689,6 @@ int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool sync_at_end) {
         }
         st = launch_tri_tet(c, 0);
         if (st != AXB_OK) return st;
-        if (!sync_at_end && attempt == 0) {
-            // optimistic path of axb_compute: overflow and singular flags are checked at the next sync
-            break;
-        }
         st = fetch_counters(c);
         if (st != AXB_OK) return st;
         if (c->h->ctr.n_pq <= c->pq_cap && c->h->ctr.n_pt <= c->pt_cap) break;
@@ -690,33 +696,36 @@ int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool sync_at_end) {
         pq_want = (uint64_t)c->h->ctr.n_pq + 1024;
         pt_want = std::max<uint64_t>(pt_want, (uint64_t)c->h->ctr.n_pt + 32);
     }
-    st = mark_event(c, AXB_ST_POT_TRIANGLES + 1);
-    if (st != AXB_OK) return st;
-    st = mark_event(c, AXB_ST_POT_TETS + 1);     // triangles and tets are one fused kernel
-    if (st != AXB_OK) return st;
-    if (sync_at_end) {
-        st = check_run_flags(c);
-        if (st != AXB_OK) return st;
-        c->n_pt = c->h->ctr.n_pt;
-        c->n_pq = c->h->ctr.n_pq;
-    }
+    if ((st = mark_event(c, AXB_ST_POT_TRIANGLES + 1)) != AXB_OK) return st;
+    if ((st = mark_event(c, AXB_ST_POT_TETS + 1)) != AXB_OK) return st;     // one kernel does both
+    if ((st = check_run_flags(c)) != AXB_OK) return st;
+    c->n_pt = c->h->ctr.n_pt;
+    c->n_pq = c->h->ctr.n_pq;
+    c->k3_cap = c->pq_cap;
     c->state = S_POTENTIAL;
     return AXB_OK;
 }
 
-int run_prune(axb_ctx *c) {
-    if (c->state < S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_prune before axb_potential");
+int run_potential(axb_ctx *c, int64_t lo, int64_t hi) {
+    int st = run_edges(c, lo, hi);
+    if (st != AXB_OK) return st;
+    return run_tri_tet_lists(c);
+}
+
+// kept-simplex state of the pruning stage (prune.cuh), zeroed
+int alloc_prune_arrays(axb_ctx *c) {
     const int n = (int)c->n;
-    ARENA(c, c->trimask, unsigned long long, (size_t)std::max<uint32_t>(c->n_pe, 1) * c->W);
-    ARENA(c, c->eflag, unsigned int, std::max<uint32_t>(c->n_pe, 1));
+    const size_t rows = (size_t)std::max<uint32_t>(c->n_pe, 1);
+    ARENA(c, c->trimask, unsigned long long, rows * c->W);
+    ARENA(c, c->eflag, unsigned int, rows);
     ARENA(c, c->vflag, unsigned char, n);
-    ARENA(c, c->k3, int4, std::max<uint32_t>(c->pq_cap, 1));
+    ARENA(c, c->k3, int4, std::max<uint32_t>(c->k3_cap, 1));
     ARENA(c, c->cnt1, uint32_t, (size_t)n + 1);
     ARENA(c, c->cnt2, uint32_t, (size_t)n + 1);
     ARENA(c, c->cnt3, uint32_t, (size_t)n + 1);
     ARENA(c, c->vkeep, uint32_t, (size_t)n + 1);
-    CUDA_TRY(c, cudaMemsetAsync(c->trimask, 0, sizeof(unsigned long long) * (size_t)std::max<uint32_t>(c->n_pe, 1) * c->W, c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->eflag, 0, sizeof(unsigned int) * std::max<uint32_t>(c->n_pe, 1), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->trimask, 0, sizeof(unsigned long long) * rows * c->W, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->eflag, 0, sizeof(unsigned int) * rows, c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->vflag, 0, (size_t)n, c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->cnt1, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->cnt2, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
@@ -724,23 +733,36 @@ int run_prune(axb_ctx *c) {
     CUDA_TRY(c, cudaMemsetAsync(c->vkeep, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(&c->ctr->n_k3, 0, sizeof(unsigned int), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(&c->ctr->lookup_miss, 0, sizeof(unsigned int), c->stream));
+    return AXB_OK;
+}
+
+// triangles, edges, vertices of the pruning stage (the tets are done by the caller)
+int run_prune_lower(axb_ctx *c) {
     PruneParams P = prune_params(c);
     const unsigned grid = (unsigned)c->sm_count * 8u;
     int st;
-    k_prune_tets<<<grid, 256, 0, c->stream>>>(P);
-    LAUNCH_CHECK(c);
-    if ((st = mark_event(c, AXB_ST_PRUNE_TETS + 1)) != AXB_OK) return st;
-    k_prune_tris<<<grid, 256, 0, c->stream>>>(P);
+    k_prune_tris<<<grid, PRUNE_THREADS, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_TRIANGLES + 1)) != AXB_OK) return st;
-    k_prune_edges<<<grid, 256, 0, c->stream>>>(P);
+    k_prune_edges<<<grid, PRUNE_THREADS, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_EDGES + 1)) != AXB_OK) return st;
-    k_prune_vertices<<<blocks_for((size_t)n, 256), 256, 0, c->stream>>>(P, c->rank_lo, c->rank_hi);
+    k_prune_vertices<<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>(P, c->rank_lo, c->rank_hi);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_VERTICES + 1)) != AXB_OK) return st;
     c->state = S_PRUNED;
     return AXB_OK;
+}
+
+int run_prune(axb_ctx *c) {
+    if (c->state < S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_prune before axb_potential");
+    int st = alloc_prune_arrays(c);
+    if (st != AXB_OK) return st;
+    PruneParams P = prune_params(c);
+    k_prune_tets<<<(unsigned)c->sm_count * 8u, 256, 0, c->stream>>>(P);
+    LAUNCH_CHECK(c);
+    if ((st = mark_event(c, AXB_ST_PRUNE_TETS + 1)) != AXB_OK) return st;
+    return run_prune_lower(c);
 }
 
 int run_canonicalize(axb_ctx *c, int64_t counts[4]) {
@@ -761,7 +783,8 @@ int run_canonicalize(axb_ctx *c, int64_t counts[4]) {
     CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[3], c->off3 + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     if ((st = fetch_counters(c)) != AXB_OK) return st;
     // deferred checks of the optimistic potential stage
-    if (c->h->ctr.n_pq > c->pq_cap || c->h->ctr.n_pt > c->pt_cap) return AXB_ERR_ARENA + 1000;   // sentinel: caller re-runs
+    if (c->h->ctr.n_pq > c->pq_cap || c->h->ctr.n_pt > c->pt_cap || c->h->ctr.n_k3 > c->k3_cap)
+        return AXB_ERR_ARENA + 1000;                       // sentinel: a guessed buffer was too small, caller re-runs
     if ((st = check_run_flags(c)) != AXB_OK) return st;
     c->n_pt = c->h->ctr.n_pt;
     c->n_pq = c->h->ctr.n_pq;
@@ -789,7 +812,7 @@ int run_canonicalize(axb_ctx *c, int64_t counts[4]) {
 
 extern "C" int axb_potential(axb_ctx *c, int64_t lo, int64_t hi) {
     if (!c) return AXB_ERR_BAD_ARG;
-    return run_potential(c, lo, hi, true);
+    return run_potential(c, lo, hi);
 }
 
 extern "C" int axb_potential_counts(const axb_ctx *c, int64_t counts[3]) {
@@ -833,6 +856,8 @@ extern "C" int axb_potential_export(axb_ctx *c, int what, int64_t *d_rows, doubl
     if (!c) return AXB_ERR_BAD_ARG;
     if (c->state < S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_potential_export before axb_potential");
     if (what < AXB_PE || what > AXB_PQ) return fail(c, AXB_ERR_BAD_ARG, "what must be AXB_PE, AXB_PT or AXB_PQ");
+    if (what == AXB_PQ && c->pq_r == nullptr)
+        return fail(c, AXB_ERR_STATE, "the potential-tet list is not materialised by axb_compute (fused path); use axb_potential");
     unsigned m = what == AXB_PE ? c->n_pe : (what == AXB_PT ? c->n_pt : c->n_pq);
     if (m) {
         k_export_potential<<<blocks_for(m, 128), 128, 0, c->stream>>>(what, m, c->atoms, c->orig, c->pe_u, c->pe_v, c->pt,
@@ -891,20 +916,11 @@ extern "C" int axb_compute(axb_ctx *c, int64_t n, const double *d_xyz, const dou
     if (!c) return AXB_ERR_BAD_ARG;
     int st = axb_grid_build(c, n, d_xyz, d_radii, prm);
     if (st != AXB_OK) return st;
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        st = run_potential(c, 0, n, attempt > 0);
-        if (st != AXB_OK) return st;
-        if (attempt == 0) {        // counts of the optimistic run are not on the host yet; prune sizes by capacity
-            c->n_pt = c->pt_cap;
-            c->n_pq = c->pq_cap;
-        }
-        st = run_prune(c);
-        if (st != AXB_OK) return st;
-        st = run_canonicalize(c, counts);
-        if (st != AXB_ERR_ARENA + 1000) return st;
-        // potential-tet buffer overflowed: second attempt sizes it exactly
-    }
-    return fail(c, AXB_ERR_INTERNAL, "potential buffers overflowed twice");
+    if ((st = run_potential(c, 0, n)) != AXB_OK) return st;
+    if ((st = run_prune(c)) != AXB_OK) return st;
+    st = run_canonicalize(c, counts);
+    if (st == AXB_ERR_ARENA + 1000) return fail(c, AXB_ERR_INTERNAL, "a potential list overflowed after it was sized exactly");
+    return st;
 }
 
 extern "C" int axb_compute_host(axb_ctx *c, int64_t n, const double *h_xyz, const double *h_radii, const axb_params *prm,

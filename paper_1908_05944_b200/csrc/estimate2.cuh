@@ -51,6 +51,8 @@ struct T2Smem {
     } u;
     unsigned char sgen[T2_SCAP], sli[T2_SCAP];
     int wtot[T2_WARPS + 1];
+    int qoff[T2_WARPS];
+    unsigned pt_base, pq_base;
     int npass;
     int g1;
 };
@@ -241,6 +243,10 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int ran
                 }
                 __syncthreads();
                 const int ntri = block_scan_excl(S.rowpre, nslots, S.wtot);
+                // one contiguous run of the global triangle list per tile: the prune kernel that reads it
+                // then works on one neighbourhood at a time (L1 locality)
+                if (tid == 0 && ntri > 0) S.pt_base = atomicAdd(&P.ctr->n_pt, (unsigned)ntri);
+                __syncthreads();
                 for (int tc0 = 0; tc0 < ntri; tc0 += T2_TCAP) {
                     const int ntc = min(T2_TCAP, ntri - tc0);
                     for (int x0 = 0; x0 < ntc; x0 += T2_THREADS) {
@@ -268,15 +274,9 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int ran
                             S.u.t.cpre[x] = cnt;
                             entry = make_int4(t0 + g0 + g, S.srank[s], S.srank[sj], (int)S.sli[s] | (j << 16));
                         }
-                        const unsigned m = __ballot_sync(FULL, valid);
-                        if (m) {
-                            unsigned base = 0;
-                            if (lane == 0) base = atomicAdd(&P.ctr->n_pt, (unsigned)__popc(m));
-                            base = __shfl_sync(FULL, base, 0);
-                            if (valid) {
-                                const unsigned pos = base + (unsigned)__popc(m & lanemask_lt());
-                                if (pos < P.pt_cap) P.pt[pos] = entry;
-                            }
+                        if (valid) {
+                            const unsigned pos = S.pt_base + (unsigned)(tc0 + x);
+                            if (pos < P.pt_cap) P.pt[pos] = entry;
                         }
                     }
                     __syncthreads();
@@ -319,16 +319,22 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int ran
                             er = make_int4(t, S.srank[s], S.srank[sj], S.srank[sk]);
                             el = (int)S.sli[s] | (j << 8) | (k << 16);
                         }
+                        // block-level compaction: one global atomic per round, kept tets of a tile stay together
                         const unsigned m = __ballot_sync(FULL, keep);
-                        if (m) {
-                            unsigned base = 0;
-                            if (lane == 0) base = atomicAdd(&P.ctr->n_pq, (unsigned)__popc(m));
-                            base = __shfl_sync(FULL, base, 0);
-                            if (keep) {
-                                const unsigned pos = base + (unsigned)__popc(m & lanemask_lt());
-                                if (pos < P.pq_cap) { P.pq_r[pos] = er; P.pq_l[pos] = el; }
-                            }
+                        if (lane == 0) S.qoff[tid >> 5] = __popc(m);
+                        __syncthreads();
+                        if (tid == 0) {
+                            int tot = 0;
+#pragma unroll
+                            for (int w = 0; w < T2_WARPS; ++w) { const int cw = S.qoff[w]; S.qoff[w] = tot; tot += cw; }
+                            S.pq_base = tot ? atomicAdd(&P.ctr->n_pq, (unsigned)tot) : 0u;
                         }
+                        __syncthreads();
+                        if (keep) {
+                            const unsigned pos = S.pq_base + (unsigned)S.qoff[tid >> 5] + (unsigned)__popc(m & lanemask_lt());
+                            if (pos < P.pq_cap) { P.pq_r[pos] = er; P.pq_l[pos] = el; }
+                        }
+                        __syncthreads();
                     }
                     __syncthreads();
                 }

@@ -47,12 +47,24 @@ struct PruneParams {
     Counters *ctr;
     int biomolecule;
     int rank_lo, rank_hi;             // generators this call owns; rows of other generators only receive marks
+    uint32_t k3_cap;                  // capacity of k3
 };
 
+// slot of `target` in a generator's partner list; four independent loads per round, no early exit
+// inside a round (the list has ~5-20 entries, so this is 2-5 memory round trips instead of up to 20)
 __device__ __forceinline__ int find_partner(const int *__restrict__ pe_v, unsigned base, int d, int target) {
-    for (int q = 0; q < d; ++q)
-        if (__ldg(pe_v + base + q) == target) return q;
-    return -1;
+    int hit = -1;
+    for (int q = 0; q < d && hit < 0; q += 4) {
+        const int a0 = __ldg(pe_v + base + q);
+        const int a1 = __ldg(pe_v + base + min(q + 1, d - 1));
+        const int a2 = __ldg(pe_v + base + min(q + 2, d - 1));
+        const int a3 = __ldg(pe_v + base + min(q + 3, d - 1));
+        if (a3 == target) hit = min(q + 3, d - 1);
+        if (a2 == target) hit = min(q + 2, d - 1);
+        if (a1 == target) hit = min(q + 1, d - 1);
+        if (a0 == target) hit = q;
+    }
+    return hit;
 }
 
 __device__ __forceinline__ void mark_tri(const PruneParams &P, unsigned row, int j, int owner) {
@@ -99,7 +111,7 @@ __global__ void __launch_bounds__(256) k_prune_tets(PruneParams P) {
             for (int b = a; b > 0; --b)
                 if (row[b - 1] > row[b]) { int t = row[b]; row[b] = row[b - 1]; row[b - 1] = t; }
         const unsigned slot = atomicAdd(&P.ctr->n_k3, 1u);
-        P.k3[slot] = make_int4(row[0], row[1], row[2], row[3]);
+        if (slot < P.k3_cap) P.k3[slot] = make_int4(row[0], row[1], row[2], row[3]);
         atomicAdd(P.cnt3 + row[0], 1u);
         // faces and edges generated by u (partner slots i < j < k of u)
         const unsigned bu = __ldg(P.adj_off + r.x);
@@ -123,44 +135,107 @@ __global__ void __launch_bounds__(256) k_prune_tets(PruneParams P) {
     }
 }
 
+// Block-level work compaction for the two kernels below: most potential triangles / edges are
+// already kept by inheritance, so a block first scans PRUNE_BATCH x 256 entries, queues the free
+// ones in shared memory and then runs the expensive part (ortho solve + AC2) with packed lanes.
+constexpr int PRUNE_THREADS = 256;
+constexpr int PRUNE_BATCH = 4;
+
+__device__ __forceinline__ void queue_push(bool want, unsigned value, unsigned *queue, int *qn) {
+    const unsigned m = __ballot_sync(FULL, want);
+    if (m) {
+        int base = 0;
+        const int leader = __ffs(m) - 1;
+        if (lane_id() == leader) base = atomicAdd(qn, __popc(m));
+        base = __shfl_sync(FULL, base, leader);
+        if (want) queue[base + __popc(m & lanemask_lt())] = value;
+    }
+}
+
 // pipeline.py:502-505: AC2 for the triangles no kept tet inherited
-__global__ void __launch_bounds__(256) k_prune_tris(PruneParams P) {
+__global__ void __launch_bounds__(PRUNE_THREADS) k_prune_tris(PruneParams P) {
+    __shared__ unsigned queue[PRUNE_THREADS * PRUNE_BATCH];
+    __shared__ int qn;
     if (lists_overflowed(P)) return;
     const unsigned n_pt = min(P.ctr->n_pt, P.pt_cap);
-    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pt; e += gridDim.x * blockDim.x) {
-        const int4 r = P.pt[e];
-        const int i = r.w & 0xffff, j = r.w >> 16;
-        const unsigned bu = __ldg(P.adj_off + r.x);
-        const unsigned long long word = P.trimask[(size_t)(bu + i) * P.W + (j >> 6)];
-        if ((word >> (j & 63)) & 1ull) continue;          // inherited: not free
-        const Atom au = load_atom(P.atoms, r.x), av = load_atom(P.atoms, r.y), aw = load_atom(P.atoms, r.z);
-        const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z);
-        const Ortho o = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);
-        if (!ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, -1)) continue;
-        mark_tri(P, bu + i, j, min3(ou, ov, ow));
-        mark_edge(P, bu + i, min(ou, ov));
-        mark_edge(P, bu + j, min(ou, ow));
-        const unsigned bv = __ldg(P.adj_off + r.y);
-        const int iw = find_partner(P.pe_v, bv, __ldg(P.deg + r.y), r.z);
-        if (iw >= 0) mark_edge(P, bv + iw, min(ov, ow)); else note_miss(P);
+    const unsigned span = PRUNE_THREADS * PRUNE_BATCH;
+    for (unsigned base = blockIdx.x * span; base < n_pt; base += gridDim.x * span) {
+        if (threadIdx.x == 0) qn = 0;
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < PRUNE_BATCH; ++b) {
+            const unsigned e = base + b * PRUNE_THREADS + threadIdx.x;
+            bool is_free = false;
+            if (e < n_pt) {
+                const int4 r = P.pt[e];
+                const int i = r.w & 0xffff, j = r.w >> 16;
+                const unsigned bu = __ldg(P.adj_off + r.x);
+                const unsigned long long word = P.trimask[(size_t)(bu + i) * P.W + (j >> 6)];
+                is_free = !((word >> (j & 63)) & 1ull);       // not inherited from a kept tet
+            }
+            queue_push(is_free, e, queue, &qn);
+        }
+        __syncthreads();
+        const int nq = qn;
+        for (int x = threadIdx.x; x < nq; x += PRUNE_THREADS) {
+            const int4 r = P.pt[queue[x]];
+            const int i = r.w & 0xffff, j = r.w >> 16;
+            const unsigned bu = __ldg(P.adj_off + r.x);
+            const Atom au = load_atom(P.atoms, r.x), av = load_atom(P.atoms, r.y), aw = load_atom(P.atoms, r.z);
+            const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z);
+            const Ortho o = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);
+            if (!ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, -1)) continue;
+            mark_tri(P, bu + i, j, min3(ou, ov, ow));
+            mark_edge(P, bu + i, min(ou, ov));
+            mark_edge(P, bu + j, min(ou, ow));
+            const unsigned bv = __ldg(P.adj_off + r.y);
+            const int iw = find_partner(P.pe_v, bv, __ldg(P.deg + r.y), r.z);
+            if (iw >= 0) mark_edge(P, bv + iw, min(ov, ow)); else note_miss(P);
+        }
+        __syncthreads();
     }
 }
 
 // pipeline.py:510-513: AC2 for the edges nothing inherited; kept edges mark their endpoints
-__global__ void __launch_bounds__(256) k_prune_edges(PruneParams P) {
+__global__ void __launch_bounds__(PRUNE_THREADS) k_prune_edges(PruneParams P) {
+    __shared__ unsigned queue[PRUNE_THREADS * PRUNE_BATCH];
+    __shared__ int qn;
     if (lists_overflowed(P)) return;
     const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
-    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pe; e += gridDim.x * blockDim.x) {
-        const int u = __ldg(P.pe_u + e), v = __ldg(P.pe_v + e);
-        bool kept = P.eflag[e] != 0u;
-        if (!kept && u >= P.rank_lo && u < P.rank_hi) {   // halo rows of a slab are never tested here: their owner does it
+    const unsigned span = PRUNE_THREADS * PRUNE_BATCH;
+    for (unsigned base = blockIdx.x * span; base < n_pe; base += gridDim.x * span) {
+        if (threadIdx.x == 0) qn = 0;
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < PRUNE_BATCH; ++b) {
+            const unsigned e = base + b * PRUNE_THREADS + threadIdx.x;
+            bool is_free = false;
+            if (e < n_pe) {
+                const int u = __ldg(P.pe_u + e);
+                if (P.eflag[e] != 0u) {                       // inherited: its endpoints are kept
+                    P.vflag[u] = 1;
+                    P.vflag[__ldg(P.pe_v + e)] = 1;
+                } else {
+                    is_free = u >= P.rank_lo && u < P.rank_hi;   // halo rows of a slab are their owner's business
+                }
+            }
+            queue_push(is_free, e, queue, &qn);
+        }
+        __syncthreads();
+        const int nq = qn;
+        for (int x = threadIdx.x; x < nq; x += PRUNE_THREADS) {
+            const unsigned e = queue[x];
+            const int u = __ldg(P.pe_u + e), v = __ldg(P.pe_v + e);
             const Atom au = load_atom(P.atoms, u), av = load_atom(P.atoms, v);
             const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + v);
             const Ortho o = ortho_edge(ou, au, ov, av, P.tol.eps_sing);
-            kept = ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, u, v, -1, -1);
-            if (kept) mark_edge(P, e, min(ou, ov));
+            if (ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, u, v, -1, -1)) {
+                mark_edge(P, e, min(ou, ov));
+                P.vflag[u] = 1;
+                P.vflag[v] = 1;
+            }
         }
-        if (kept) { P.vflag[u] = 1; P.vflag[v] = 1; }
+        __syncthreads();
     }
 }
 
