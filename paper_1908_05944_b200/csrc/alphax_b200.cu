@@ -70,7 +70,8 @@ struct axb_ctx {
     Counters *ctr = nullptr;
     ErrRecord *errs = nullptr;
     int2 *dups = nullptr;
-    int *key_of_ball = nullptr, *key_of_rank = nullptr, *orig = nullptr, *rank = nullptr;
+    int *key_of_ball = nullptr, *orig = nullptr, *rank = nullptr;
+    int4 *cell_of_rank = nullptr;
     uint32_t *cell_start = nullptr;
     Atom *atoms = nullptr;
     double *reach = nullptr;
@@ -203,7 +204,7 @@ int bin_balls(axb_ctx *c, double side, const double lo[3], const int64_t dims[3]
     ARENA(c, c->cell_start, uint32_t, (size_t)G + 2);
     ARENA(c, c->orig, int, n);
     ARENA(c, c->rank, int, n);
-    ARENA(c, c->key_of_rank, int, n);
+    ARENA(c, c->cell_of_rank, int4, n);
     ARENA(c, c->atoms, Atom, n);
     ARENA(c, c->reach, double, n);
     const size_t mark = c->arena_used;          // everything below is scratch of this function
@@ -220,7 +221,7 @@ int bin_balls(axb_ctx *c, double side, const double lo[3], const int64_t dims[3]
     LAUNCH_CHECK(c);
     k_cell_finalize<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->d_xyz, c->d_radii, c->key_of_ball, c->cell_start,
                                                              arrival, c->prm.alpha, c->prm.eps_abs, c->orig, c->rank,
-                                                             c->key_of_rank, c->atoms, c->reach, c->ctr, c->dups);
+                                                             c->cell_of_rank, g.dx, g.dy, c->atoms, c->reach, c->ctr, c->dups);
     LAUNCH_CHECK(c);
     // the scratch is dead once the stream has passed k_cell_finalize; later stages
     // are ordered on the same stream, so it can be handed out again
@@ -259,7 +260,7 @@ int report_duplicate(axb_ctx *c, unsigned ndup) {
 EstParams est_params(axb_ctx *c, unsigned long long report_key) {
     EstParams P;
     P.g = c->g; P.tol = c->tol;
-    P.atoms = c->atoms; P.reach = c->reach; P.orig = c->orig; P.key_of_rank = c->key_of_rank;
+    P.atoms = c->atoms; P.reach = c->reach; P.orig = c->orig; P.cell_of_rank = c->cell_of_rank;
     P.adj_off = c->adj_off; P.deg = c->deg; P.pe_v = c->pe_v; P.pe_u = c->pe_u; P.pe_cap = c->pe_cap;
     P.pt = c->pt; P.pt_cap = c->pt_cap; P.pq_r = c->pq_r; P.pq_l = c->pq_l; P.pq_cap = c->pq_cap;
     P.ctr = c->ctr; P.errs = c->errs; P.report_key = report_key;

@@ -25,6 +25,7 @@ constexpr int EBUF = 512;      // partner ranks staged per warp
 constexpr int EGEN = 32;       // generators staged per warp
 constexpr int MAXP = 256;      // AXB_MAX_PARTNERS
 constexpr int EST_TILE = 64;   // consecutive ranks handled by one block at a time
+constexpr int ROWOF_CAP = 128; // candidates per generator covered by the stamped row table
 
 struct EstParams {
     GridView g;
@@ -32,7 +33,7 @@ struct EstParams {
     const Atom *atoms;
     const double *reach;
     const int *orig;            // ball index per rank
-    const int *key_of_rank;
+    const int4 *cell_of_rank;   // (cx, cy, cz, key) per rank
     uint32_t *adj_off;          // per rank: start of the partner list in pe_v
     int *deg;                   // per rank: number of partners (pre-zeroed)
     int *pe_v;                  // partner rank per potential edge
@@ -74,12 +75,13 @@ __device__ __noinline__ void record_singular(const EstParams &P, unsigned long l
 }
 
 // ---------------------------------------------------------------- k_edges
-__global__ void __launch_bounds__(EST_WARPS * 32) k_edges(EstParams P, int rank_lo, int rank_hi) {
+__global__ void __launch_bounds__(EST_WARPS * 32, 4) k_edges(EstParams P, int rank_lo, int rank_hi) {
     __shared__ int s_buf[EST_WARPS][EBUF];
     __shared__ int s_gen[EST_WARPS][EGEN];
     __shared__ int s_goff[EST_WARPS][EGEN + 1];
     __shared__ int s_rs[EST_WARPS][16];
     __shared__ int s_rp[EST_WARPS][16];
+    __shared__ unsigned char s_rowof[EST_WARPS][ROWOF_CAP];   // candidate number -> row (stamped by the row lanes)
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const GridView &g = P.g;
     int nbuf = 0, ngen = 0;                 // warp-uniform staging state
@@ -123,9 +125,8 @@ __global__ void __launch_bounds__(EST_WARPS * 32) k_edges(EstParams P, int rank_
             if (!(ru >= 0.0)) continue;                     // not viable (pipeline.py:336-337)
             const Atom au = load_atom(P.atoms, t);
             const int ou = __ldg(P.orig + t);
-            const int key = __ldg(P.key_of_rank + t);
-            const int cx = key % g.dx, rest = key / g.dx;
-            const int cy = rest % g.dy, cz = rest / g.dy;
+            const int4 cell = __ldg(P.cell_of_rank + t);
+            const int cx = cell.x, cy = cell.y, cz = cell.z;
             // the 13 rows of the 5x5x5 block whose balls can out-rank t (pipeline.py:332-338)
             int rs = 0, rc = 0;
             if (lane < 13) {
@@ -149,6 +150,10 @@ __global__ void __launch_bounds__(EST_WARPS * 32) k_edges(EstParams P, int rank_
             if (nbuf + min(total, MAXP) > EBUF || ngen == EGEN) flush();
             __syncwarp();
             if (lane < 16) { s_rs[warp][lane] = rs; s_rp[warp][lane] = incl - rc; }
+            if (lane < 13) {                                // stamp: candidate number -> row
+                const int pe = min(incl, ROWOF_CAP);
+                for (int p = incl - rc; p < pe; ++p) s_rowof[warp][p] = (unsigned char)lane;
+            }
             __syncwarp();
             int deg = 0;
             for (int p0 = 0; p0 < total; p0 += 32) {
@@ -156,9 +161,14 @@ __global__ void __launch_bounds__(EST_WARPS * 32) k_edges(EstParams P, int rank_
                 bool keep = false;
                 int cand = -1;
                 if (p < total) {
-                    int r = 0;
+                    int r;
+                    if (p < ROWOF_CAP) {
+                        r = s_rowof[warp][p];
+                    } else {
+                        r = 0;
 #pragma unroll
-                    for (int k = 1; k < 13; ++k) r += (s_rp[warp][k] <= p) ? 1 : 0;
+                        for (int k = 1; k < 13; ++k) r += (s_rp[warp][k] <= p) ? 1 : 0;
+                    }
                     cand = s_rs[warp][r] + (p - s_rp[warp][r]);
                     const double rv = __ldg(P.reach + cand);
                     const Atom av = load_atom(P.atoms, cand);

@@ -27,8 +27,8 @@ constexpr int T2_THREADS = 256;
 constexpr int T2_WARPS = T2_THREADS / 32;
 constexpr int T2_GENS = 128;       // generators per tile
 constexpr int T2_SCAP = 1024;      // partner slots per sub-pass (>= 64 * W so one generator always fits)
-constexpr int T2_PLCAP = 8192;     // passing pairs per round
 constexpr int T2_TCAP = 4096;      // triangles per round
+constexpr int T2_WQCAP = 1024;     // reach-passing pairs queued per warp
 
 template <int W>
 struct T2Smem {
@@ -43,7 +43,7 @@ struct T2Smem {
     int sp[T2_GENS + 1];           // slot prefix of the sub-pass
     int pp[T2_GENS + 1];           // pair prefix of the sub-pass
     union {
-        int passlist[T2_PLCAP];
+        unsigned wq[T2_WARPS][T2_WQCAP];       // phase B: per-warp queue of reach-passing pairs (slot i | slot j << 16)
         struct {
             unsigned short tri_si[T2_TCAP], tri_sj[T2_TCAP];
             int cpre[T2_TCAP + 1];
@@ -55,6 +55,7 @@ struct T2Smem {
     unsigned pt_base, pq_base;
     int npass;
     int g1;
+    int fits;
 };
 
 // largest idx in [0, n) with pre[idx] <= v (pre = exclusive prefix, pre[0] = 0)
@@ -129,23 +130,45 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int ran
             S.gdeg[tid] = d;
         }
         __syncthreads();
+        // slot / pair prefixes of the whole window (warp 0, four generators per lane)
+        if (tid < 32) {
+            int d[4], ls = 0, lp = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { d[k] = S.gdeg[4 * tid + k]; ls += d[k]; lp += d[k] * (d[k] - 1) / 2; }
+            const int is = warp_incl_scan(ls), ip = warp_incl_scan(lp);
+            int es = is - ls, ep = ip - lp;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                S.sp[4 * tid + k] = es; S.pp[4 * tid + k] = ep;
+                es += d[k]; ep += d[k] * (d[k] - 1) / 2;
+            }
+            if (tid == 31) { S.sp[T2_GENS] = es; S.pp[T2_GENS] = ep; S.fits = es <= T2_SCAP; }
+        }
+        __syncthreads();
+        const bool fits = S.fits;
         int g0 = 0;
         while (g0 < ng_all) {
-            // ---- sub-pass [g0, g1): as many generators as fit into the slot budget
-            if (tid == 0) {
-                int slots = 0, pairs = 0, g = g0;
-                S.sp[0] = 0; S.pp[0] = 0;
-                while (g < ng_all && slots + S.gdeg[g] <= T2_SCAP) {
-                    const int d = S.gdeg[g];
-                    slots += d;
-                    pairs += d * (d - 1) / 2;
-                    ++g;
-                    S.sp[g - g0] = slots;
-                    S.pp[g - g0] = pairs;
+            // ---- sub-pass [g0, g1): the whole window when it fits the slot budget (the common case),
+            // otherwise as many generators as fit, found by one thread
+            if (!fits) {
+                if (tid == 0) {
+                    int slots = 0, pairs = 0, g = g0;
+                    S.sp[0] = 0; S.pp[0] = 0;
+                    while (g < ng_all && slots + S.gdeg[g] <= T2_SCAP) {
+                        const int d = S.gdeg[g];
+                        slots += d;
+                        pairs += d * (d - 1) / 2;
+                        ++g;
+                        S.sp[g - g0] = slots;
+                        S.pp[g - g0] = pairs;
+                    }
+                    S.g1 = g;
                 }
-                S.g1 = g;
+                __syncthreads();
+            } else if (tid == 0) {
+                S.g1 = ng_all;
             }
-            __syncthreads();
+            if (fits) __syncthreads();
             const int g1 = S.g1;
             const int ng = g1 - g0;
             const int nslots = S.sp[ng];
@@ -167,73 +190,84 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int ran
                     for (int w = 0; w < W; ++w) { S.M[s * W + w] = 0ull; S.T[s * W + w] = 0ull; }
                 }
                 __syncthreads();
-                // ---- B: partner pairs
-                for (int pc0 = 0; pc0 < npairs; pc0 += T2_PLCAP) {
-                    const int pend = min(pc0 + T2_PLCAP, npairs);
-                    if (tid == 0) S.npass = 0;
-                    __syncthreads();
-                    for (int p0 = pc0; p0 < pend; p0 += T2_THREADS) {          // B1: reach pre-filter (pipeline.py:398-401)
-                        const int p = p0 + tid;
-                        bool pass = false;
-                        if (p < pend) {
-                            const int g = owner_of(S.pp, ng, p);
-                            const int q = p - S.pp[g];
-                            const int d = S.gdeg[g0 + g];
-                            const float b2 = (float)(2 * d - 1);
-                            int i = (int)((b2 - sqrtf(b2 * b2 - 8.0f * (float)q)) * 0.5f);
-                            i = max(0, min(i, d - 2));
-                            while (i > 0 && i * (2 * d - i - 1) / 2 > q) --i;
-                            while ((i + 1) * (2 * d - i - 2) / 2 <= q) ++i;
-                            const int j = q - i * (2 * d - i - 1) / 2 + i + 1;
-                            const int si = S.sp[g] + i, sj = S.sp[g] + j;
-                            Atom av, aw;
+                // ---- B: partner pairs, warp-autonomous.  Lane = partner slot i; round r pairs it with slot
+                // i + r of the same generator (np.triu_indices order is irrelevant here: results are bits).
+                // B1 queues the pairs that pass the reach pre-filter (pipeline.py:398-401) with a ballot;
+                // B2 solves a full warp of queued pairs at a time, so the ortho code runs with packed lanes.
+                {
+                    const int warp = tid >> 5;
+                    unsigned *wq = S.u.wq[warp];
+                    int qn = 0;                                           // warp-uniform queue fill
+                    auto solve_queue = [&](int count) {                    // dense ortho2 + ortho3 over wq[0..count)
+                        for (int x0 = 0; x0 < count; x0 += 32) {
+                            const int x = x0 + lane;
+                            if (x < count) {
+                                const unsigned pr = wq[x];
+                                const int si = (int)(pr & 0xffffu), sj = (int)(pr >> 16);
+                                const int g = S.sgen[si];
+                                const int i = S.sli[si], j = S.sli[sj];
+                                Atom av, aw;
+                                av.x = S.sx[si]; av.y = S.sy[si]; av.z = S.sz[si]; av.r2 = S.sr2[si];
+                                aw.x = S.sx[sj]; aw.y = S.sy[sj]; aw.z = S.sz[sj]; aw.r2 = S.sr2[sj];
+                                const int ov = S.sorig[si], ow = S.sorig[sj];
+                                const int t = t0 + g0 + g;
+                                const int d = S.gdeg[g0 + g];
+                                const unsigned q = (unsigned)(i * (2 * d - i - 1) / 2 + (j - i - 1));   // triu ordinal
+                                const Ortho e2 = ortho_edge(ov, av, ow, aw, P.tol.eps_sing);             // pipeline.py:412-414
+                                if (e2.singular) record_singular(P, make_err_key(ST_VW, t, q), ov, ow, -1, -1, 2);
+                                if (e2.size <= P.tol.lim_a) {                                            // pipeline.py:415
+                                    atomicOr(&S.M[si * W + (j >> 6)], 1ull << (j & 63));
+                                    atomicOr(&S.M[sj * W + (i >> 6)], 1ull << (i & 63));
+                                    Atom au;
+                                    au.x = S.gx[g0 + g]; au.y = S.gy[g0 + g]; au.z = S.gz[g0 + g]; au.r2 = S.gr2[g0 + g];
+                                    const int ou = S.gorig[g0 + g];
+                                    const Ortho e3 = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);  // pipeline.py:417-419
+                                    if (e3.singular) record_singular(P, make_err_key(ST_TRI, t, q), ou, ov, ow, -1, 3);
+                                    if (e3.size <= P.tol.lim_a)                                          // pipeline.py:420
+                                        atomicOr(&S.T[si * W + (j >> 6)], 1ull << (j & 63));
+                                }
+                            }
+                        }
+                        __syncwarp();
+                    };
+                    for (int s0 = warp * 32; s0 < nslots; s0 += T2_THREADS) {
+                        const int si = s0 + lane;
+                        int more = 0, sbase = 0;
+                        Atom av;
+                        double rv = 0.0;
+                        av.x = av.y = av.z = av.r2 = 0.0;
+                        if (si < nslots) {
+                            const int g = S.sgen[si];
+                            more = S.gdeg[g0 + g] - 1 - (int)S.sli[si];   // partners after slot i in its generator
+                            sbase = si;
                             av.x = S.sx[si]; av.y = S.sy[si]; av.z = S.sz[si]; av.r2 = S.sr2[si];
-                            aw.x = S.sx[sj]; aw.y = S.sy[sj]; aw.z = S.sz[sj]; aw.r2 = S.sr2[sj];
-                            pass = reach_pair(av, S.sreach[si], aw, S.sreach[sj]);
+                            rv = S.sreach[si];
                         }
-                        const unsigned m = __ballot_sync(FULL, pass);
-                        if (m) {
-                            int base = 0;
-                            if (lane == __ffs(m) - 1) base = atomicAdd(&S.npass, __popc(m));
-                            base = __shfl_sync(FULL, base, __ffs(m) - 1);
-                            if (pass) S.u.passlist[base + __popc(m & lanemask_lt())] = p;
-                        }
-                    }
-                    __syncthreads();
-                    const int npass = S.npass;
-                    for (int x = tid; x < npass; x += T2_THREADS) {             // B2: dense ortho2 + ortho3
-                        const int p = S.u.passlist[x];
-                        const int g = owner_of(S.pp, ng, p);
-                        const int q = p - S.pp[g];
-                        const int d = S.gdeg[g0 + g];
-                        const float b2 = (float)(2 * d - 1);
-                        int i = (int)((b2 - sqrtf(b2 * b2 - 8.0f * (float)q)) * 0.5f);
-                        i = max(0, min(i, d - 2));
-                        while (i > 0 && i * (2 * d - i - 1) / 2 > q) --i;
-                        while ((i + 1) * (2 * d - i - 2) / 2 <= q) ++i;
-                        const int j = q - i * (2 * d - i - 1) / 2 + i + 1;
-                        const int si = S.sp[g] + i, sj = S.sp[g] + j;
-                        Atom av, aw;
-                        av.x = S.sx[si]; av.y = S.sy[si]; av.z = S.sz[si]; av.r2 = S.sr2[si];
-                        aw.x = S.sx[sj]; aw.y = S.sy[sj]; aw.z = S.sz[sj]; aw.r2 = S.sr2[sj];
-                        const int ov = S.sorig[si], ow = S.sorig[sj];
-                        const int t = t0 + g0 + g;
-                        const Ortho e2 = ortho_edge(ov, av, ow, aw, P.tol.eps_sing);             // pipeline.py:412-414
-                        if (e2.singular) record_singular(P, make_err_key(ST_VW, t, (unsigned)q), ov, ow, -1, -1, 2);
-                        if (e2.size <= P.tol.lim_a) {                                            // pipeline.py:415
-                            atomicOr(&S.M[si * W + (j >> 6)], 1ull << (j & 63));
-                            atomicOr(&S.M[sj * W + (i >> 6)], 1ull << (i & 63));
-                            Atom au;
-                            au.x = S.gx[g0 + g]; au.y = S.gy[g0 + g]; au.z = S.gz[g0 + g]; au.r2 = S.gr2[g0 + g];
-                            const int ou = S.gorig[g0 + g];
-                            const Ortho e3 = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);  // pipeline.py:417-419
-                            if (e3.singular) record_singular(P, make_err_key(ST_TRI, t, (unsigned)q), ou, ov, ow, -1, 3);
-                            if (e3.size <= P.tol.lim_a)                                          // pipeline.py:420
-                                atomicOr(&S.T[si * W + (j >> 6)], 1ull << (j & 63));
+                        int rounds = more;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) rounds = max(rounds, __shfl_xor_sync(FULL, rounds, o));
+                        for (int r = 1; r <= rounds; ++r) {
+                            bool pass = false;
+                            const int sj = sbase + r;
+                            if (r <= more) {
+                                Atom aw;
+                                aw.x = S.sx[sj]; aw.y = S.sy[sj]; aw.z = S.sz[sj]; aw.r2 = S.sr2[sj];
+                                pass = reach_pair(av, rv, aw, S.sreach[sj]);
+                            }
+                            const unsigned m = __ballot_sync(FULL, pass);
+                            if (m) {
+                                if (qn + 32 > T2_WQCAP) { __syncwarp(); solve_queue(qn); qn = 0; }
+                                if (pass) wq[qn + __popc(m & lanemask_lt())] = (unsigned)si | ((unsigned)sj << 16);
+                                qn += __popc(m);
+                                __syncwarp();
+                                if (qn >= 32 * 8) { solve_queue(qn); qn = 0; }
+                            }
                         }
                     }
-                    __syncthreads();
+                    __syncwarp();
+                    solve_queue(qn);
                 }
+                __syncthreads();
                 // ---- C: triangle list of the tile
                 for (int s = tid; s < nslots; s += T2_THREADS) {
                     int c = 0;
@@ -249,34 +283,38 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int ran
                 __syncthreads();
                 for (int tc0 = 0; tc0 < ntri; tc0 += T2_TCAP) {
                     const int ntc = min(T2_TCAP, ntri - tc0);
-                    for (int x0 = 0; x0 < ntc; x0 += T2_THREADS) {
-                        const int x = x0 + tid;
-                        const bool valid = x < ntc;
-                        int4 entry = make_int4(0, 0, 0, 0);
-                        if (valid) {
-                            const int tt = tc0 + x;
-                            const int s = owner_of(S.rowpre, nslots, tt);
-                            const int j = nth_bit_multi<W>(&S.T[s * W], tt - S.rowpre[s]);
-                            const int g = S.sgen[s];
-                            const int sj = S.sp[g] + j;
-                            S.u.t.tri_si[x] = (unsigned short)s;
-                            S.u.t.tri_sj[x] = (unsigned short)sj;
-                            // partners above j adjacent (in M) to both: rank[x] > rank_hi (pipeline.py:447)
-                            int cnt = 0;
+                    // every partner slot expands its own triangles (bits of its T row) into the round's list
+                    for (int srow = tid; srow < nslots; srow += T2_THREADS) {
+                        int tt = S.rowpre[srow];
+                        if (tt >= tc0 + ntc || S.rowpre[srow + 1] <= tc0) continue;
+                        const int g = S.sgen[srow];
 #pragma unroll
-                            for (int w = 0; w < W; ++w) {
-                                unsigned long long m = S.M[s * W + w] & S.M[sj * W + w];
-                                const int lowbit = j + 1 - 64 * w;
-                                if (lowbit >= 64) m = 0ull;
-                                else if (lowbit > 0) m &= ~0ull << lowbit;
-                                cnt += __popcll(m);
+                        for (int w = 0; w < W; ++w) {
+                            unsigned long long bits = S.T[srow * W + w];
+                            while (bits) {
+                                const int j = 64 * w + __ffsll((long long)bits) - 1;
+                                bits &= bits - 1;
+                                const int x = tt - tc0;
+                                ++tt;
+                                if (x < 0 || x >= ntc) continue;
+                                const int sj = S.sp[g] + j;
+                                S.u.t.tri_si[x] = (unsigned short)srow;
+                                S.u.t.tri_sj[x] = (unsigned short)sj;
+                                // partners above j adjacent (in M) to both: rank[x] > rank_hi (pipeline.py:447)
+                                int cnt = 0;
+#pragma unroll
+                                for (int w2 = 0; w2 < W; ++w2) {
+                                    unsigned long long m = S.M[srow * W + w2] & S.M[sj * W + w2];
+                                    const int lowbit = j + 1 - 64 * w2;
+                                    if (lowbit >= 64) m = 0ull;
+                                    else if (lowbit > 0) m &= ~0ull << lowbit;
+                                    cnt += __popcll(m);
+                                }
+                                S.u.t.cpre[x] = cnt;
+                                const unsigned pos = S.pt_base + (unsigned)(tc0 + x);
+                                if (pos < P.pt_cap)
+                                    P.pt[pos] = make_int4(t0 + g0 + g, S.srank[srow], S.srank[sj], (int)S.sli[srow] | (j << 16));
                             }
-                            S.u.t.cpre[x] = cnt;
-                            entry = make_int4(t0 + g0 + g, S.srank[s], S.srank[sj], (int)S.sli[s] | (j << 16));
-                        }
-                        if (valid) {
-                            const unsigned pos = S.pt_base + (unsigned)(tc0 + x);
-                            if (pos < P.pt_cap) P.pt[pos] = entry;
                         }
                     }
                     __syncthreads();

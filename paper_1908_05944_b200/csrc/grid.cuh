@@ -143,7 +143,7 @@ __global__ void k_cell_finalize(int n, const double *__restrict__ xyz, const dou
                                 const int *__restrict__ key_of_ball, const uint32_t *__restrict__ cell_start,
                                 const int *__restrict__ arrival, double alpha, double eps_abs,
                                 int *__restrict__ orig_of_rank, int *__restrict__ rank_of_orig,
-                                int *__restrict__ key_of_rank, Atom *__restrict__ atoms, double *__restrict__ reach,
+                                int4 *__restrict__ cell_of_rank, int dimx, int dimy, Atom *__restrict__ atoms, double *__restrict__ reach,
                                 Counters *__restrict__ ctr, int2 *__restrict__ dup_records) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
@@ -174,7 +174,8 @@ __global__ void k_cell_finalize(int n, const double *__restrict__ xyz, const dou
     reach[pos] = (lim >= 0.0) ? sqrt(fmax(lim, 0.0)) : -1.0;   // pipeline.py:323-324
     orig_of_rank[pos] = i;
     rank_of_orig[i] = pos;
-    key_of_rank[pos] = key;
+    const int rest = key / dimx;                           // (cx, cy, cz, key): k_edges wants the coordinates
+    cell_of_rank[pos] = make_int4(key - rest * dimx, rest % dimy, rest / dimy, key);
 }
 
 __global__ void k_grid_export(int n, const int *__restrict__ orig_of_rank, const int *__restrict__ rank_of_orig,
