@@ -113,25 +113,41 @@ __global__ void __launch_bounds__(256) k_prune_tets(PruneParams P) {
         const unsigned slot = atomicAdd(&P.ctr->n_k3, 1u);
         if (slot < P.k3_cap) P.k3[slot] = make_int4(row[0], row[1], row[2], row[3]);
         atomicAdd(P.cnt3 + row[0], 1u);
-        // faces and edges generated by u (partner slots i < j < k of u)
+        // Inheritance marks (pipeline.py:501, 509): 4 faces, 6 edges.  All lookups first, then all
+        // atomics back to back (their round trips overlap), then the owner counters of what was new.
         const unsigned bu = __ldg(P.adj_off + r.x);
-        mark_tri(P, bu + i, j, min3(ou, ov, ow));
-        mark_tri(P, bu + i, k, min3(ou, ov, ox));
-        mark_tri(P, bu + j, k, min3(ou, ow, ox));
-        mark_edge(P, bu + i, min(ou, ov));
-        mark_edge(P, bu + j, min(ou, ow));
-        mark_edge(P, bu + k, min(ou, ox));
-        // face (v, w, x) and edges (v, w), (v, x) live in v's rows; edge (w, x) in w's row
         const unsigned bv = __ldg(P.adj_off + r.y);
-        const int dv = __ldg(P.deg + r.y);
-        const int iw = find_partner(P.pe_v, bv, dv, r.z);
-        const int ix = find_partner(P.pe_v, bv, dv, r.w);
-        if (iw >= 0 && ix >= 0) mark_tri(P, bv + iw, ix, min3(ov, ow, ox)); else note_miss(P);
-        if (iw >= 0) mark_edge(P, bv + iw, min(ov, ow)); else note_miss(P);
-        if (ix >= 0) mark_edge(P, bv + ix, min(ov, ox)); else note_miss(P);
         const unsigned bw = __ldg(P.adj_off + r.z);
-        const int jx = find_partner(P.pe_v, bw, __ldg(P.deg + r.z), r.w);
-        if (jx >= 0) mark_edge(P, bw + jx, min(ow, ox)); else note_miss(P);
+        const int dv = __ldg(P.deg + r.y);
+        const int iw = find_partner(P.pe_v, bv, dv, r.z);       // face (v, w, x) and edges (v, w), (v, x) live in v's rows
+        const int ix = find_partner(P.pe_v, bv, dv, r.w);
+        const int jx = find_partner(P.pe_v, bw, __ldg(P.deg + r.z), r.w);   // edge (w, x) in w's row
+        const unsigned long long bj = 1ull << (j & 63), bk = 1ull << (k & 63);
+        const size_t W = (size_t)P.W;
+        const unsigned long long t0 = atomicOr(P.trimask + (size_t)(bu + i) * W + (j >> 6), bj);
+        const unsigned long long t1 = atomicOr(P.trimask + (size_t)(bu + i) * W + (k >> 6), bk);
+        const unsigned long long t2 = atomicOr(P.trimask + (size_t)(bu + j) * W + (k >> 6), bk);
+        unsigned long long t3 = ~0ull;
+        const unsigned long long bx = 1ull << (ix & 63);
+        if (iw >= 0 && ix >= 0) t3 = atomicOr(P.trimask + (size_t)(bv + iw) * W + (ix >> 6), bx);
+        const unsigned e0 = atomicExch(P.eflag + bu + i, 1u);
+        const unsigned e1 = atomicExch(P.eflag + bu + j, 1u);
+        const unsigned e2 = atomicExch(P.eflag + bu + k, 1u);
+        const unsigned e3 = iw >= 0 ? atomicExch(P.eflag + bv + iw, 1u) : 1u;
+        const unsigned e4 = ix >= 0 ? atomicExch(P.eflag + bv + ix, 1u) : 1u;
+        const unsigned e5 = jx >= 0 ? atomicExch(P.eflag + bw + jx, 1u) : 1u;
+        if (!(t0 & bj)) atomicAdd(P.cnt2 + min3(ou, ov, ow), 1u);
+        if (!(t1 & bk)) atomicAdd(P.cnt2 + min3(ou, ov, ox), 1u);
+        if (!(t2 & bk)) atomicAdd(P.cnt2 + min3(ou, ow, ox), 1u);
+        if (iw >= 0 && ix >= 0 && !(t3 & bx)) atomicAdd(P.cnt2 + min3(ov, ow, ox), 1u);
+        if (!e0) atomicAdd(P.cnt1 + min(ou, ov), 1u);
+        if (!e1) atomicAdd(P.cnt1 + min(ou, ow), 1u);
+        if (!e2) atomicAdd(P.cnt1 + min(ou, ox), 1u);
+        if (!e3) atomicAdd(P.cnt1 + min(ov, ow), 1u);
+        if (!e4) atomicAdd(P.cnt1 + min(ov, ox), 1u);
+        if (!e5) atomicAdd(P.cnt1 + min(ow, ox), 1u);
+        if (iw < 0 || ix < 0) { note_miss(P); if (iw < 0) note_miss(P); if (ix < 0) note_miss(P); }
+        if (jx < 0) note_miss(P);
     }
 }
 
