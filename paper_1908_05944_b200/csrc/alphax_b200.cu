@@ -92,6 +92,8 @@ struct axb_ctx {
     uint32_t n_pe = 0, n_pt = 0, n_pq = 0;
     int64_t counts[4] = {0, 0, 0, 0};
     size_t mark_after_grid = 0, mark_after_edges = 0;
+    int cull_mask = 1;                    // bit 0: tets, bit 1: triangles (A/B switch AXB_CULL=0..3)
+    bool cull = false;                    // one-call path: k_tri_tet2 settles partner-dominated simplices itself
     bool slab_mode = false;               // grid geometry fixed by the caller (one z-slab of a global grid)
     const int64_t *gidx = nullptr;        // slab mode: global ball index per local ball (ascending)
 };
@@ -264,6 +266,7 @@ EstParams est_params(axb_ctx *c, unsigned long long report_key) {
     P.adj_off = c->adj_off; P.deg = c->deg; P.pe_v = c->pe_v; P.pe_u = c->pe_u; P.pe_cap = c->pe_cap;
     P.pt = c->pt; P.pt_cap = c->pt_cap; P.pq_r = c->pq_r; P.pq_l = c->pq_l; P.pq_cap = c->pq_cap;
     P.ctr = c->ctr; P.errs = c->errs; P.report_key = report_key;
+    P.cull = c->cull ? c->cull_mask : 0;
     return P;
 }
 
@@ -291,32 +294,15 @@ int launch_edges(axb_ctx *c, const EstParams &P, int lo, int hi) {
 int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
     EstParams P = est_params(c, report_key);
     const int ngen = c->rank_hi - c->rank_lo;
-    static const bool use_v1 = getenv("AXB_TRITET_V1") != nullptr;      // A/B switch: warp-per-generator kernel
-    if (!use_v1) {
-        const unsigned ntiles = (unsigned)std::max(1, (ngen + T2_GENS - 1) / T2_GENS);
-        if (c->W == 1) {
-            const size_t smem = sizeof(T2Smem<1>);
-            CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_tri_tet2<1><<<std::min(ntiles, (unsigned)c->sm_count * 2u), T2_THREADS, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
-        } else {
-            const size_t smem = sizeof(T2Smem<4>);
-            CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_tri_tet2<4><<<std::min(ntiles, (unsigned)c->sm_count), T2_THREADS, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
-        }
-        LAUNCH_CHECK(c);
-        return AXB_OK;
-    }
-    const unsigned ntiles = (unsigned)((ngen + EST_TILE - 1) / EST_TILE);
+    const unsigned ntiles = (unsigned)std::max(1, (ngen + T2_GENS - 1) / T2_GENS);
     if (c->W == 1) {
-        size_t smem = sizeof(TriWarpSmem<1>) * 8;
-        CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        unsigned grid = std::max(1u, std::min(ntiles, (unsigned)c->sm_count * 3u));
-        k_tri_tet<1><<<grid, 256, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
+        const size_t smem = sizeof(T2Smem<1>);
+        CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_tri_tet2<1><<<std::min(ntiles, (unsigned)c->sm_count * 2u), T2_THREADS, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
     } else {
-        size_t smem = sizeof(TriWarpSmem<4>) * 4;
-        CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        unsigned grid = std::max(1u, std::min(ntiles, (unsigned)c->sm_count));
-        k_tri_tet<4><<<grid, 128, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
+        const size_t smem = sizeof(T2Smem<4>);
+        CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_tri_tet2<4><<<std::min(ntiles, (unsigned)c->sm_count), T2_THREADS, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
     }
     LAUNCH_CHECK(c);
     return AXB_OK;
@@ -813,6 +799,7 @@ int run_canonicalize(axb_ctx *c, int64_t counts[4]) {
 
 extern "C" int axb_potential(axb_ctx *c, int64_t lo, int64_t hi) {
     if (!c) return AXB_ERR_BAD_ARG;
+    c->cull = false;          // the stage API exposes the complete potential levels
     return run_potential(c, lo, hi);
 }
 
@@ -917,7 +904,11 @@ extern "C" int axb_compute(axb_ctx *c, int64_t n, const double *d_xyz, const dou
     if (!c) return AXB_ERR_BAD_ARG;
     int st = axb_grid_build(c, n, d_xyz, d_radii, prm);
     if (st != AXB_OK) return st;
-    if ((st = run_potential(c, 0, n)) != AXB_OK) return st;
+    c->cull = true;
+    if (const char *e = getenv("AXB_CULL")) c->cull_mask = atoi(e);
+    st = run_potential(c, 0, n);
+    c->cull = false;
+    if (st != AXB_OK) return st;
     if ((st = run_prune(c)) != AXB_OK) return st;
     st = run_canonicalize(c, counts);
     if (st == AXB_ERR_ARENA + 1000) return fail(c, AXB_ERR_INTERNAL, "a potential list overflowed after it was sized exactly");

@@ -1,18 +1,14 @@
-// estimate.cuh -- stage one: potential edges, triangles and tetrahedra
-// (reference pipeline.py:316-479), one warp per generator ball.
+// estimate.cuh -- stage one, potential edges (reference pipeline.py:316-359),
+// one warp per generator ball; shared parameter block of the estimation kernels.
 //
 // A generator is the minimum-RANK vertex of a simplex (pipeline.py:10-15).
-//   k_edges    : scans the upper half of the generator's 5x5x5 cell block --
-//                13 rows of cells, each a contiguous rank range -- lanes over
-//                candidates, reach pre-filter + ortho-size test, warp-ballot
-//                compaction into the generator's partner list (ascending rank).
-//   k_tri_tet  : stages the partner atoms in shared memory, tests all partner
-//                pairs (bit matrix M of "is a potential edge"), derives the
-//                potential triangles (bit matrix T) and extends each triangle
-//                by the higher partners that are M-adjacent to both its
-//                vertices (potential tets).
-// Variable-length outputs go through warp-private shared-memory staging
-// buffers that are flushed with ONE global atomicAdd per flush.
+//   k_edges : scans the upper half of the generator's 5x5x5 cell block -- 13 rows
+//             of cells, each a contiguous rank range -- lanes over candidates
+//             (coalesced 32-byte atom loads), reach pre-filter + ortho-size test,
+//             warp-ballot/popc compaction into the generator's partner list
+//             (ascending rank).  Partner lists are staged in warp-private shared
+//             memory and flushed with ONE global atomicAdd per ~32 generators.
+// Potential triangles and tets: estimate2.cuh.
 #pragma once
 
 #include "common.cuh"
@@ -47,6 +43,7 @@ struct EstParams {
     Counters *ctr;
     ErrRecord *errs;
     unsigned long long report_key;   // != 0: only the solve with this key writes errs[0]
+    int cull;                        // k_tri_tet2: drop / flag simplices dominated by a partner of their generator
 };
 
 __device__ __forceinline__ void sort_small(int *v, int k) {
@@ -207,221 +204,9 @@ __global__ void __launch_bounds__(EST_WARPS * 32, 4) k_edges(EstParams P, int ra
     }
 }
 
-// -------------------------------------------------------------- k_tri_tet
-constexpr int TBUF = 128;   // staged potential triangles per warp
-constexpr int QBUF = 128;   // staged potential tets per warp
-
-template <int W>
-struct TriWarpSmem {
-    static constexpr int PCAP = 64 * W;
-    double x[PCAP], y[PCAP], z[PCAP], r2[PCAP], reach[PCAP];
-    unsigned long long M[PCAP * W];      // M[i] bit j: (P_i, P_j) passes reach filter and ortho-size test
-    unsigned long long T[PCAP * W];      // T[i] bit j (j > i): (u, P_i, P_j) is a potential triangle
-    int orig[PCAP];
-    int rank[PCAP];
-    int rowpre[PCAP + 1];
-    int4 tbuf[TBUF];
-    int4 qbuf_r[QBUF];
-    int qbuf_l[QBUF];
-};
-
 __device__ __forceinline__ int nth_set_bit(unsigned long long m, int n) {
     for (int q = 0; q < n; ++q) m &= m - 1;
     return __ffsll((long long)m) - 1;
-}
-
-template <int W>
-__global__ void __launch_bounds__(W == 1 ? 256 : 128) k_tri_tet(EstParams P, int rank_lo, int rank_hi) {
-    constexpr int WARPS = (W == 1) ? 8 : 4;
-    constexpr int PCAP = 64 * W;
-    extern __shared__ __align__(16) unsigned char s_raw[];
-    TriWarpSmem<W> &S = reinterpret_cast<TriWarpSmem<W> *>(s_raw)[threadIdx.x >> 5];
-    const int warp = threadIdx.x >> 5, lane = lane_id();
-    int ntb = 0, nqb = 0;                   // warp-uniform staging fill
-
-    auto flush_t = [&]() {
-        if (ntb == 0) return;
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&P.ctr->n_pt, (unsigned)ntb);
-        base = __shfl_sync(FULL, base, 0);
-        __syncwarp();
-        if ((unsigned long long)base + (unsigned)ntb <= P.pt_cap) {
-            for (int idx = lane; idx < ntb; idx += 32) P.pt[base + idx] = S.tbuf[idx];
-        } else if (lane == 0) {
-            atomicOr(&P.ctr->overflow, 1u << 1);
-        }
-        __syncwarp();
-        ntb = 0;
-    };
-    auto flush_q = [&]() {
-        if (nqb == 0) return;
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&P.ctr->n_pq, (unsigned)nqb);
-        base = __shfl_sync(FULL, base, 0);
-        __syncwarp();
-        if ((unsigned long long)base + (unsigned)nqb <= P.pq_cap) {
-            for (int idx = lane; idx < nqb; idx += 32) {
-                P.pq_r[base + idx] = S.qbuf_r[idx];
-                P.pq_l[base + idx] = S.qbuf_l[idx];
-            }
-        } else if (lane == 0) {
-            atomicOr(&P.ctr->overflow, 1u << 2);
-        }
-        __syncwarp();
-        nqb = 0;
-    };
-
-    const int ntiles = (rank_hi - rank_lo + EST_TILE - 1) / EST_TILE;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int t_end = min(rank_lo + (tile + 1) * EST_TILE, rank_hi);
-        for (int t = rank_lo + tile * EST_TILE + warp; t < t_end; t += WARPS) {
-            const int d = min(__ldg(P.deg + t), PCAP);
-            if (d < 2) continue;
-            const unsigned abase = __ldg(P.adj_off + t);
-            const Atom au = load_atom(P.atoms, t);
-            const int ou = __ldg(P.orig + t);
-            // ---- stage the partner atoms (ascending rank = pipeline.py:362-370 order)
-            for (int i = lane; i < d; i += 32) {
-                int rk = __ldg(P.pe_v + abase + i);
-                Atom a = load_atom(P.atoms, rk);
-                S.x[i] = a.x; S.y[i] = a.y; S.z[i] = a.z; S.r2[i] = a.r2;
-                S.reach[i] = __ldg(P.reach + rk);
-                S.orig[i] = __ldg(P.orig + rk);
-                S.rank[i] = rk;
-#pragma unroll
-                for (int w = 0; w < W; ++w) { S.M[i * W + w] = 0ull; S.T[i * W + w] = 0ull; }
-            }
-            __syncwarp();
-            // ---- all partner pairs in np.triu_indices order (pipeline.py:393-401)
-            const int npairs = d * (d - 1) / 2;
-            for (int p0 = 0; p0 < npairs; p0 += 32) {
-                const int p = p0 + lane;
-                if (p < npairs) {
-                    const float b2 = (float)(2 * d - 1);
-                    int i = (int)((b2 - sqrtf(b2 * b2 - 8.0f * (float)p)) * 0.5f);
-                    i = max(0, min(i, d - 2));
-                    while (i > 0 && i * (2 * d - i - 1) / 2 > p) --i;
-                    while ((i + 1) * (2 * d - i - 2) / 2 <= p) ++i;
-                    const int j = p - i * (2 * d - i - 1) / 2 + i + 1;
-                    Atom av, aw;
-                    av.x = S.x[i]; av.y = S.y[i]; av.z = S.z[i]; av.r2 = S.r2[i];
-                    aw.x = S.x[j]; aw.y = S.y[j]; aw.z = S.z[j]; aw.r2 = S.r2[j];
-                    if (reach_pair(av, S.reach[i], aw, S.reach[j])) {                    // pipeline.py:398-401
-                        const int ov = S.orig[i], ow = S.orig[j];
-                        const Ortho e2 = ortho_edge(ov, av, ow, aw, P.tol.eps_sing);     // pipeline.py:412-414
-                        if (e2.singular) record_singular(P, make_err_key(ST_VW, t, (unsigned)p), ov, ow, -1, -1, 2);
-                        if (e2.size <= P.tol.lim_a) {                                    // pipeline.py:415
-                            atomicOr(&S.M[i * W + (j >> 6)], 1ull << (j & 63));
-                            atomicOr(&S.M[j * W + (i >> 6)], 1ull << (i & 63));
-                            const Ortho e3 = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);   // pipeline.py:417-419
-                            if (e3.singular) record_singular(P, make_err_key(ST_TRI, t, (unsigned)p), ou, ov, ow, -1, 3);
-                            if (e3.size <= P.tol.lim_a)                                  // pipeline.py:420
-                                atomicOr(&S.T[i * W + (j >> 6)], 1ull << (j & 63));
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            // ---- prefix of triangles per row
-            int carry = 0;
-            for (int i0 = 0; i0 < d; i0 += 32) {
-                const int i = i0 + lane;
-                int c = 0;
-                if (i < d) {
-#pragma unroll
-                    for (int w = 0; w < W; ++w) c += __popcll(S.T[i * W + w]);
-                }
-                const int incl = warp_incl_scan(c);
-                if (i < d) S.rowpre[i] = carry + incl - c;
-                carry += __shfl_sync(FULL, incl, 31);
-            }
-            const int ntri = carry;
-            if (lane == 0) S.rowpre[d] = ntri;
-            __syncwarp();
-            if (ntri == 0) continue;
-            // ---- lanes over triangles: emit the triangle, then extend it (pipeline.py:447-479)
-            for (int tt0 = 0; tt0 < ntri; tt0 += 32) {
-                const int tt = tt0 + lane;
-                const bool valid = tt < ntri;
-                int i = 0, j = 0;
-                unsigned long long cand[W];
-#pragma unroll
-                for (int w = 0; w < W; ++w) cand[w] = 0ull;
-                if (valid) {
-                    int lo = 0, hi = d;                     // last row with rowpre <= tt
-                    while (hi - lo > 1) {
-                        int mid = (lo + hi) >> 1;
-                        if (S.rowpre[mid] <= tt) lo = mid; else hi = mid;
-                    }
-                    i = lo;
-                    int nth = tt - S.rowpre[i];
-                    j = -1;
-#pragma unroll
-                    for (int w = 0; w < W; ++w) {
-                        unsigned long long m = S.T[i * W + w];
-                        int c = __popcll(m);
-                        if (j < 0) {
-                            if (nth < c) j = 64 * w + nth_set_bit(m, nth);
-                            else nth -= c;
-                        }
-                    }
-                    // partners above j adjacent (in M) to both P_i and P_j: rank[x] > rank_hi (pipeline.py:447)
-#pragma unroll
-                    for (int w = 0; w < W; ++w) {
-                        unsigned long long m = S.M[i * W + w] & S.M[j * W + w];
-                        int lowbit = j + 1 - 64 * w;        // keep bits >= lowbit
-                        if (lowbit >= 64) m = 0ull;
-                        else if (lowbit > 0) m &= ~0ull << lowbit;
-                        cand[w] = m;
-                    }
-                }
-                // stage the triangles of this round
-                {
-                    const int cnt = min(32, ntri - tt0);
-                    if (ntb + cnt > TBUF) flush_t();
-                    if (valid) S.tbuf[ntb + lane] = make_int4(t, S.rank[i], S.rank[j], i | (j << 16));
-                    ntb += cnt;
-                    __syncwarp();
-                }
-                // extend: every lane walks its own candidate bits; rounds are warp-synchronous
-                for (;;) {
-                    int k = -1;
-#pragma unroll
-                    for (int w = 0; w < W; ++w)
-                        if (k < 0 && cand[w]) { k = 64 * w + __ffsll((long long)cand[w]) - 1; cand[w] &= cand[w] - 1; }
-                    if (!__any_sync(FULL, k >= 0)) break;
-                    bool keep = false;
-                    if (k >= 0) {
-                        Atom av, aw, ax;
-                        av.x = S.x[i]; av.y = S.y[i]; av.z = S.z[i]; av.r2 = S.r2[i];
-                        aw.x = S.x[j]; aw.y = S.y[j]; aw.z = S.z[j]; aw.r2 = S.r2[j];
-                        ax.x = S.x[k]; ax.y = S.y[k]; ax.z = S.z[k]; ax.r2 = S.r2[k];
-                        const int ov = S.orig[i], ow = S.orig[j], ox = S.orig[k];
-                        const Ortho e4 = ortho_tet(ou, au, ov, av, ow, aw, ox, ax, P.tol.eps_sing);   // pipeline.py:475-477
-                        if (e4.singular)
-                            record_singular(P, make_err_key(ST_TET, t, ((unsigned)tt << 8) | (unsigned)k), ou, ov, ow, ox, 4);
-                        keep = e4.size <= P.tol.lim_a;                                               // pipeline.py:478
-                    }
-                    const unsigned m = __ballot_sync(FULL, keep);
-                    const int cnt = __popc(m);
-                    if (cnt) {
-                        if (nqb + cnt > QBUF) flush_q();
-                        if (keep) {
-                            int slot = nqb + __popc(m & lanemask_lt());
-                            S.qbuf_r[slot] = make_int4(t, S.rank[i], S.rank[j], S.rank[k]);
-                            S.qbuf_l[slot] = i | (j << 8) | (k << 16);
-                        }
-                        nqb += cnt;
-                        __syncwarp();
-                    }
-                }
-            }
-            __syncwarp();
-        }
-    }
-    flush_t();
-    flush_q();
-    (void)warp;
 }
 
 }  // namespace axb

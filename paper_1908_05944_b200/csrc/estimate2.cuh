@@ -27,8 +27,8 @@ constexpr int T2_THREADS = 256;
 constexpr int T2_WARPS = T2_THREADS / 32;
 constexpr int T2_GENS = 128;       // generators per tile
 constexpr int T2_SCAP = 1024;      // partner slots per sub-pass (>= 64 * W so one generator always fits)
-constexpr int T2_TCAP = 4096;      // triangles per round
-constexpr int T2_WQCAP = 1024;     // reach-passing pairs queued per warp
+constexpr int T2_TCAP = 3072;      // triangles per round
+constexpr int T2_WQCAP = 768;      // reach-passing pairs queued per warp
 
 template <int W>
 struct T2Smem {
@@ -36,6 +36,7 @@ struct T2Smem {
     double gx[T2_GENS], gy[T2_GENS], gz[T2_GENS], gr2[T2_GENS];
     unsigned long long M[T2_SCAP * W];
     unsigned long long T[T2_SCAP * W];
+    unsigned long long D[T2_SCAP * W];         // potential triangles already known to be dominated (cull mode)
     int sorig[T2_SCAP], srank[T2_SCAP];
     int rowpre[T2_SCAP + 1];
     int gorig[T2_GENS], gdeg[T2_GENS];
@@ -103,6 +104,25 @@ __device__ __forceinline__ int nth_bit_multi(const unsigned long long *row, int 
         nth -= c;
     }
     return -1;
+}
+
+// Cull mode (the one-call path; the standalone stage API needs the complete potential lists and
+// switches it off): a simplex whose ortho-centre is dominated by another partner of its generator
+// fails the domination check of the pruning stage for certain -- a dominating ball is closer than
+// one cell side to the centre (pipeline.py:288-289), so it is one of the 27-cell candidates, and the
+// power distance below is evaluated exactly like pipeline.py:308-309.  The partners are already in
+// shared memory, so most dominated simplices are settled here and never reach the AC2 kernels.
+template <int W>
+__device__ __forceinline__ bool dominated_by_partner(const T2Smem<W> &S, int g, int g0, int s0, int s1, int s2,
+                                                     double cx, double cy, double cz, double thr) {
+    const int sb = S.sp[g], se = sb + S.gdeg[g0 + g];
+    for (int s = sb; s < se; ++s) {
+        if (s == s0 || s == s1 || s == s2) continue;
+        const double ddx = S.sx[s] - cx, ddy = S.sy[s] - cy, ddz = S.sz[s] - cz;
+        const double dp = ((ddx * ddx + ddy * ddy) + ddz * ddz) - S.sr2[s];
+        if (dp < thr) return true;
+    }
+    return false;
 }
 
 template <int W>
@@ -187,7 +207,7 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int ran
                     S.sgen[s] = (unsigned char)g;
                     S.sli[s] = (unsigned char)li;
 #pragma unroll
-                    for (int w = 0; w < W; ++w) { S.M[s * W + w] = 0ull; S.T[s * W + w] = 0ull; }
+                    for (int w = 0; w < W; ++w) { S.M[s * W + w] = 0ull; S.T[s * W + w] = 0ull; S.D[s * W + w] = 0ull; }
                 }
                 __syncthreads();
                 // ---- B: partner pairs, warp-autonomous.  Lane = partner slot i; round r pairs it with slot
@@ -223,8 +243,12 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int ran
                                     const int ou = S.gorig[g0 + g];
                                     const Ortho e3 = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);  // pipeline.py:417-419
                                     if (e3.singular) record_singular(P, make_err_key(ST_TRI, t, q), ou, ov, ow, -1, 3);
-                                    if (e3.size <= P.tol.lim_a)                                          // pipeline.py:420
+                                    if (e3.size <= P.tol.lim_a) {                                        // pipeline.py:420
                                         atomicOr(&S.T[si * W + (j >> 6)], 1ull << (j & 63));
+                                        if ((P.cull & 2) && dominated_by_partner(S, g, g0, si, sj, -1, e3.cx, e3.cy, e3.cz,
+                                                                           e3.size - P.tol.eps_abs))
+                                            atomicOr(&S.D[si * W + (j >> 6)], 1ull << (j & 63));
+                                    }
                                 }
                             }
                         }
@@ -312,8 +336,10 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int ran
                                 }
                                 S.u.t.cpre[x] = cnt;
                                 const unsigned pos = S.pt_base + (unsigned)(tc0 + x);
+                                const int dom = (int)((S.D[srow * W + (j >> 6)] >> (j & 63)) & 1ull);
                                 if (pos < P.pt_cap)
-                                    P.pt[pos] = make_int4(t0 + g0 + g, S.srank[srow], S.srank[sj], (int)S.sli[srow] | (j << 16));
+                                    P.pt[pos] = make_int4(t0 + g0 + g, S.srank[srow], S.srank[sj],
+                                                          (int)S.sli[srow] | (j << 16) | (dom << 31));
                             }
                         }
                     }
@@ -354,6 +380,9 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int ran
                                 record_singular(P, make_err_key(ST_TET, t, (tri_ord << 8) | (unsigned)k), ou, ov, ow, ox, 4);
                             }
                             keep = e4.size <= P.tol.lim_a;                                               // pipeline.py:478
+                            if (keep && (P.cull & 1) &&
+                                dominated_by_partner(S, g, g0, s, sj, sk, e4.cx, e4.cy, e4.cz, e4.size - P.tol.eps_abs))
+                                keep = false;        // AC2 would fail at this partner (it lies in the 27-cell block): never kept
                             er = make_int4(t, S.srank[s], S.srank[sj], S.srank[sk]);
                             el = (int)S.sli[s] | (j << 8) | (k << 16);
                         }

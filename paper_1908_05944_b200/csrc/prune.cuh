@@ -184,10 +184,12 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_tris(PruneParams P) {
             bool is_free = false;
             if (e < n_pt) {
                 const int4 r = P.pt[e];
-                const int i = r.w & 0xffff, j = r.w >> 16;
-                const unsigned bu = __ldg(P.adj_off + r.x);
-                const unsigned long long word = P.trimask[(size_t)(bu + i) * P.W + (j >> 6)];
-                is_free = !((word >> (j & 63)) & 1ull);       // not inherited from a kept tet
+                if (r.w >= 0) {                               // bit 31: already known to be dominated (k_tri_tet2 cull mode)
+                    const int i = r.w & 0xffff, j = (r.w >> 16) & 0x7fff;
+                    const unsigned bu = __ldg(P.adj_off + r.x);
+                    const unsigned long long word = P.trimask[(size_t)(bu + i) * P.W + (j >> 6)];
+                    is_free = !((word >> (j & 63)) & 1ull);   // not inherited from a kept tet
+                }
             }
             queue_push(is_free, e, queue, &qn);
         }
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_tris(PruneParams P) {
         const int nq = qn;
         for (int x = threadIdx.x; x < nq; x += PRUNE_THREADS) {
             const int4 r = P.pt[queue[x]];
-            const int i = r.w & 0xffff, j = r.w >> 16;
+            const int i = r.w & 0xffff, j = (r.w >> 16) & 0x7fff;
             const unsigned bu = __ldg(P.adj_off + r.x);
             const Atom au = load_atom(P.atoms, r.x), av = load_atom(P.atoms, r.y), aw = load_atom(P.atoms, r.z);
             const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z);
