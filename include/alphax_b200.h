@@ -160,6 +160,14 @@ int axb_export_host(axb_ctx *ctx, int64_t *h_vertices, int64_t *h_edges, int64_t
 int axb_merge_rows(axb_ctx *ctx, int k, int64_t n_index, const int64_t *d_rows, int64_t m, int64_t *d_out,
                    int64_t *count_out);
 
+/* ---- canonical text document (a "next" row of SURVEY 8(f)) ---------------- */
+/* The body of write_complex (reference io.py:228-236): one line "dim v0 [v1 [v2 [v3]]]\n" per
+ * simplex in (dimension, lexicographic) order, from the four HOST int64 arrays.  Host threads, no
+ * GPU.  *needed receives the byte count; with out == NULL only the size is computed; returns
+ * AXB_ERR_ARENA if capacity is too small. */
+int axb_format_complex(const int64_t counts[4], const int64_t *vertices, const int64_t *edges,
+                       const int64_t *triangles, const int64_t *tets, char *out, int64_t capacity, int64_t *needed);
+
 /* ---- measurement -------------------------------------------------------- */
 /* CUDA-event milliseconds per stage of the last run */
 int axb_stage_ms(const axb_ctx *ctx, float out[AXB_ST_COUNT]);

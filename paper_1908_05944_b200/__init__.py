@@ -37,6 +37,9 @@ from .pipeline import (
     compute_alpha_complex_arrays,
     default_engine,
 )
+from .io import read_complex, stats_csv, write_complex
+from .stages import (CellKey, Grid, PotentialLevel, PotentialSets, build_grid, potential_edges, potential_tets,
+                     potential_triangles, prune)
 from . import synth
 
 __all__ = [
@@ -45,4 +48,6 @@ __all__ = [
     "NoAtoms", "NonFiniteCoordinate", "NonFiniteValue", "NonPositiveRadius", "OrthoResult", "PipelineConfig",
     "STAGE_NAMES", "SimplexKey", "TolerancePolicy", "as_ball_arrays", "closure_ok", "complex_stats",
     "compute_alpha_complex", "compute_alpha_complex_arrays", "default_engine", "simplex_compare", "synth",
+    "CellKey", "Grid", "PotentialLevel", "PotentialSets", "build_grid", "potential_edges", "potential_triangles",
+    "potential_tets", "prune", "read_complex", "stats_csv", "write_complex",
 ]

@@ -21,6 +21,9 @@
 
 #include <algorithm>
 #include <new>
+#include <atomic>
+#include <thread>
+#include <vector>
 
 using namespace axb;
 
@@ -1034,5 +1037,83 @@ extern "C" int axb_ortho_batch(axb_ctx *c, int64_t m, int k, const double *d_pts
     k_ortho_batch<<<blocks_for((size_t)m, 128), 128, 0, c->stream>>>(m, k, d_pts, d_r2, eps_sing, d_centers, d_sizes, d_singular);
     LAUNCH_CHECK(c);
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return AXB_OK;
+}
+
+
+// ------------------------------------------------------------ canonical text
+// write_complex (reference io.py:228-236): one line per simplex, "dim v0 [v1 [v2 [v3]]]\n", in
+// (dimension, lexicographic) order -- which is the order of the four arrays.  Pure host code
+// (threads over row ranges: sizes, prefix, write); no GPU involved.
+
+namespace {
+
+inline int dec_len(int64_t v) {
+    int n = 1;
+    uint64_t u = v < 0 ? (uint64_t)(-(v + 1)) + 1 : (uint64_t)v;
+    while (u >= 10) { u /= 10; ++n; }
+    return n + (v < 0 ? 1 : 0);
+}
+
+inline char *put_dec(char *p, int64_t v) {
+    char tmp[24];
+    int n = 0;
+    uint64_t u = v < 0 ? (uint64_t)(-(v + 1)) + 1 : (uint64_t)v;
+    do { tmp[n++] = (char)('0' + u % 10); u /= 10; } while (u);
+    if (v < 0) *p++ = '-';
+    while (n) *p++ = tmp[--n];
+    return p;
+}
+
+struct RowSpan { int dim; int64_t lo, hi; const int64_t *rows; int64_t bytes; };
+
+}  // namespace
+
+extern "C" int axb_format_complex(const int64_t counts[4], const int64_t *v, const int64_t *e, const int64_t *t,
+                                  const int64_t *q, char *out, int64_t capacity, int64_t *needed) {
+    if (!counts || !needed) return AXB_ERR_BAD_ARG;
+    const int64_t *arr[4] = {v, e, t, q};
+    for (int d = 0; d < 4; ++d)
+        if (counts[d] < 0 || (counts[d] > 0 && !arr[d])) return AXB_ERR_BAD_ARG;
+    unsigned nthreads = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    std::vector<RowSpan> spans;
+    for (int d = 0; d < 4; ++d) {
+        const int64_t chunk = std::max<int64_t>(1 << 16, (counts[d] + nthreads - 1) / nthreads);
+        for (int64_t lo = 0; lo < counts[d]; lo += chunk)
+            spans.push_back({d, lo, std::min(counts[d], lo + chunk), arr[d], 0});
+    }
+    auto for_spans = [&](auto fn) {
+        std::vector<std::thread> pool;
+        std::atomic<size_t> next{0};
+        const unsigned workers = (unsigned)std::min<size_t>(nthreads, std::max<size_t>(1, spans.size()));
+        for (unsigned w = 0; w < workers; ++w)
+            pool.emplace_back([&]() { for (size_t i; (i = next.fetch_add(1)) < spans.size();) fn(spans[i]); });
+        for (auto &th : pool) th.join();
+    };
+    for_spans([](RowSpan &s) {
+        const int k = s.dim + 1;
+        int64_t b = 0;
+        for (int64_t r = s.lo; r < s.hi; ++r) {
+            b += 2;                                          // dim digit + newline
+            for (int c = 0; c < k; ++c) b += 1 + dec_len(s.rows[r * k + c]);   // space + number
+        }
+        s.bytes = b;
+    });
+    int64_t total = 0;
+    std::vector<int64_t> offset(spans.size());
+    for (size_t i = 0; i < spans.size(); ++i) { offset[i] = total; total += spans[i].bytes; }
+    *needed = total;
+    if (!out || capacity < total) return out ? AXB_ERR_ARENA : AXB_OK;
+    std::vector<char *> where(spans.size());
+    for (size_t i = 0; i < spans.size(); ++i) where[i] = out + offset[i];
+    for_spans([&](RowSpan &s) {
+        char *p = where[&s - spans.data()];
+        const int k = s.dim + 1;
+        for (int64_t r = s.lo; r < s.hi; ++r) {
+            *p++ = (char)('0' + s.dim);
+            for (int c = 0; c < k; ++c) { *p++ = ' '; p = put_dec(p, s.rows[r * k + c]); }
+            *p++ = '\n';
+        }
+    });
     return AXB_OK;
 }

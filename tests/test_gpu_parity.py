@@ -271,3 +271,28 @@ def test_device_merge_rows_matches_numpy():
         want = np.unique(rows, axis=0)
         assert np.array_equal(got.reshape(-1, k), want)
     assert eng.merge_rows(torch.empty((0, 3), dtype=torch.int64, device="cuda"), 3, 10).shape[0] == 0
+
+
+def test_standalone_stage_api_against_reference_golden(gold_small):
+    """build_grid / potential_* / prune with the reference's names and result types."""
+    for name in ("g1_200_a14", "tetra_a05", "profile0_s0_a1.2", "near_regular_a15"):
+        rec = gold_small[name]
+        m = rec["meta"]
+        balls = [ax.Ball(tuple(c), float(r), i) for i, (c, r) in enumerate(zip(rec["centers"], rec["radii"]))]
+        cfg = ax.PipelineConfig(alpha=m["alpha"], tolerance=ax.TolerancePolicy(m["eps_abs"], m["eps_singular"]))
+        grid = ax.build_grid(balls, m["alpha"])
+        st, g = oracle.grid_build(rec["centers"], rec["radii"], m["alpha"])
+        assert grid.dims == g.dims and grid.cell_side == g.side and np.array_equal(grid.order, g.order)
+        assert grid.range_offsets[-1] == len(balls) and (np.diff(grid.occupied_keys) > 0).all()
+        edges = ax.potential_edges(grid, balls, cfg)
+        tris = ax.potential_triangles(edges, grid, balls, cfg)
+        tets = ax.potential_tets(tris, grid, balls, cfg)
+        for d, lv in ((1, edges), (2, tris), (3, tets)):
+            rows, cen, siz = rec[f"p{d}"]
+            assert np.array_equal(lv.simplices, rows.reshape(lv.simplices.shape))
+            assert np.array_equal(lv.centers.view(np.uint64), cen.view(np.uint64).reshape(lv.centers.shape))
+            assert np.array_equal(lv.sizes.view(np.uint64), siz.view(np.uint64))
+        k = ax.prune(ax.PotentialSets(edges=edges, triangles=tris, tets=tets, alpha=m["alpha"]), grid, balls, cfg)
+        assert list(k.counts()) == m["counts"]
+        assert hashlib.sha256(ax.write_complex(k).encode()).hexdigest() == m["sha256_complex"]
+        assert ax.read_complex(ax.write_complex(k)) == k

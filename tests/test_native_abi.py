@@ -48,3 +48,24 @@ def test_product_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 text = open(os.path.join(base, f)).read()
                 assert "import oracle" not in text and "alpha_oracle" not in text, f
+
+
+def test_write_complex_bytes_match_reference_golden(gold_config1, gold_small):
+    """The C++ formatter (no GPU needed) reproduces the reference's canonical document byte for byte."""
+    import hashlib
+
+    from paper_1908_05944_b200 import AlphaComplex, read_complex, stats_csv, write_complex
+
+    data, meta = gold_config1
+    for tag, m in meta.items():
+        k = AlphaComplex(data[f"{tag}__k0"], data[f"{tag}__k1"], data[f"{tag}__k2"], data[f"{tag}__k3"], m["alpha"], 1000)
+        text = write_complex(k)
+        assert hashlib.sha256(text.encode()).hexdigest() == m["sha256_complex"]
+        assert read_complex(text) == k
+    for name, rec in gold_small.items():
+        m = rec["meta"]
+        k = AlphaComplex(rec["k0"], rec["k1"], rec["k2"], rec["k3"], m["alpha"], len(rec["radii"]))
+        assert hashlib.sha256(write_complex(k).encode()).hexdigest() == m["sha256_complex"], name
+    tetra = gold_small["tetra_a05"]
+    k = AlphaComplex(tetra["k0"], tetra["k1"], tetra["k2"], tetra["k3"], 0.5, 4)
+    assert stats_csv(k) == "dim,count\n0,4\n1,6\n2,4\n3,1\ntotal,15\neuler,1\n"      # reference T/test_cli.py:25-35
