@@ -13,7 +13,7 @@ import paper_1908_05944_b200 as ax
 from paper_1908_05944_b200 import synth
 
 from conftest import GOLD
-from helpers import canonical_text, digest_arrays
+from helpers import canonical_text, digest_arrays, digest_values
 
 pytestmark = pytest.mark.gpu
 
@@ -288,10 +288,13 @@ def test_standalone_stage_api_against_reference_golden(gold_small):
         tris = ax.potential_triangles(edges, grid, balls, cfg)
         tets = ax.potential_tets(tris, grid, balls, cfg)
         for d, lv in ((1, edges), (2, tris), (3, tets)):
-            rows, cen, siz = rec[f"p{d}"]
-            assert np.array_equal(lv.simplices, rows.reshape(lv.simplices.shape))
-            assert np.array_equal(lv.centers.view(np.uint64), cen.view(np.uint64).reshape(lv.centers.shape))
-            assert np.array_equal(lv.sizes.view(np.uint64), siz.view(np.uint64))
+            pm = m["potentials"][f"p{d}"]
+            assert len(lv) == pm["count"]
+            assert digest_arrays(lv.simplices) == pm["sha256_rows"]                    # rows as the reference lists them
+            assert digest_values(lv.centers, lv.sizes) == pm["sha256_values"]          # cached fp64 ortho data, bitwise
+            if m["potentials_stored"]:
+                rows, cen, siz = rec[f"p{d}"]
+                assert np.array_equal(lv.simplices, rows.reshape(lv.simplices.shape))
         k = ax.prune(ax.PotentialSets(edges=edges, triangles=tris, tets=tets, alpha=m["alpha"]), grid, balls, cfg)
         assert list(k.counts()) == m["counts"]
         assert hashlib.sha256(ax.write_complex(k).encode()).hexdigest() == m["sha256_complex"]
