@@ -12,6 +12,7 @@
 #include "predicates.cuh"
 #include "prune.cuh"
 #include "scan.cuh"
+#include "sparse.cuh"
 
 #include <math.h>
 #include <stdarg.h>
@@ -74,6 +75,7 @@ struct axb_ctx {
     ErrRecord *errs = nullptr;
     int2 *dups = nullptr;
     int *key_of_ball = nullptr, *orig = nullptr, *rank = nullptr;
+    long long *key64_of_ball = nullptr, *skeys = nullptr;    // sparse mode (no dense cell table)
     int4 *cell_of_rank = nullptr;
     uint32_t *cell_start = nullptr;
     Atom *atoms = nullptr;
@@ -179,17 +181,86 @@ int fetch_counters(axb_ctx *c) {
     return AXB_OK;
 }
 
+// sparse twin of bin_balls: stable radix sort by 64-bit cell key (sparse.cuh)
+int bin_balls_sparse(axb_ctx *c, double side, const double lo[3], const int64_t dims[3]) {
+    const int n = (int)c->n;
+    const int64_t G = dims[0] * dims[1] * dims[2];
+    c->ginfo.cell_side = side;
+    for (int a = 0; a < 3; ++a) { c->ginfo.origin[a] = lo[a]; c->ginfo.dims[a] = dims[a]; }
+    c->ginfo.n_cells = G;
+    c->ginfo.n_balls = c->n;
+    GridView &g = c->g;
+    g.ox = lo[0]; g.oy = lo[1]; g.oz = lo[2];
+    g.side = side;
+    g.dx = (int)dims[0]; g.dy = (int)dims[1]; g.dz = (int)dims[2];
+    g.z_lo = 0;
+    g.dz_glob = (int)dims[2];
+    g.n = n;
+    g.cell_start = nullptr;
+    c->cell_start = nullptr;
+    c->key_of_ball = nullptr;
+    ARENA(c, c->key64_of_ball, long long, n);
+    ARENA(c, c->skeys, long long, n);
+    ARENA(c, c->orig, int, n);
+    ARENA(c, c->rank, int, n);
+    ARENA(c, c->cell_of_rank, int4, n);
+    ARENA(c, c->atoms, Atom, n);
+    ARENA(c, c->reach, double, n);
+    const size_t mark = c->arena_used;
+    long long *kbuf;
+    int *vbuf[2];
+    uint32_t *hist;
+    const int nchunks = (n + RS_CHUNK - 1) / RS_CHUNK;
+    ARENA(c, kbuf, long long, n);
+    ARENA(c, vbuf[0], int, n);
+    ARENA(c, vbuf[1], int, n);
+    ARENA(c, hist, uint32_t, (size_t)256 * nchunks + 2);
+    g.skeys = c->skeys;
+    k_cell_keys64<<<blocks_for(n, 256), 256, 0, c->stream>>>(c->d_xyz, g, c->key64_of_ball, c->skeys, vbuf[0]);
+    LAUNCH_CHECK(c);
+    int bits = 0;
+    while (bits < 63 && ((int64_t)1 << bits) < G) ++bits;
+    long long *kin = c->skeys, *kout = kbuf;
+    int cur = 0;
+    const unsigned rs_blocks = (unsigned)((nchunks + RS_WARPS - 1) / RS_WARPS);
+    for (int shift = 0; shift < std::max(bits, 1); shift += 8) {
+        k_rs_hist<<<rs_blocks, RS_WARPS * 32, 0, c->stream>>>(kin, n, shift, nchunks, hist);
+        LAUNCH_CHECK(c);
+        int st = device_scan(c, hist, (size_t)256 * nchunks, hist);
+        if (st != AXB_OK) return st;
+        k_rs_scatter<<<rs_blocks, RS_WARPS * 32, 0, c->stream>>>(kin, vbuf[cur], n, shift, nchunks, hist, kout, vbuf[cur ^ 1]);
+        LAUNCH_CHECK(c);
+        std::swap(kin, kout);
+        cur ^= 1;
+    }
+    if (kin != c->skeys)
+        CUDA_TRY(c, cudaMemcpyAsync(c->skeys, kin, sizeof(long long) * (size_t)n, cudaMemcpyDeviceToDevice, c->stream));
+    k_sparse_finalize<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->d_xyz, c->d_radii, c->skeys, vbuf[cur], g, c->prm.alpha,
+                                                               c->prm.eps_abs, c->orig, c->rank, c->cell_of_rank, c->atoms,
+                                                               c->reach, c->ctr, c->dups);
+    LAUNCH_CHECK(c);
+    c->arena_used = mark;
+    return AXB_OK;
+}
+
 // counting sort of the balls by cell key + rank-space records (grid.cuh).
 // dims = dims of the GLOBAL grid; [z_lo, z_hi) = loaded z layers (the whole grid unless this is a slab).
 int bin_balls(axb_ctx *c, double side, const double lo[3], const int64_t dims[3], int64_t z_lo, int64_t z_hi) {
     const int n = (int)c->n;
     const int64_t zc = z_hi - z_lo;
-    // guard the product before multiplying
+    if (dims[0] >= MAX_CELLS || dims[1] >= MAX_CELLS || dims[2] >= MAX_CELLS)
+        return fail(c, AXB_ERR_GRID_TOO_LARGE, "a grid axis of %lld x %lld x %lld cells exceeds 2^31",
+                    (long long)dims[0], (long long)dims[1], (long long)dims[2]);
     long double cells = (long double)dims[0] * (long double)dims[1] * (long double)zc;
-    if (cells >= (long double)MAX_CELLS || dims[0] >= MAX_CELLS || dims[1] >= MAX_CELLS || dims[2] >= MAX_CELLS)
-        return fail(c, AXB_ERR_GRID_TOO_LARGE,
-                    "grid of %lld x %lld x %lld cells exceeds the dense cell table limit (%lld cells)", (long long)dims[0],
-                    (long long)dims[1], (long long)zc, (long long)MAX_CELLS);
+    if (cells >= 4.0e18L) return fail(c, AXB_ERR_GRID_TOO_LARGE, "cell keys would overflow 63 bits");
+    // a dense table pays off while it is not much larger than the input; beyond that (or beyond 2^31 cells)
+    // bin by sorting the keys
+    const bool force_sparse = getenv("AXB_FORCE_SPARSE") != nullptr;      // test hook
+    const bool sparse = force_sparse || cells >= (long double)MAX_CELLS || cells > 64.0L * (long double)n + 16777216.0L;
+    if (sparse) {
+        if (c->slab_mode) return fail(c, AXB_ERR_GRID_TOO_LARGE, "slab sharding needs the dense cell table");
+        return bin_balls_sparse(c, side, lo, dims);
+    }
     const int64_t G = dims[0] * dims[1] * zc;
     c->ginfo.cell_side = side;
     for (int a = 0; a < 3; ++a) { c->ginfo.origin[a] = lo[a]; c->ginfo.dims[a] = dims[a]; }
@@ -216,6 +287,8 @@ int bin_balls(axb_ctx *c, double side, const double lo[3], const int64_t dims[3]
     ARENA(c, cell_count, uint32_t, (size_t)G + 2);
     ARENA(c, arrival, int, n);
     g.cell_start = c->cell_start;
+    g.skeys = nullptr;
+    c->skeys = nullptr;
 
     CUDA_TRY(c, cudaMemsetAsync(cell_count, 0, ((size_t)G + 2) * sizeof(uint32_t), c->stream));
     k_cell_keys<<<blocks_for(n, 256), 256, 0, c->stream>>>(c->d_xyz, g, c->key_of_ball, cell_count);
@@ -570,6 +643,7 @@ extern "C" int axb_grid_build_slab(axb_ctx *c, int64_t n, const double *d_xyz, c
 extern "C" int axb_slab_rank_range(axb_ctx *c, int64_t z_own_lo, int64_t z_own_hi, int64_t *rank_lo, int64_t *rank_hi) {
     if (!c || !rank_lo || !rank_hi) return AXB_ERR_BAD_ARG;
     if (c->state < S_GRID) return fail(c, AXB_ERR_STATE, "axb_slab_rank_range before axb_grid_build");
+    if (!c->cell_start) return fail(c, AXB_ERR_STATE, "axb_slab_rank_range needs the dense cell table");
     const GridView &g = c->g;
     int64_t a = std::min<int64_t>(std::max<int64_t>(z_own_lo - g.z_lo, 0), g.dz);
     int64_t b = std::min<int64_t>(std::max<int64_t>(z_own_hi - g.z_lo, 0), g.dz);
@@ -593,8 +667,12 @@ extern "C" int axb_grid_get_info(const axb_ctx *c, axb_grid_info *out) {
 extern "C" int axb_grid_export(axb_ctx *c, int64_t *d_order, int64_t *d_rank, int64_t *d_cells) {
     if (!c) return AXB_ERR_BAD_ARG;
     if (c->state < S_GRID) return fail(c, AXB_ERR_STATE, "axb_grid_export before axb_grid_build");
-    k_grid_export<<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>((int)c->n, c->orig, c->rank, c->key_of_ball,
-                                                                       d_order, d_rank, d_cells);
+    if (c->skeys)
+        k_grid_export64<<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>((int)c->n, c->orig, c->rank, c->key64_of_ball,
+                                                                             d_order, d_rank, d_cells);
+    else
+        k_grid_export<<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>((int)c->n, c->orig, c->rank, c->key_of_ball,
+                                                                           d_order, d_rank, d_cells);
     LAUNCH_CHECK(c);
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return AXB_OK;

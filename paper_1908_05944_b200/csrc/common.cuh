@@ -24,7 +24,9 @@ struct GridView {
     int z_lo;                 // first loaded z layer of the global grid (0 unless this is a slab)
     int dz_glob;              // z layers of the global grid (== dz unless this is a slab)
     int n;                    // balls
-    const uint32_t *cell_start;   // (n_cells + 1) exclusive prefix of per-cell counts
+    const uint32_t *cell_start;   // dense mode: (n_cells + 1) exclusive prefix of per-cell counts
+    const long long *skeys;       // sparse mode (cell_start == nullptr): the n cell keys in rank order (ascending);
+                                  // the reference's implicit storage (grid.py:38-39, 76-88) without the table
 };
 
 // Scalar run parameters needed by the predicate kernels.

@@ -132,10 +132,9 @@ __global__ void __launch_bounds__(EST_WARPS * 32, 4) k_edges(EstParams P, int ra
                 else { int q = lane - 3; oz = 1 + q / 5; oy = q % 5 - 2; }
                 int y = cy + oy, z = cz + oz;
                 if (y >= 0 && y < g.dy && z < g.dz) {
-                    int row = g.dx * (y + g.dy * z);
                     int x0 = max(cx - 2, 0), x1 = min(cx + 2, g.dx - 1);
-                    int s = (int)__ldg(g.cell_start + row + x0);
-                    int e = (int)__ldg(g.cell_start + row + x1 + 1);
+                    int s, e;
+                    row_range(g, x0, x1, y, z, s, e);
                     if (lane == 0) s = t + 1;               // own row: only ranks above t
                     rs = s;
                     rc = max(e - s, 0);

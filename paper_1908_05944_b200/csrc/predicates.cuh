@@ -185,53 +185,35 @@ AXB_HD int cell_coord_z(double v, const GridView &g) {
 }
 
 #ifdef __CUDACC__
-// pipeline.py:286-313 for one simplex: true iff no non-incident ball of the
-// 27-cell block around the ortho-centre has power distance < size - eps_abs.
-// inc0..inc3 are the RANKS of the incident balls (-1 = unused).
-__device__ __forceinline__ bool ac2_pass_v2(const GridView &g, const Atom *__restrict__ atoms, double cx, double cy,
-                                         double cz, double thr, int inc0, int inc1, int inc2, int inc3) {
-    const int ix = cell_coord(cx, g.ox, g.side, g.dx);
-    const int iy = cell_coord(cy, g.oy, g.side, g.dy);
-    const int iz = cell_coord_z(cz, g);
-    const int x0 = max(ix - 1, 0), x1 = min(ix + 1, g.dx - 1);
-    // The 9 rows of the 3x3x3 block, the centre's own row first (a dominating ball is usually
-    // close, so the early exit fires sooner); all 18 range bounds are fetched before any atom so
-    // the loads overlap.  The visiting order does not change the boolean.
-    int rs[9], re[9];
-#pragma unroll
-    for (int r = 0; r < 9; ++r) {
-        const int oy = (r == 1 || r == 5 || r == 7) ? -1 : ((r == 2 || r == 6 || r == 8) ? 1 : 0);
-        const int oz = (r == 3 || r == 5 || r == 6) ? -1 : ((r == 4 || r == 7 || r == 8) ? 1 : 0);
-        const int y = iy + oy, z = iz + oz;
-        const bool in = y >= 0 && y < g.dy && z >= 0 && z < g.dz;
-        const int row = g.dx * (y + g.dy * z);
-        rs[r] = in ? (int)__ldg(g.cell_start + row + x0) : 0;
-        re[r] = in ? (int)__ldg(g.cell_start + row + x1 + 1) : 0;
+// Rank range [s, e) of the balls in cells x0..x1 of row (y, z): consecutive cells of a row are
+// consecutive keys, and the balls are sorted by key, so it is one contiguous range.
+// Dense mode reads the cell table; sparse mode binary-searches the sorted keys (the reference's
+// searchsorted over occupied keys, grid.py:80-82).
+__device__ __forceinline__ int rank_lower_bound(const GridView &g, long long key) {
+    int lo = 0, hi = g.n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(g.skeys + mid) < key) lo = mid + 1; else hi = mid;
     }
-#pragma unroll
-    for (int r = 0; r < 9; ++r) {
-        for (int t = rs[r]; t < re[r]; t += 2) {
-            const int t1 = min(t + 1, re[r] - 1);
-            const double2 *q0 = reinterpret_cast<const double2 *>(atoms + t);
-            const double2 *q1 = reinterpret_cast<const double2 *>(atoms + t1);
-            const double2 a0 = __ldg(q0), b0 = __ldg(q0 + 1), a1 = __ldg(q1), b1 = __ldg(q1 + 1);
-            {
-                const double ddx = a0.x - cx, ddy = a0.y - cy, ddz = b0.x - cz;
-                const double dp = ((ddx * ddx + ddy * ddy) + ddz * ddz) - b0.y;
-                if (dp < thr && t != inc0 && t != inc1 && t != inc2 && t != inc3) return false;
-            }
-            {
-                const double ddx = a1.x - cx, ddy = a1.y - cy, ddz = b1.x - cz;
-                const double dp = ((ddx * ddx + ddy * ddy) + ddz * ddz) - b1.y;
-                if (dp < thr && t1 != inc0 && t1 != inc1 && t1 != inc2 && t1 != inc3) return false;
-            }
-        }
-    }
-    return true;
+    return lo;
 }
 
-// straightforward variant: rows in key order, bounds fetched row by row
-__device__ __forceinline__ bool ac2_pass_v1(const GridView &g, const Atom *__restrict__ atoms, double cx, double cy,
+__device__ __forceinline__ void row_range(const GridView &g, int x0, int x1, int y, int z, int &s, int &e) {
+    if (g.cell_start) {
+        const int row = g.dx * (y + g.dy * z);
+        s = (int)__ldg(g.cell_start + row + x0);
+        e = (int)__ldg(g.cell_start + row + x1 + 1);
+    } else {
+        const long long row = (long long)g.dx * ((long long)y + (long long)g.dy * (long long)z);
+        s = rank_lower_bound(g, row + x0);
+        e = rank_lower_bound(g, row + x1 + 1);
+    }
+}
+
+// pipeline.py:286-313 for one simplex: true iff no non-incident ball of the 27-cell block around the
+// ortho-centre has power distance < size - eps_abs.  inc0..inc3 are the RANKS of the incident balls
+// (-1 = unused).  Rows in key order, early exit at the first dominating ball.
+__device__ __forceinline__ bool ac2_pass(const GridView &g, const Atom *__restrict__ atoms, double cx, double cy,
                                             double cz, double thr, int inc0, int inc1, int inc2, int inc3) {
     int ix = cell_coord(cx, g.ox, g.side, g.dx);
     int iy = cell_coord(cy, g.oy, g.side, g.dy);
@@ -241,9 +223,8 @@ __device__ __forceinline__ bool ac2_pass_v1(const GridView &g, const Atom *__res
     int z0 = max(iz - 1, 0), z1 = min(iz + 1, g.dz - 1);
     for (int z = z0; z <= z1; ++z)
         for (int y = y0; y <= y1; ++y) {
-            int row = g.dx * (y + g.dy * z);
-            int s = (int)__ldg(g.cell_start + row + x0);
-            int e = (int)__ldg(g.cell_start + row + x1 + 1);
+            int s, e;
+            row_range(g, x0, x1, y, z, s, e);
             for (int t = s; t < e; ++t) {
                 if (t == inc0 || t == inc1 || t == inc2 || t == inc3) continue;
                 const double2 *q = reinterpret_cast<const double2 *>(atoms + t);
@@ -254,18 +235,6 @@ __device__ __forceinline__ bool ac2_pass_v1(const GridView &g, const Atom *__res
             }
         }
     return true;
-}
-
-#ifndef AXB_AC2_VARIANT
-#define AXB_AC2_VARIANT 1
-#endif
-__device__ __forceinline__ bool ac2_pass(const GridView &g, const Atom *__restrict__ atoms, double cx, double cy,
-                                         double cz, double thr, int inc0, int inc1, int inc2, int inc3) {
-#if AXB_AC2_VARIANT == 2
-    return ac2_pass_v2(g, atoms, cx, cy, cz, thr, inc0, inc1, inc2, inc3);
-#else
-    return ac2_pass_v1(g, atoms, cx, cy, cz, thr, inc0, inc1, inc2, inc3);
-#endif
 }
 
 __device__ __forceinline__ Atom load_atom(const Atom *__restrict__ atoms, int t) {

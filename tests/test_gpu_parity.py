@@ -299,3 +299,34 @@ def test_standalone_stage_api_against_reference_golden(gold_small):
         assert list(k.counts()) == m["counts"]
         assert hashlib.sha256(ax.write_complex(k).encode()).hexdigest() == m["sha256_complex"]
         assert ax.read_complex(ax.write_complex(k)) == k
+
+
+def test_sparse_grid_mode(monkeypatch):
+    """Widely spread inputs (the dense cell table would need > 2^31 cells) go through the sorted-key
+    grid; forcing that mode on ordinary inputs must not change a bit either."""
+    # two globules 2e6 A apart plus a stray ball: ~1e18 cells
+    c1, r1 = synth.random_globule(400, 3, 1.0, (1.2, 1.9), 1 / 12)
+    c2, r2 = synth.random_globule(300, 4, 1.0, (1.2, 1.9), 1 / 12)
+    c = np.concatenate([c1, c2 + np.array([2.0e6, -1.5e6, 1.0e6]), np.array([[5.0e5, 5.0e5, 5.0e5]])])
+    r = np.concatenate([r1, r2, [1.5]])
+    perm = np.random.default_rng(1).permutation(len(r))
+    c, r = np.ascontiguousarray(c[perm]), r[perm]
+    for alpha in (0.0, 1.4):
+        ref = oracle.compute(c, r, alpha, keep_potentials=True)
+        assert ref.status == oracle.OK
+        k = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=alpha))
+        assert_same_complex(k, ref, f"sparse a={alpha}")
+    grid = ax.build_grid([ax.Ball(tuple(p), float(q), i) for i, (p, q) in enumerate(zip(c, r))], 0.0)
+    st, g = oracle.grid_build(c, r, 0.0)
+    assert grid.dims == g.dims and np.array_equal(grid.order, g.order) and np.array_equal(grid.ball_cells, g.cells)
+    # ordinary inputs, sparse mode forced
+    monkeypatch.setenv("AXB_FORCE_SPARSE", "1")
+    for (cc, rr), alpha, eps in ((synth.jittered_lattice(30_000, 6), 1.4, 1e-300),
+                                 (synth.adversarial_density(20_000, 1, shuffle=True), 0.0, 1e-300),
+                                 (synth.random_globule(160, 9, 0.35, (0.4, 1.6), 0.9), 1.0, 1e-300)):
+        ref = oracle.compute(cc, rr, alpha, eps_singular=eps, threads=os.cpu_count(), chunk=2000)
+        k = ax.compute_alpha_complex_arrays(cc, rr, ax.PipelineConfig(alpha=alpha, tolerance=ax.TolerancePolicy(1e-9, eps)))
+        assert_same_complex(k, ref, "forced sparse")
+    dup = np.array([[0, 0, 0], [1e7, 1, 1], [0, 0, 0.0]])
+    with pytest.raises(ax.DuplicateCenter, match="balls 0 and 2 share"):
+        ax.compute_alpha_complex_arrays(dup, np.array([1, 1, 1.5]), ax.PipelineConfig(alpha=0.0))
