@@ -34,6 +34,7 @@ struct Tol {
     double lim_a;             // alpha + eps_abs         (pipeline.py:358)
     double eps_abs;
     double eps_sing;
+    double r2max;             // largest squared radius of the input (AC2 reach bound)
 };
 
 // Device-side counters / status block (one per context, zeroed per run).

@@ -211,18 +211,46 @@ __device__ __forceinline__ void row_range(const GridView &g, int x0, int x1, int
 }
 
 // pipeline.py:286-313 for one simplex: true iff no non-incident ball of the 27-cell block around the
-// ortho-centre has power distance < size - eps_abs.  inc0..inc3 are the RANKS of the incident balls
-// (-1 = unused).  Rows in key order, early exit at the first dominating ball.
+// ortho-centre has power distance < thr = size - eps_abs.  inc0..inc3 are the RANKS of the incident
+// balls (-1 = unused).  Early exit at the first dominating ball.
+//
+// Exact trimming of the block: a ball p can only dominate if |p - c|^2 - r_p^2 < thr, hence only if
+// |p - c|^2 < r2max + thr =: R2 (r2max = largest squared radius of the input).  Cells of the block
+// whose nearest point is farther than sqrt(R2) from c (with a 1e-9 slack, far above any rounding)
+// cannot hold such a ball and are skipped -- often most of the 27.  The boolean is unchanged.
 __device__ __forceinline__ bool ac2_pass(const GridView &g, const Atom *__restrict__ atoms, double cx, double cy,
-                                            double cz, double thr, int inc0, int inc1, int inc2, int inc3) {
-    int ix = cell_coord(cx, g.ox, g.side, g.dx);
-    int iy = cell_coord(cy, g.oy, g.side, g.dy);
-    int iz = cell_coord_z(cz, g);
-    int x0 = max(ix - 1, 0), x1 = min(ix + 1, g.dx - 1);
-    int y0 = max(iy - 1, 0), y1 = min(iy + 1, g.dy - 1);
-    int z0 = max(iz - 1, 0), z1 = min(iz + 1, g.dz - 1);
-    for (int z = z0; z <= z1; ++z)
+                                         double cz, double thr, double r2max, int inc0, int inc1, int inc2, int inc3) {
+    double R2 = r2max + thr;
+    if (!(R2 > 0.0)) return true;                       // dp >= -r_p^2 >= -r2max >= thr for every ball
+    R2 = R2 * (1.0 + 1e-9) + 1e-9;
+    const int ix = cell_coord(cx, g.ox, g.side, g.dx);
+    const int iy = cell_coord(cy, g.oy, g.side, g.dy);
+    const int iz = cell_coord_z(cz, g);
+    // distances from c to the faces of its own cell (>= 0; c may sit outside a clamped border cell)
+    const double xa = g.ox + (double)ix * g.side, ya = g.oy + (double)iy * g.side;
+    const double za = g.oz + (double)(iz + g.z_lo) * g.side;
+    const double dxl = fmax(cx - xa, 0.0), dxh = fmax(xa + g.side - cx, 0.0);
+    const double dyl = fmax(cy - ya, 0.0), dyh = fmax(ya + g.side - cy, 0.0);
+    const double dzl = fmax(cz - za, 0.0), dzh = fmax(za + g.side - cz, 0.0);
+    const double ox2 = fmax(fmax(xa - cx, cx - (xa + g.side)), 0.0);     // distance to the own cell itself (0 inside)
+    const double oy2 = fmax(fmax(ya - cy, cy - (ya + g.side)), 0.0);
+    const double oz2 = fmax(fmax(za - cz, cz - (za + g.side)), 0.0);
+    const int y0 = max(iy - 1, 0), y1 = min(iy + 1, g.dy - 1);
+    const int z0 = max(iz - 1, 0), z1 = min(iz + 1, g.dz - 1);
+    for (int z = z0; z <= z1; ++z) {
+        const double gz = z < iz ? dzl : (z > iz ? dzh : oz2);
+        const double rem_z = R2 - gz * gz;
+        if (rem_z < 0.0) continue;
         for (int y = y0; y <= y1; ++y) {
+            const double gy = y < iy ? dyl : (y > iy ? dyh : oy2);
+            const double rem = rem_z - gy * gy;
+            if (rem < 0.0) continue;
+            int x0 = ix, x1 = ix;
+            if (ix > 0 && dxl * dxl <= rem) x0 = ix - 1;
+            if (ix < g.dx - 1 && dxh * dxh <= rem) x1 = ix + 1;
+            if (ox2 * ox2 > rem) {                       // even the own column is out of reach (clamped centre)
+                if (x0 == ix && x1 == ix) continue;
+            }
             int s, e;
             row_range(g, x0, x1, y, z, s, e);
             for (int t = s; t < e; ++t) {
@@ -234,6 +262,7 @@ __device__ __forceinline__ bool ac2_pass(const GridView &g, const Atom *__restri
                 if (dp < thr) return false;
             }
         }
+    }
     return true;
 }
 

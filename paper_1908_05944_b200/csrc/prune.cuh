@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256) k_prune_tets(PruneParams P) {
         const Atom aw = load_atom(P.atoms, r.z), ax = load_atom(P.atoms, r.w);
         const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z), ox = __ldg(P.orig + r.w);
         const Ortho o = ortho_tet(ou, au, ov, av, ow, aw, ox, ax, P.tol.eps_sing);
-        if (!ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, r.w)) continue;
+        if (!ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, P.tol.r2max, r.x, r.y, r.z, r.w)) continue;
         int row[4] = {ou, ov, ow, ox};
 #pragma unroll
         for (int a = 1; a < 4; ++a)
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_tris(PruneParams P) {
             const Atom au = load_atom(P.atoms, r.x), av = load_atom(P.atoms, r.y), aw = load_atom(P.atoms, r.z);
             const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z);
             const Ortho o = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);
-            if (!ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, -1)) continue;
+            if (!ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, P.tol.r2max, r.x, r.y, r.z, -1)) continue;
             mark_tri(P, bu + i, j, min3(ou, ov, ow));
             mark_edge(P, bu + i, min(ou, ov));
             mark_edge(P, bu + j, min(ou, ow));
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_edges(PruneParams P) {
             const Atom au = load_atom(P.atoms, u), av = load_atom(P.atoms, v);
             const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + v);
             const Ortho o = ortho_edge(ou, au, ov, av, P.tol.eps_sing);
-            if (ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, u, v, -1, -1)) {
+            if (ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, P.tol.r2max, u, v, -1, -1)) {
                 mark_edge(P, e, min(ou, ov));
                 P.vflag[u] = 1;
                 P.vflag[v] = 1;
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(256) k_prune_vertices(PruneParams P, int rank_
         if (!kept) {
             const Atom a = load_atom(P.atoms, t);
             if (-a.r2 <= P.tol.lim_a)                                  // pipeline.py:520
-                kept = ac2_pass(P.g, P.atoms, a.x, a.y, a.z, -a.r2 - P.tol.eps_abs, t, -1, -1, -1);
+                kept = ac2_pass(P.g, P.atoms, a.x, a.y, a.z, -a.r2 - P.tol.eps_abs, P.tol.r2max, t, -1, -1, -1);
         }
     }
     P.vkeep[__ldg(P.orig + t)] = kept ? 1u : 0u;
