@@ -590,6 +590,7 @@ int grid_build_common(axb_ctx *c, int64_t n, const double *d_xyz, const double *
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     const BoundsPartial &b = c->h->bounds;
     c->tol.r2max = b.rmax * b.rmax;
+    c->tol.reach_max = sqrt(std::max(c->tol.r2max + prm->alpha + prm->eps_abs, 0.0)) * (1.0 + 1e-12);
     if (b.first_bad != 0xffffffffu) {                     // pipeline.py:235-237
         c->err_verts[0] = b.first_bad;
         c->err_nverts = 1;

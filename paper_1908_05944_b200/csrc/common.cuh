@@ -35,6 +35,7 @@ struct Tol {
     double eps_abs;
     double eps_sing;
     double r2max;             // largest squared radius of the input (AC2 reach bound)
+    double reach_max;         // upper bound of every ball's reach sqrt(r^2 + alpha + eps_abs) (edge candidate bound)
 };
 
 // Device-side counters / status block (one per context, zeroed per run).
