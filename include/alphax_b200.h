@@ -146,6 +146,12 @@ int axb_sync_check(axb_ctx *ctx);
  * grid_build -> potential(0,n) -> prune -> canonicalize. */
 int axb_compute(axb_ctx *ctx, int64_t n, const double *d_xyz, const double *d_radii,
                 const axb_params *params, int64_t counts[4]);
+/* One z-slab of a sharded run in one call (what one GPU of a multi-GPU job executes):
+ * axb_grid_build_slab -> generators of the OWNED layers [z_own_lo, z_own_hi) -> prune -> canonicalize.
+ * Rows exported afterwards carry global ball indices. */
+int axb_compute_slab(axb_ctx *ctx, int64_t n, const double *d_xyz, const double *d_radii,
+                     const int64_t *d_global_index, const axb_params *params, const axb_slab *slab,
+                     int64_t z_own_lo, int64_t z_own_hi, int64_t counts[4]);
 /* Same from HOST buffers: copies inputs to the arena, runs axb_compute. */
 int axb_compute_host(axb_ctx *ctx, int64_t n, const double *h_xyz, const double *h_radii,
                      const axb_params *params, int64_t counts[4]);

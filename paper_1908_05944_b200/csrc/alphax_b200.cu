@@ -998,6 +998,24 @@ extern "C" int axb_compute(axb_ctx *c, int64_t n, const double *d_xyz, const dou
     return st;
 }
 
+extern "C" int axb_compute_slab(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii,
+                                const int64_t *d_global_index, const axb_params *prm, const axb_slab *slab,
+                                int64_t z_own_lo, int64_t z_own_hi, int64_t counts[4]) {
+    if (!c || !slab) return AXB_ERR_BAD_ARG;
+    int st = axb_grid_build_slab(c, n, d_xyz, d_radii, d_global_index, prm, slab);
+    if (st != AXB_OK) return st;
+    int64_t lo = 0, hi = 0;
+    if ((st = axb_slab_rank_range(c, z_own_lo, z_own_hi, &lo, &hi)) != AXB_OK) return st;
+    c->cull = true;
+    st = run_potential(c, lo, hi);
+    c->cull = false;
+    if (st != AXB_OK) return st;
+    if ((st = run_prune(c)) != AXB_OK) return st;
+    st = run_canonicalize(c, counts);
+    if (st == AXB_ERR_ARENA + 1000) return fail(c, AXB_ERR_INTERNAL, "a potential list overflowed after it was sized exactly");
+    return st;
+}
+
 extern "C" int axb_compute_host(axb_ctx *c, int64_t n, const double *h_xyz, const double *h_radii, const axb_params *prm,
                                 int64_t counts[4]) {
     if (!c) return AXB_ERR_BAD_ARG;

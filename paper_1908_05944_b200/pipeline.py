@@ -428,20 +428,9 @@ class Engine:
 
         def run():
             lib, h = self.lib, self.handle
-            st = lib.axb_grid_build_slab(h, n, centers.data_ptr(), radii.data_ptr(), global_index.data_ptr(),
-                                         C.byref(prm), C.byref(geo))
-            if st != N.OK:
-                return st
-            lo, hi = C.c_int64(), C.c_int64()
-            st = lib.axb_slab_rank_range(h, int(slab.z_own_lo), int(slab.z_own_hi), C.byref(lo), C.byref(hi))
-            if st != N.OK:
-                return st
-            for call in (lambda: lib.axb_potential(h, lo.value, hi.value), lambda: lib.axb_prune(h)):
-                st = call()
-                if st != N.OK:
-                    return st
             counts = (C.c_int64 * 4)()
-            st = lib.axb_canonicalize(h, counts)
+            st = lib.axb_compute_slab(h, n, centers.data_ptr(), radii.data_ptr(), global_index.data_ptr(), C.byref(prm),
+                                      C.byref(geo), int(slab.z_own_lo), int(slab.z_own_hi), counts)
             if st != N.OK:
                 return st
             outs.clear()
