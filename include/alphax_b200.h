@@ -155,6 +155,16 @@ int axb_compute_slab(axb_ctx *ctx, int64_t n, const double *d_xyz, const double 
 /* Same from HOST buffers: copies inputs to the arena, runs axb_compute. */
 int axb_compute_host(axb_ctx *ctx, int64_t n, const double *h_xyz, const double *h_radii,
                      const axb_params *params, int64_t counts[4]);
+/* Pipelined variant of axb_compute_host + axb_export_host: `begin` runs up to the potential stage and
+ * returns row CAPACITIES for the four host arrays (tight upper bounds known at that point); the
+ * caller allocates them (pinned memory makes the copies asynchronous) and calls `finish`, which
+ * canonicalises every dimension as soon as it is final and copies it to the host on a second stream
+ * while the remaining kernels run.  counts[d] <= capacity[d] rows of each array are valid.
+ * AXB_ERR_STATE from `finish` means a capacity bound did not hold (then use the two-call path). */
+int axb_compute_host_begin(axb_ctx *ctx, int64_t n, const double *h_xyz, const double *h_radii,
+                           const axb_params *params, int64_t capacity[4]);
+int axb_compute_host_finish(axb_ctx *ctx, int64_t *h_vertices, int64_t *h_edges, int64_t *h_triangles,
+                            int64_t *h_tets, int64_t counts[4]);
 /* axb_export into HOST buffers (pinned or pageable). */
 int axb_export_host(axb_ctx *ctx, int64_t *h_vertices, int64_t *h_edges, int64_t *h_triangles, int64_t *h_tets);
 

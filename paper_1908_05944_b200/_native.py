@@ -27,7 +27,8 @@ SYMBOLS = (
     "axb_last_error", "axb_grid_build", "axb_grid_build_slab", "axb_slab_rank_range", "axb_merge_rows", "axb_compute_slab",
     "axb_grid_get_info", "axb_grid_export", "axb_potential",
     "axb_potential_counts", "axb_potential_export", "axb_prune", "axb_canonicalize", "axb_export",
-    "axb_sync_check", "axb_compute", "axb_compute_host", "axb_export_host", "axb_stage_ms",
+    "axb_sync_check", "axb_compute", "axb_compute_host", "axb_export_host", "axb_compute_host_begin",
+    "axb_compute_host_finish", "axb_stage_ms",
     "axb_kernel_launches", "axb_ortho_batch", "axb_format_complex",
 )
 
@@ -91,6 +92,8 @@ def load() -> C.CDLL:
         "axb_compute": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params), pi64]),
         "axb_compute_host": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params), pi64]),
         "axb_export_host": (C.c_int, [vp, vp, vp, vp, vp]),
+        "axb_compute_host_begin": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params), pi64]),
+        "axb_compute_host_finish": (C.c_int, [vp, vp, vp, vp, vp, pi64]),
         "axb_stage_ms": (C.c_int, [vp, C.POINTER(C.c_float)]),
         "axb_kernel_launches": (i64, [vp]),
         "axb_format_complex": (C.c_int, [pi64, vp, vp, vp, vp, vp, i64, pi64]),

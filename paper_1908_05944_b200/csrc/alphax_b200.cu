@@ -49,6 +49,8 @@ struct axb_ctx {
     int device = 0;
     int sm_count = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;     // D2H of finished dimensions overlaps the remaining kernels
+    cudaEvent_t dim_ready[4] = {}, dim_count[4] = {};
     char *arena = nullptr;
     size_t arena_bytes = 0, arena_used = 0, arena_needed = 0;
     HostBlock *h = nullptr;
@@ -96,6 +98,7 @@ struct axb_ctx {
     int4 *tmp2 = nullptr, *tmp3 = nullptr;
     uint32_t n_pe = 0, n_pt = 0, n_pq = 0;
     int64_t counts[4] = {0, 0, 0, 0};
+    int64_t host_cap[4] = {0, 0, 0, 0};
     size_t mark_after_grid = 0, mark_after_edges = 0;
     int cull_mask = 1;                    // bit 0: tets, bit 1: triangles (A/B switch AXB_CULL=0..3)
     bool cull = false;                    // one-call path: k_tri_tet2 settles partner-dominated simplices itself
@@ -459,6 +462,9 @@ extern "C" int axb_ctx_create(axb_ctx **out, int device) {
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void **>(&c->h), sizeof(HostBlock), cudaHostAllocDefault);
     for (int i = 0; e == cudaSuccess && i < AXB_ST_COUNT + 2; ++i) e = cudaEventCreate(&c->ev[i]);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+    for (int i = 0; e == cudaSuccess && i < 4; ++i) e = cudaEventCreateWithFlags(&c->dim_ready[i], cudaEventDisableTiming);
+    for (int i = 0; e == cudaSuccess && i < 4; ++i) e = cudaEventCreateWithFlags(&c->dim_count[i], cudaEventDisableTiming);
     if (e != cudaSuccess) {
         fprintf(stderr, "axb_ctx_create: %s\n", cudaGetErrorString(e));
         delete c;
@@ -473,6 +479,11 @@ extern "C" void axb_ctx_destroy(axb_ctx *c) {
     cudaSetDevice(c->device);
     for (int i = 0; i < AXB_ST_COUNT + 2; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    for (int i = 0; i < 4; ++i) {
+        if (c->dim_ready[i]) cudaEventDestroy(c->dim_ready[i]);
+        if (c->dim_count[i]) cudaEventDestroy(c->dim_count[i]);
+    }
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->h) cudaFreeHost(c->h);
     delete c;
 }
@@ -961,15 +972,15 @@ extern "C" int axb_export(axb_ctx *c, int64_t *d_v, int64_t *d_e, int64_t *d_t, 
         LAUNCH_CHECK(c);
     }
     if (d_e && c->counts[1]) {
-        k_emit_edges<<<blocks_for((size_t)c->counts[1], 256), 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->counts[1], c->gidx, d_e, c->ctr);
+        k_emit_edges<<<blocks_for((size_t)c->counts[1], 256), 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->counts[1], nullptr, c->gidx, d_e, c->ctr);
         LAUNCH_CHECK(c);
     }
     if (d_t && c->counts[2]) {
-        k_emit_tris<<<blocks_for((size_t)c->counts[2], 256), 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->counts[2], c->gidx, d_t, c->ctr);
+        k_emit_tris<<<blocks_for((size_t)c->counts[2], 256), 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->counts[2], nullptr, c->gidx, d_t, c->ctr);
         LAUNCH_CHECK(c);
     }
     if (d_q && c->counts[3]) {
-        k_emit_tets<<<blocks_for((size_t)c->counts[3], 256), 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->counts[3], c->gidx, d_q, c->ctr);
+        k_emit_tets<<<blocks_for((size_t)c->counts[3], 256), 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->counts[3], nullptr, c->gidx, d_q, c->ctr);
         LAUNCH_CHECK(c);
     }
     return mark_event(c, AXB_ST_COUNT + 1);
@@ -1037,6 +1048,147 @@ extern "C" int axb_compute_host(axb_ctx *c, int64_t n, const double *h_xyz, cons
     c->arena_bytes = full;
     if (st == AXB_ERR_ARENA) c->arena_needed += in_bytes;
     return st;
+}
+
+// ---- pipelined host path: the D2H copy of a finished dimension overlaps the remaining kernels ----
+// begin: inputs up, grid, potential stage; returns row CAPACITIES for the four host arrays (tight upper
+// bounds: K0 <= n, K1 <= potential edges, K2 <= ~potential triangles, K3 <= potential tets).
+// finish: tets are final after their prune kernel -> canonicalise + start their copy on a second stream;
+// then triangles, edges, vertices the same way; one synchronisation at the very end.
+extern "C" int axb_compute_host_begin(axb_ctx *c, int64_t n, const double *h_xyz, const double *h_radii,
+                                      const axb_params *prm, int64_t capacity[4]) {
+    if (!c || !capacity) return AXB_ERR_BAD_ARG;
+    if (n <= 0) return fail(c, AXB_ERR_EMPTY, "at least one ball is required");
+    if (!h_xyz || !h_radii) return fail(c, AXB_ERR_BAD_ARG, "null input pointer");
+    size_t in_bytes = ((size_t)n * 4 * sizeof(double) + ARENA_ALIGN - 1) / ARENA_ALIGN * ARENA_ALIGN;
+    if (!c->arena || c->arena_bytes < in_bytes + ARENA_ALIGN) {
+        c->arena_needed = in_bytes + axb_arena_hint(n, prm ? prm->alpha : 0.0, 1.9);
+        return fail(c, AXB_ERR_ARENA, "scratch arena too small for the input copy");
+    }
+    double *d_in = reinterpret_cast<double *>(c->arena + c->arena_bytes - in_bytes);
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemcpyAsync(d_in, h_xyz, (size_t)n * 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(d_in + 3 * (size_t)n, h_radii, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    const size_t full = c->arena_bytes;
+    c->arena_bytes = full - in_bytes;
+    int st = axb_grid_build(c, n, d_in, d_in + 3 * (size_t)n, prm);
+    if (st == AXB_OK) {
+        c->cull = true;
+        st = run_potential(c, 0, n);
+        c->cull = false;
+    }
+    c->arena_bytes = full;
+    if (st == AXB_ERR_ARENA) c->arena_needed += in_bytes;
+    if (st != AXB_OK) return st;
+    capacity[0] = n;
+    capacity[1] = c->n_pe;
+    capacity[2] = (int64_t)c->n_pt + c->n_pt / 8 + 1024;     // inherited faces outside the potential list are rare
+    capacity[3] = c->n_pq;
+    for (int d = 0; d < 4; ++d) c->host_cap[d] = capacity[d];
+    return AXB_OK;
+}
+
+extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, int64_t *h_t, int64_t *h_q,
+                                       int64_t counts[4]) {
+    if (!c || !counts) return AXB_ERR_BAD_ARG;
+    if (c->state != S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_compute_host_finish needs axb_compute_host_begin first");
+    const size_t n = (size_t)c->n;
+    int st = alloc_prune_arrays(c);
+    if (st != AXB_OK) return st;
+    int64_t *h[4] = {h_v, h_e, h_t, h_q};
+    int64_t *d_out[4];
+    for (int d = 0; d < 4; ++d) ARENA(c, d_out[d], int64_t, (size_t)std::max<int64_t>(c->host_cap[d], 1) * (d + 1));
+    ARENA(c, c->off1, uint32_t, n + 2);
+    ARENA(c, c->off2, uint32_t, n + 2);
+    ARENA(c, c->off3, uint32_t, n + 2);
+    ARENA(c, c->voff, uint32_t, n + 2);
+    ARENA(c, c->tmp1, int2, (size_t)std::max<int64_t>(c->host_cap[1], 1));
+    ARENA(c, c->tmp2, int4, (size_t)std::max<int64_t>(c->host_cap[2], 1));
+    ARENA(c, c->tmp3, int4, (size_t)std::max<int64_t>(c->host_cap[3], 1));
+    PruneParams P = prune_params(c);
+    CanonParams Q;
+    Q.n = (int)n; Q.orig = c->orig; Q.adj_off = c->adj_off; Q.pe_u = c->pe_u; Q.pe_v = c->pe_v; Q.pe_cap = c->pe_cap;
+    Q.W = c->W; Q.trimask = c->trimask; Q.eflag = c->eflag; Q.k3 = c->k3;
+    Q.cnt1 = c->cnt1; Q.cnt2 = c->cnt2; Q.cnt3 = c->cnt3; Q.off1 = c->off1; Q.off2 = c->off2; Q.off3 = c->off3;
+    Q.tmp1 = c->tmp1; Q.tmp2 = c->tmp2; Q.tmp3 = c->tmp3; Q.ctr = c->ctr;
+    const unsigned grid = (unsigned)c->sm_count * 8u;
+    // Everything is queued up front.  After the scan of a dimension its exact row count goes to the
+    // host (4 bytes + an event); the host then waits for those events one by one and queues the copy
+    // of exactly the valid rows on the second stream, behind the event that marks the rows complete.
+    auto mark_total = [&](int d, const uint32_t *off_end) -> int {
+        CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[d], off_end, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaEventRecord(c->dim_count[d], c->stream));
+        return AXB_OK;
+    };
+    auto mark_ready = [&](int d) -> int {
+        CUDA_TRY(c, cudaEventRecord(c->dim_ready[d], c->stream));
+        return AXB_OK;
+    };
+    // tets
+    k_prune_tets<<<grid, 256, 0, c->stream>>>(P);
+    LAUNCH_CHECK(c);
+    if ((st = mark_event(c, AXB_ST_PRUNE_TETS + 1)) != AXB_OK) return st;
+    if ((st = device_scan(c, c->cnt3, n, c->off3)) != AXB_OK) return st;
+    if ((st = mark_total(3, c->off3 + n)) != AXB_OK) return st;
+    k_scatter_tets<<<grid, 256, 0, c->stream>>>(Q);
+    LAUNCH_CHECK(c);
+    k_emit_tets<<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, 0u, c->off3 + n, c->gidx, d_out[3], c->ctr);
+    LAUNCH_CHECK(c);
+    if ((st = mark_ready(3)) != AXB_OK) return st;
+    // triangles
+    k_prune_tris<<<grid, PRUNE_THREADS, 0, c->stream>>>(P);
+    LAUNCH_CHECK(c);
+    if ((st = mark_event(c, AXB_ST_PRUNE_TRIANGLES + 1)) != AXB_OK) return st;
+    if ((st = device_scan(c, c->cnt2, n, c->off2)) != AXB_OK) return st;
+    if ((st = mark_total(2, c->off2 + n)) != AXB_OK) return st;
+    k_scatter_tris<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[2]);
+    LAUNCH_CHECK(c);
+    k_emit_tris<<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, c->gidx, d_out[2], c->ctr);
+    LAUNCH_CHECK(c);
+    if ((st = mark_ready(2)) != AXB_OK) return st;
+    // edges
+    k_prune_edges<<<grid, PRUNE_THREADS, 0, c->stream>>>(P);
+    LAUNCH_CHECK(c);
+    if ((st = mark_event(c, AXB_ST_PRUNE_EDGES + 1)) != AXB_OK) return st;
+    if ((st = device_scan(c, c->cnt1, n, c->off1)) != AXB_OK) return st;
+    if ((st = mark_total(1, c->off1 + n)) != AXB_OK) return st;
+    k_scatter_edges<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[1]);
+    LAUNCH_CHECK(c);
+    k_emit_edges<<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, c->gidx, d_out[1], c->ctr);
+    LAUNCH_CHECK(c);
+    if ((st = mark_ready(1)) != AXB_OK) return st;
+    // vertices
+    k_prune_vertices<<<blocks_for(n, 256), 256, 0, c->stream>>>(P, c->rank_lo, c->rank_hi);
+    LAUNCH_CHECK(c);
+    if ((st = mark_event(c, AXB_ST_PRUNE_VERTICES + 1)) != AXB_OK) return st;
+    if ((st = device_scan(c, c->vkeep, n, c->voff)) != AXB_OK) return st;
+    if ((st = mark_total(0, c->voff + n)) != AXB_OK) return st;
+    k_emit_vertices<<<blocks_for(n, 256), 256, 0, c->stream>>>((int)n, c->vkeep, c->voff, c->gidx, d_out[0]);
+    LAUNCH_CHECK(c);
+    if ((st = mark_ready(0)) != AXB_OK) return st;
+    // the host follows the GPU dimension by dimension and feeds the copy stream
+    for (int d = 3; d >= 0; --d) {
+        CUDA_TRY(c, cudaEventSynchronize(c->dim_count[d]));
+        c->counts[d] = c->h->totals[d];
+        if (c->counts[d] > c->host_cap[d]) {
+            cudaStreamSynchronize(c->stream);
+            cudaStreamSynchronize(c->copy_stream);
+            return fail(c, AXB_ERR_STATE, "dimension %d has %lld rows, more than the %lld the capacity bound allowed; use axb_compute_host + axb_export_host",
+                        d, (long long)c->counts[d], (long long)c->host_cap[d]);
+        }
+        if (h[d] && c->counts[d]) {
+            CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->dim_ready[d], 0));
+            CUDA_TRY(c, cudaMemcpyAsync(h[d], d_out[d], sizeof(int64_t) * (size_t)c->counts[d] * (d + 1),
+                                        cudaMemcpyDeviceToHost, c->copy_stream));
+        }
+    }
+    if ((st = mark_event(c, AXB_ST_CANONICAL + 1)) != AXB_OK) return st;
+    if ((st = fetch_counters(c)) != AXB_OK) return st;
+    CUDA_TRY(c, cudaStreamSynchronize(c->copy_stream));
+    if ((st = check_run_flags(c)) != AXB_OK) return st;
+    for (int d = 0; d < 4; ++d) counts[d] = c->counts[d];
+    c->state = S_PRUNED;      // the buckets were consumed; axb_export is not available after this path
+    return AXB_OK;
 }
 
 extern "C" int axb_export_host(axb_ctx *c, int64_t *h_v, int64_t *h_e, int64_t *h_t, int64_t *h_q) {

@@ -63,6 +63,45 @@ __global__ void __launch_bounds__(256) k_scatter_edges_tris(CanonParams P) {
     }
 }
 
+// one dimension at a time (the pipelined host path canonicalises a dimension as soon as it is final);
+// `cap` guards the bucket array, whose size was fixed before the exact count was known
+__global__ void __launch_bounds__(256) k_scatter_edges(CanonParams P, unsigned cap) {
+    const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
+    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pe; e += gridDim.x * blockDim.x) {
+        if (!P.eflag[e]) continue;
+        const int ou = __ldg(P.orig + __ldg(P.pe_u + e)), ov = __ldg(P.orig + __ldg(P.pe_v + e));
+        const int a = min(ou, ov), b = max(ou, ov);
+        const unsigned pos = P.off1[a] + atomicSub(P.cnt1 + a, 1u) - 1u;
+        if (pos < cap) P.tmp1[pos] = make_int2(a, b);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_scatter_tris(CanonParams P, unsigned cap) {
+    const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
+    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pe; e += gridDim.x * blockDim.x) {
+        unsigned long long any = 0ull;
+        for (int w = 0; w < P.W; ++w) any |= P.trimask[(size_t)e * P.W + w];
+        if (!any) continue;
+        const int u = __ldg(P.pe_u + e);
+        const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + __ldg(P.pe_v + e));
+        const unsigned bu = __ldg(P.adj_off + u);
+        for (int w = 0; w < P.W; ++w) {
+            unsigned long long m = P.trimask[(size_t)e * P.W + w];
+            while (m) {
+                const int j = 64 * w + __ffsll((long long)m) - 1;
+                m &= m - 1;
+                const int ow = __ldg(P.orig + __ldg(P.pe_v + bu + j));
+                int a = ou, b = ov, c = ow, t;
+                if (a > b) { t = a; a = b; b = t; }
+                if (b > c) { t = b; b = c; c = t; }
+                if (a > b) { t = a; a = b; b = t; }
+                const unsigned pos = P.off2[a] + atomicSub(P.cnt2 + a, 1u) - 1u;
+                if (pos < cap) P.tmp2[pos] = make_int4(a, b, c, 0);
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_scatter_tets(CanonParams P) {
     const unsigned n_k3 = P.ctr->n_k3;
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_k3; e += gridDim.x * blockDim.x) {
@@ -77,11 +116,13 @@ __global__ void __launch_bounds__(256) k_scatter_tets(CanonParams P) {
 // `map` (optional) renames local ball indices to global ones; it is ascending, so order is preserved.
 __device__ __forceinline__ int64_t mapped(const int64_t *__restrict__ map, int v) { return map ? map[v] : (int64_t)v; }
 
+// `total_dev` (optional) = device-side row count (the last entry of the offset array): lets the caller
+// launch without knowing the count on the host.
 __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp, const uint32_t *__restrict__ off,
-                                                    unsigned total, const int64_t *__restrict__ map,
-                                                    int64_t *__restrict__ out, Counters *ctr) {
-    unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= total) return;
+                                                    unsigned total, const uint32_t *__restrict__ total_dev,
+                                                    const int64_t *__restrict__ map, int64_t *__restrict__ out, Counters *ctr) {
+    if (total_dev) total = *total_dev;
+    for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int2 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];
     unsigned pos = lo;
@@ -92,13 +133,14 @@ __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp
     }
     out[2 * (size_t)pos] = mapped(map, me.x);
     out[2 * (size_t)pos + 1] = mapped(map, me.y);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
-                                                   unsigned total, const int64_t *__restrict__ map,
-                                                   int64_t *__restrict__ out, Counters *ctr) {
-    unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= total) return;
+                                                   unsigned total, const uint32_t *__restrict__ total_dev,
+                                                   const int64_t *__restrict__ map, int64_t *__restrict__ out, Counters *ctr) {
+    if (total_dev) total = *total_dev;
+    for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int4 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];
     unsigned pos = lo;
@@ -110,13 +152,14 @@ __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp,
     out[3 * (size_t)pos] = mapped(map, me.x);
     out[3 * (size_t)pos + 1] = mapped(map, me.y);
     out[3 * (size_t)pos + 2] = mapped(map, me.z);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
-                                                   unsigned total, const int64_t *__restrict__ map,
-                                                   int64_t *__restrict__ out, Counters *ctr) {
-    unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= total) return;
+                                                   unsigned total, const uint32_t *__restrict__ total_dev,
+                                                   const int64_t *__restrict__ map, int64_t *__restrict__ out, Counters *ctr) {
+    if (total_dev) total = *total_dev;
+    for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int4 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];
     unsigned pos = lo;
@@ -129,6 +172,7 @@ __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp,
     out[4 * (size_t)pos + 1] = mapped(map, me.y);
     out[4 * (size_t)pos + 2] = mapped(map, me.z);
     out[4 * (size_t)pos + 3] = mapped(map, me.w);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_emit_vertices(int n, const uint32_t *__restrict__ vkeep,

@@ -273,8 +273,15 @@ class Engine:
         return int(self.lib.axb_kernel_launches(self.handle))
 
     # -- the hot path
-    def compute_host(self, centers: np.ndarray, radii: np.ndarray, cfg: PipelineConfig, pinned_out: bool = True):
-        """Host arrays in, four host int64 arrays out (H2D and D2H inside)."""
+    def compute_host(self, centers: np.ndarray, radii: np.ndarray, cfg: PipelineConfig, pinned_out: bool = True,
+                     pipelined: bool = True):
+        """Host arrays in, four host int64 arrays out (H2D and D2H inside).
+
+        ``pipelined``: the result arrays are allocated from tight capacity bounds known after the
+        potential stage (``axb_compute_host_begin``) and every dimension is copied to the host as soon
+        as it is final, overlapping the remaining kernels (``axb_compute_host_finish``); the returned
+        arrays are then leading slices of slightly larger pinned buffers.  Otherwise (or if a bound did
+        not hold) the plain two-call path ``axb_compute_host`` + ``axb_export_host`` is used."""
         torch = self.torch
         centers = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 3)
         radii = np.ascontiguousarray(radii, dtype=np.float64).reshape(-1)
@@ -287,23 +294,39 @@ class Engine:
         counts = (C.c_int64 * 4)()
         outs: list = []
 
-        def run():
-            st = self.lib.axb_compute_host(self.handle, n, centers.ctypes.data, radii.ctypes.data, C.byref(prm), counts)
-            if st != N.OK:
-                return st
+        def host_arrays(rows):
             outs.clear()
             for d in range(4):
-                shape = (int(counts[d]),) if d == 0 else (int(counts[d]), d + 1)
-                if pinned_out and counts[d]:
+                shape = (int(rows[d]),) if d == 0 else (int(rows[d]), d + 1)
+                if pinned_out and rows[d]:
                     outs.append(torch.empty(shape, dtype=torch.int64, pin_memory=True).numpy())
                 else:
                     outs.append(np.empty(shape, dtype=np.int64))
+
+        def run_two_calls():
+            st = self.lib.axb_compute_host(self.handle, n, centers.ctypes.data, radii.ctypes.data, C.byref(prm), counts)
+            if st != N.OK:
+                return st
+            host_arrays(counts)
             # an arena overflow here re-runs the whole computation with a larger arena
             return self.lib.axb_export_host(self.handle, *(o.ctypes.data if o.size else None for o in outs))
 
+        def run_pipelined():
+            cap = (C.c_int64 * 4)()
+            st = self.lib.axb_compute_host_begin(self.handle, n, centers.ctypes.data, radii.ctypes.data, C.byref(prm), cap)
+            if st != N.OK:
+                return st
+            host_arrays(cap)
+            st = self.lib.axb_compute_host_finish(self.handle, *(o.ctypes.data if o.size else None for o in outs), counts)
+            if st == N.OK:
+                outs[:] = [o[: int(counts[d])] for d, o in enumerate(outs)]
+            return st
+
         with torch.cuda.device(self.device):
             self._bind_stream()
-            st = self._with_arena(n, cfg, run)
+            st = self._with_arena(n, cfg, run_pipelined if pipelined else run_two_calls)
+            if st == N.ERR_STATE and pipelined:
+                st = self._with_arena(n, cfg, run_two_calls)
             if st != N.OK:
                 self._raise(st, cfg, centers, radii)
             self._collect_stage_ms()

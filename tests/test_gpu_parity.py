@@ -330,3 +330,18 @@ def test_sparse_grid_mode(monkeypatch):
     dup = np.array([[0, 0, 0], [1e7, 1, 1], [0, 0, 0.0]])
     with pytest.raises(ax.DuplicateCenter, match="balls 0 and 2 share"):
         ax.compute_alpha_complex_arrays(dup, np.array([1, 1, 1.5]), ax.PipelineConfig(alpha=0.0))
+
+
+def test_pipelined_host_path_equals_two_call_path():
+    eng = ax.default_engine()
+    cases = [(synth.jittered_lattice(120_000, 3), 0.0, 1e-300),
+             (synth.jittered_lattice(40_000, 3), 1.4, 1e-300),
+             (synth.random_globule(160, 9, 0.35, (0.4, 1.6), 0.9), 1.0, 1e-300),
+             ((np.array([[0.0, 0, 0], [10, 0, 0]]), np.array([2.0, 0.5])), -1.0, 1e-12),
+             ((np.array([[1.0, 2, 3]]), np.array([1.0])), 0.0, 1e-12)]
+    for (c, r), alpha, eps in cases:
+        cfg = ax.PipelineConfig(alpha=alpha, tolerance=ax.TolerancePolicy(1e-9, eps))
+        a = eng.compute_host(c, r, cfg, pipelined=True)
+        b = eng.compute_host(c, r, cfg, pipelined=False)
+        for x, y in zip(a, b):
+            assert x.dtype == np.int64 and np.array_equal(x, y)
