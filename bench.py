@@ -289,7 +289,10 @@ def bench_b200(args, rank, world, local_rank):
 
         def e2e_step():
             k = ax.compute_alpha_complex_arrays(hc_np, hr_np, cfg, device=local_rank)   # the public API call
-            return sum(a.nbytes for a in (k.vertices, k.edges, k.triangles, k.tets))
+            assert k.edges.dtype == np.int64 and k.tets.shape[1] == 4
+            # bytes that actually crossed PCIe: the rows travel as int32 and host threads widen them to the
+            # reference's int64 while later chunks are in flight (axb_compute_host_finish)
+            return int(eng.lib.axb_last_d2h_bytes(eng.handle))
     else:
         slab = job.slab
         pins = [torch.as_tensor(a).pin_memory() for a in (slab.centers, slab.radii, slab.global_index)] if slab else []

@@ -160,11 +160,16 @@ int axb_compute_host(axb_ctx *ctx, int64_t n, const double *h_xyz, const double 
  * caller allocates them (pinned memory makes the copies asynchronous) and calls `finish`, which
  * canonicalises every dimension as soon as it is final and copies it to the host on a second stream
  * while the remaining kernels run.  counts[d] <= capacity[d] rows of each array are valid.
+ * The host arrays may be pageable: the DMA target is a pinned staging area owned by the context.
  * AXB_ERR_STATE from `finish` means a capacity bound did not hold (then use the two-call path). */
 int axb_compute_host_begin(axb_ctx *ctx, int64_t n, const double *h_xyz, const double *h_radii,
                            const axb_params *params, int64_t capacity[4]);
 int axb_compute_host_finish(axb_ctx *ctx, int64_t *h_vertices, int64_t *h_edges, int64_t *h_triangles,
                             int64_t *h_tets, int64_t counts[4]);
+/* bytes the last axb_compute_host_finish moved device -> host: the rows cross PCIe as int32 (ball
+ * indices < 2^31) and host threads widen them to the int64 rows of the reference while later
+ * chunks are still in flight (AXB_WIDEN_THREADS overrides the thread count) */
+int64_t axb_last_d2h_bytes(const axb_ctx *ctx);
 /* axb_export into HOST buffers (pinned or pageable). */
 int axb_export_host(axb_ctx *ctx, int64_t *h_vertices, int64_t *h_edges, int64_t *h_triangles, int64_t *h_tets);
 

@@ -28,7 +28,7 @@ SYMBOLS = (
     "axb_grid_get_info", "axb_grid_export", "axb_potential",
     "axb_potential_counts", "axb_potential_export", "axb_prune", "axb_canonicalize", "axb_export",
     "axb_sync_check", "axb_compute", "axb_compute_host", "axb_export_host", "axb_compute_host_begin",
-    "axb_compute_host_finish", "axb_stage_ms",
+    "axb_compute_host_finish", "axb_last_d2h_bytes", "axb_stage_ms",
     "axb_kernel_launches", "axb_ortho_batch", "axb_format_complex",
 )
 
@@ -94,6 +94,7 @@ def load() -> C.CDLL:
         "axb_export_host": (C.c_int, [vp, vp, vp, vp, vp]),
         "axb_compute_host_begin": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params), pi64]),
         "axb_compute_host_finish": (C.c_int, [vp, vp, vp, vp, vp, pi64]),
+        "axb_last_d2h_bytes": (i64, [vp]),
         "axb_stage_ms": (C.c_int, [vp, C.POINTER(C.c_float)]),
         "axb_kernel_launches": (i64, [vp]),
         "axb_format_complex": (C.c_int, [pi64, vp, vp, vp, vp, vp, i64, pi64]),

@@ -13,12 +13,14 @@
 #include "prune.cuh"
 #include "scan.cuh"
 #include "sparse.cuh"
+#include "widen_pool.h"
 
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #include <algorithm>
 #include <new>
@@ -51,9 +53,16 @@ struct axb_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;     // D2H of finished dimensions overlaps the remaining kernels
     cudaEvent_t dim_ready[4] = {}, dim_count[4] = {};
+    // host path: rows cross PCIe as int32 into this pinned staging area and are widened by the pool
+    int32_t *h_stage = nullptr;
+    size_t h_stage_elems = 0;
+    axb::WidenPool *pool = nullptr;
+    std::vector<cudaEvent_t> chunk_ev;
+    int64_t last_d2h_bytes = 0;
     char *arena = nullptr;
     size_t arena_bytes = 0, arena_used = 0, arena_needed = 0;
     HostBlock *h = nullptr;
+    HostBlock *h_dev = nullptr;             // device-side address of the same pinned block (zero-copy stores)
     int state = S_NONE;
     int last_status = AXB_OK;
     int64_t err_verts[4] = {-1, -1, -1, -1};
@@ -377,7 +386,7 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
     if (c->W == 1) {
         const size_t smem = sizeof(T2Smem<1>);
         CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_tri_tet2<1><<<std::min(ntiles, (unsigned)c->sm_count * 2u), T2_THREADS, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
+        k_tri_tet2<1><<<std::min(ntiles, (unsigned)c->sm_count * (unsigned)T2_MINB), T2_THREADS, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
     } else {
         const size_t smem = sizeof(T2Smem<4>);
         CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -460,7 +469,8 @@ extern "C" int axb_ctx_create(axb_ctx **out, int device) {
     c->device = device;
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
-    if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void **>(&c->h), sizeof(HostBlock), cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void **>(&c->h), sizeof(HostBlock), cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->h_dev), c->h, 0);
     for (int i = 0; e == cudaSuccess && i < AXB_ST_COUNT + 2; ++i) e = cudaEventCreate(&c->ev[i]);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
     for (int i = 0; e == cudaSuccess && i < 4; ++i) e = cudaEventCreateWithFlags(&c->dim_ready[i], cudaEventDisableTiming);
@@ -483,7 +493,10 @@ extern "C" void axb_ctx_destroy(axb_ctx *c) {
         if (c->dim_ready[i]) cudaEventDestroy(c->dim_ready[i]);
         if (c->dim_count[i]) cudaEventDestroy(c->dim_count[i]);
     }
+    delete c->pool;
+    for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->h) cudaFreeHost(c->h);
     delete c;
 }
@@ -968,19 +981,19 @@ extern "C" int axb_export(axb_ctx *c, int64_t *d_v, int64_t *d_e, int64_t *d_t, 
     int st;
     if ((st = mark_event(c, AXB_ST_COUNT)) != AXB_OK) return st;
     if (d_v) {
-        k_emit_vertices<<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>((int)c->n, c->vkeep, c->voff, c->gidx, d_v);
+        k_emit_vertices<int64_t><<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>((int)c->n, c->vkeep, c->voff, c->gidx, d_v);
         LAUNCH_CHECK(c);
     }
     if (d_e && c->counts[1]) {
-        k_emit_edges<<<blocks_for((size_t)c->counts[1], 256), 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->counts[1], nullptr, c->gidx, d_e, c->ctr);
+        k_emit_edges<int64_t><<<blocks_for((size_t)c->counts[1], 256), 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->counts[1], nullptr, c->gidx, d_e, c->ctr);
         LAUNCH_CHECK(c);
     }
     if (d_t && c->counts[2]) {
-        k_emit_tris<<<blocks_for((size_t)c->counts[2], 256), 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->counts[2], nullptr, c->gidx, d_t, c->ctr);
+        k_emit_tris<int64_t><<<blocks_for((size_t)c->counts[2], 256), 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->counts[2], nullptr, c->gidx, d_t, c->ctr);
         LAUNCH_CHECK(c);
     }
     if (d_q && c->counts[3]) {
-        k_emit_tets<<<blocks_for((size_t)c->counts[3], 256), 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->counts[3], nullptr, c->gidx, d_q, c->ctr);
+        k_emit_tets<int64_t><<<blocks_for((size_t)c->counts[3], 256), 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->counts[3], nullptr, c->gidx, d_q, c->ctr);
         LAUNCH_CHECK(c);
     }
     return mark_event(c, AXB_ST_COUNT + 1);
@@ -1088,6 +1101,25 @@ extern "C" int axb_compute_host_begin(axb_ctx *c, int64_t n, const double *h_xyz
     return AXB_OK;
 }
 
+namespace {
+// A row count goes to the host as a zero-copy store from a one-thread kernel, NOT as a 4-byte
+// cudaMemcpyAsync: that would queue on the same D2H copy engine behind megabytes of row chunks and
+// stall the compute stream until they have drained.
+__global__ void k_publish_total(const uint32_t *__restrict__ src, uint32_t *host_dst) {
+    *host_dst = *src;
+    __threadfence_system();
+}
+
+size_t D2H_CHUNK = (size_t)1 << 19;                // int32 elements per D2H copy (2 MiB; AXB_D2H_CHUNK overrides)
+constexpr size_t WIDEN_PIECE = (size_t)1 << 16;    // int32 elements per widening task
+
+struct PoolRun {                                   // every exit path closes the pool run
+    axb::WidenPool *pool;
+    ~PoolRun() { if (pool) pool->finish(); }
+};
+struct PendingChunk { cudaEvent_t ev; const int32_t *src; int64_t *dst; size_t n; };
+}  // namespace
+
 extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, int64_t *h_t, int64_t *h_q,
                                        int64_t counts[4]) {
     if (!c || !counts) return AXB_ERR_BAD_ARG;
@@ -1096,8 +1128,14 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     int st = alloc_prune_arrays(c);
     if (st != AXB_OK) return st;
     int64_t *h[4] = {h_v, h_e, h_t, h_q};
-    int64_t *d_out[4];
-    for (int d = 0; d < 4; ++d) ARENA(c, d_out[d], int64_t, (size_t)std::max<int64_t>(c->host_cap[d], 1) * (d + 1));
+    int32_t *d_out[4];
+    size_t stage_off[4], stage_elems = 0;
+    for (int d = 0; d < 4; ++d) {
+        const size_t elems = (size_t)std::max<int64_t>(c->host_cap[d], 1) * (d + 1);
+        ARENA(c, d_out[d], int32_t, elems);
+        stage_off[d] = stage_elems;
+        stage_elems += (elems + 63) / 64 * 64;
+    }
     ARENA(c, c->off1, uint32_t, n + 2);
     ARENA(c, c->off2, uint32_t, n + 2);
     ARENA(c, c->off3, uint32_t, n + 2);
@@ -1105,6 +1143,29 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     ARENA(c, c->tmp1, int2, (size_t)std::max<int64_t>(c->host_cap[1], 1));
     ARENA(c, c->tmp2, int4, (size_t)std::max<int64_t>(c->host_cap[2], 1));
     ARENA(c, c->tmp3, int4, (size_t)std::max<int64_t>(c->host_cap[3], 1));
+    // pinned staging area + widening threads (created once, grown on demand)
+    if (c->h_stage_elems < stage_elems) {
+        if (c->h_stage) cudaFreeHost(c->h_stage);
+        c->h_stage = nullptr;
+        c->h_stage_elems = 0;
+        const size_t want = stage_elems + stage_elems / 4;
+        CUDA_TRY(c, cudaHostAlloc(reinterpret_cast<void **>(&c->h_stage), want * sizeof(int32_t), cudaHostAllocDefault));
+        c->h_stage_elems = want;
+    }
+    if (!c->pool) {
+        unsigned hw = std::thread::hardware_concurrency();
+        unsigned workers = std::max(1u, std::min(16u, hw ? hw : 4u)) - 1u;      // the calling thread helps too
+        if (const char *e = getenv("AXB_WIDEN_THREADS")) workers = (unsigned)std::max(0, atoi(e) - 1);
+        c->pool = new (std::nothrow) axb::WidenPool(workers);
+        if (!c->pool) return fail(c, AXB_ERR_INTERNAL, "cannot create the widening threads");
+    }
+    if (const char *e = getenv("AXB_D2H_CHUNK")) D2H_CHUNK = std::max<size_t>(1 << 14, (size_t)atol(e));
+    const size_t max_chunks = stage_elems / D2H_CHUNK + 8;
+    while (c->chunk_ev.size() < max_chunks) {
+        cudaEvent_t e;
+        CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->chunk_ev.push_back(e);
+    }
     PruneParams P = prune_params(c);
     CanonParams Q;
     Q.n = (int)n; Q.orig = c->orig; Q.adj_off = c->adj_off; Q.pe_u = c->pe_u; Q.pe_v = c->pe_v; Q.pe_cap = c->pe_cap;
@@ -1113,10 +1174,12 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     Q.tmp1 = c->tmp1; Q.tmp2 = c->tmp2; Q.tmp3 = c->tmp3; Q.ctr = c->ctr;
     const unsigned grid = (unsigned)c->sm_count * 8u;
     // Everything is queued up front.  After the scan of a dimension its exact row count goes to the
-    // host (4 bytes + an event); the host then waits for those events one by one and queues the copy
-    // of exactly the valid rows on the second stream, behind the event that marks the rows complete.
+    // host (4 bytes + an event); the host follows those events, queues the copies of exactly the valid
+    // rows on the second stream in 2 MiB chunks (behind the event that marks the rows complete) and
+    // hands every chunk that has landed to the widening threads.
     auto mark_total = [&](int d, const uint32_t *off_end) -> int {
-        CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[d], off_end, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        k_publish_total<<<1, 1, 0, c->stream>>>(off_end, &c->h_dev->totals[d]);
+        LAUNCH_CHECK(c);
         CUDA_TRY(c, cudaEventRecord(c->dim_count[d], c->stream));
         return AXB_OK;
     };
@@ -1132,7 +1195,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(3, c->off3 + n)) != AXB_OK) return st;
     k_scatter_tets<<<grid, 256, 0, c->stream>>>(Q);
     LAUNCH_CHECK(c);
-    k_emit_tets<<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, 0u, c->off3 + n, c->gidx, d_out[3], c->ctr);
+    k_emit_tets<int32_t><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, 0u, c->off3 + n, nullptr, d_out[3], c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(3)) != AXB_OK) return st;
     // triangles
@@ -1143,7 +1206,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(2, c->off2 + n)) != AXB_OK) return st;
     k_scatter_tris<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[2]);
     LAUNCH_CHECK(c);
-    k_emit_tris<<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, c->gidx, d_out[2], c->ctr);
+    k_emit_tris<int32_t><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, d_out[2], c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(2)) != AXB_OK) return st;
     // edges
@@ -1154,7 +1217,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(1, c->off1 + n)) != AXB_OK) return st;
     k_scatter_edges<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[1]);
     LAUNCH_CHECK(c);
-    k_emit_edges<<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, c->gidx, d_out[1], c->ctr);
+    k_emit_edges<int32_t><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, d_out[1], c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(1)) != AXB_OK) return st;
     // vertices
@@ -1163,13 +1226,42 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_event(c, AXB_ST_PRUNE_VERTICES + 1)) != AXB_OK) return st;
     if ((st = device_scan(c, c->vkeep, n, c->voff)) != AXB_OK) return st;
     if ((st = mark_total(0, c->voff + n)) != AXB_OK) return st;
-    k_emit_vertices<<<blocks_for(n, 256), 256, 0, c->stream>>>((int)n, c->vkeep, c->voff, c->gidx, d_out[0]);
+    k_emit_vertices<int32_t><<<blocks_for(n, 256), 256, 0, c->stream>>>((int)n, c->vkeep, c->voff, nullptr, d_out[0]);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(0)) != AXB_OK) return st;
-    // the host follows the GPU dimension by dimension and feeds the copy stream
+    if ((st = mark_event(c, AXB_ST_CANONICAL + 1)) != AXB_OK) return st;
+
+    // the host follows the GPU dimension by dimension, feeds the copy stream and the widening threads
+    static const bool trace = getenv("AXB_TRACE") != nullptr;
+    auto now_ms = []() { timespec t; clock_gettime(CLOCK_MONOTONIC, &t); return t.tv_sec * 1e3 + t.tv_nsec * 1e-6; };
+    const double t_q = now_ms();
+    double t_dim[4] = {0, 0, 0, 0};
+    c->pool->begin(stage_elems / WIDEN_PIECE + max_chunks + 8);
+    PoolRun run{c->pool};
+    std::vector<PendingChunk> chunks;
+    chunks.reserve(max_chunks);
+    size_t pumped = 0;
+    c->last_d2h_bytes = 0;
+    auto pump = [&](bool block) -> int {              // publish every chunk that has landed, in order
+        while (pumped < chunks.size()) {
+            const PendingChunk &k = chunks[pumped];
+            cudaError_t e = block ? cudaEventSynchronize(k.ev) : cudaEventQuery(k.ev);
+            if (e == cudaErrorNotReady) return AXB_OK;
+            if (e != cudaSuccess) return fail(c, AXB_ERR_CUDA, "D2H chunk failed: %s", cudaGetErrorString(e));
+            c->pool->publish(k.src, k.dst, k.n, WIDEN_PIECE);
+            ++pumped;
+        }
+        return AXB_OK;
+    };
     for (int d = 3; d >= 0; --d) {
-        CUDA_TRY(c, cudaEventSynchronize(c->dim_count[d]));
+        for (;;) {
+            cudaError_t e = cudaEventQuery(c->dim_count[d]);
+            if (e == cudaSuccess) break;
+            if (e != cudaErrorNotReady) return fail(c, AXB_ERR_CUDA, "row count of dimension %d: %s", d, cudaGetErrorString(e));
+            if ((st = pump(false)) != AXB_OK) return st;
+        }
         c->counts[d] = c->h->totals[d];
+        t_dim[d] = now_ms();
         if (c->counts[d] > c->host_cap[d]) {
             cudaStreamSynchronize(c->stream);
             cudaStreamSynchronize(c->copy_stream);
@@ -1177,12 +1269,27 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
                         d, (long long)c->counts[d], (long long)c->host_cap[d]);
         }
         if (h[d] && c->counts[d]) {
+            const size_t elems = (size_t)c->counts[d] * (d + 1);
+            int32_t *stage = c->h_stage + stage_off[d];
             CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->dim_ready[d], 0));
-            CUDA_TRY(c, cudaMemcpyAsync(h[d], d_out[d], sizeof(int64_t) * (size_t)c->counts[d] * (d + 1),
-                                        cudaMemcpyDeviceToHost, c->copy_stream));
+            for (size_t lo = 0; lo < elems; lo += D2H_CHUNK) {
+                const size_t m = std::min(D2H_CHUNK, elems - lo);
+                if (chunks.size() >= c->chunk_ev.size()) return fail(c, AXB_ERR_INTERNAL, "chunk event pool exhausted");
+                cudaEvent_t ev = c->chunk_ev[chunks.size()];
+                CUDA_TRY(c, cudaMemcpyAsync(stage + lo, d_out[d] + lo, m * sizeof(int32_t), cudaMemcpyDeviceToHost, c->copy_stream));
+                CUDA_TRY(c, cudaEventRecord(ev, c->copy_stream));
+                chunks.push_back(PendingChunk{ev, stage + lo, h[d] + lo, m});
+            }
+            c->last_d2h_bytes += (int64_t)(elems * sizeof(int32_t));
         }
     }
-    if ((st = mark_event(c, AXB_ST_CANONICAL + 1)) != AXB_OK) return st;
+    if ((st = pump(true)) != AXB_OK) return st;
+    const double t_landed = now_ms();
+    run.pool = nullptr;
+    c->pool->finish();
+    if (trace)
+        fprintf(stderr, "[axb] finish: counts known at +%.3f %.3f %.3f %.3f ms (tets..vertices), last chunk landed +%.3f, widened +%.3f (%zu chunks)\n",
+                t_dim[3] - t_q, t_dim[2] - t_q, t_dim[1] - t_q, t_dim[0] - t_q, t_landed - t_q, now_ms() - t_q, chunks.size());
     if ((st = fetch_counters(c)) != AXB_OK) return st;
     CUDA_TRY(c, cudaStreamSynchronize(c->copy_stream));
     if ((st = check_run_flags(c)) != AXB_OK) return st;
@@ -1190,6 +1297,8 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     c->state = S_PRUNED;      // the buckets were consumed; axb_export is not available after this path
     return AXB_OK;
 }
+
+extern "C" int64_t axb_last_d2h_bytes(const axb_ctx *c) { return c ? c->last_d2h_bytes : 0; }
 
 extern "C" int axb_export_host(axb_ctx *c, int64_t *h_v, int64_t *h_e, int64_t *h_t, int64_t *h_q) {
     if (!c) return AXB_ERR_BAD_ARG;

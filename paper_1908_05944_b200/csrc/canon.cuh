@@ -116,11 +116,14 @@ __global__ void __launch_bounds__(256) k_scatter_tets(CanonParams P) {
 // `map` (optional) renames local ball indices to global ones; it is ascending, so order is preserved.
 __device__ __forceinline__ int64_t mapped(const int64_t *__restrict__ map, int v) { return map ? map[v] : (int64_t)v; }
 
+// OutT = int64_t (the reference dtype, device-resident results) or int32_t (the host path: half the
+// PCIe bytes, widened to int64 by host threads while the next chunk is in flight).
 // `total_dev` (optional) = device-side row count (the last entry of the offset array): lets the caller
 // launch without knowing the count on the host.
+template <class OutT>
 __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                     unsigned total, const uint32_t *__restrict__ total_dev,
-                                                    const int64_t *__restrict__ map, int64_t *__restrict__ out, Counters *ctr) {
+                                                    const int64_t *__restrict__ map, OutT *__restrict__ out, Counters *ctr) {
     if (total_dev) total = *total_dev;
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int2 me = tmp[s];
@@ -131,14 +134,15 @@ __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp
         if (b < me.y) ++pos;
         else if (b == me.y && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
-    out[2 * (size_t)pos] = mapped(map, me.x);
-    out[2 * (size_t)pos + 1] = mapped(map, me.y);
+    out[2 * (size_t)pos] = (OutT)mapped(map, me.x);
+    out[2 * (size_t)pos + 1] = (OutT)mapped(map, me.y);
     }
 }
 
+template <class OutT>
 __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                    unsigned total, const uint32_t *__restrict__ total_dev,
-                                                   const int64_t *__restrict__ map, int64_t *__restrict__ out, Counters *ctr) {
+                                                   const int64_t *__restrict__ map, OutT *__restrict__ out, Counters *ctr) {
     if (total_dev) total = *total_dev;
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int4 me = tmp[s];
@@ -149,15 +153,16 @@ __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp,
         if (o.y < me.y || (o.y == me.y && o.z < me.z)) ++pos;
         else if (o.y == me.y && o.z == me.z && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
-    out[3 * (size_t)pos] = mapped(map, me.x);
-    out[3 * (size_t)pos + 1] = mapped(map, me.y);
-    out[3 * (size_t)pos + 2] = mapped(map, me.z);
+    out[3 * (size_t)pos] = (OutT)mapped(map, me.x);
+    out[3 * (size_t)pos + 1] = (OutT)mapped(map, me.y);
+    out[3 * (size_t)pos + 2] = (OutT)mapped(map, me.z);
     }
 }
 
+template <class OutT>
 __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                    unsigned total, const uint32_t *__restrict__ total_dev,
-                                                   const int64_t *__restrict__ map, int64_t *__restrict__ out, Counters *ctr) {
+                                                   const int64_t *__restrict__ map, OutT *__restrict__ out, Counters *ctr) {
     if (total_dev) total = *total_dev;
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int4 me = tmp[s];
@@ -168,19 +173,20 @@ __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp,
         if (o.y < me.y || (o.y == me.y && (o.z < me.z || (o.z == me.z && o.w < me.w)))) ++pos;
         else if (o.y == me.y && o.z == me.z && o.w == me.w && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
-    out[4 * (size_t)pos] = mapped(map, me.x);
-    out[4 * (size_t)pos + 1] = mapped(map, me.y);
-    out[4 * (size_t)pos + 2] = mapped(map, me.z);
-    out[4 * (size_t)pos + 3] = mapped(map, me.w);
+    out[4 * (size_t)pos] = (OutT)mapped(map, me.x);
+    out[4 * (size_t)pos + 1] = (OutT)mapped(map, me.y);
+    out[4 * (size_t)pos + 2] = (OutT)mapped(map, me.z);
+    out[4 * (size_t)pos + 3] = (OutT)mapped(map, me.w);
     }
 }
 
+template <class OutT>
 __global__ void __launch_bounds__(256) k_emit_vertices(int n, const uint32_t *__restrict__ vkeep,
                                                        const uint32_t *__restrict__ voff,
-                                                       const int64_t *__restrict__ map, int64_t *__restrict__ out) {
+                                                       const int64_t *__restrict__ map, OutT *__restrict__ out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    if (vkeep[i]) out[voff[i]] = mapped(map, i);
+    if (vkeep[i]) out[voff[i]] = (OutT)mapped(map, i);
 }
 
 // ---- merge of canonical row lists from several slabs / chunks (reference pipeline.py:611-614):

@@ -23,12 +23,23 @@
 
 namespace axb {
 
-constexpr int T2_THREADS = 256;
+#ifndef T2_THREADS_V
+#define T2_THREADS_V 128
+#endif
+#ifndef T2_GENS_V
+#define T2_GENS_V 64
+#endif
+#ifndef T2_MINB
+#define T2_MINB 4
+#endif
+constexpr int T2_THREADS = T2_THREADS_V;
 constexpr int T2_WARPS = T2_THREADS / 32;
-constexpr int T2_GENS = 128;       // generators per tile
-constexpr int T2_SCAP = 1024;      // partner slots per sub-pass (>= 64 * W so one generator always fits)
-constexpr int T2_TCAP = 3072;      // triangles per round
-constexpr int T2_WQCAP = 768;      // reach-passing pairs queued per warp
+constexpr int T2_GENS = T2_GENS_V;       // generators per tile (multiple of 32)
+constexpr int T2_GPL = T2_GENS / 32;     // generators per lane in the tile prefix
+constexpr int T2_SCAP = 8 * T2_GENS;     // partner slots per sub-pass (>= 64 * W so one generator always fits)
+constexpr int T2_TCAP = 24 * T2_GENS;    // triangles per round
+constexpr int T2_WQCAP = 288;            // reach-passing pairs queued per warp (solved as soon as 256 are waiting)
+static_assert(T2_GENS % 32 == 0 && T2_GENS <= T2_THREADS && T2_SCAP >= 256, "tile shape");
 
 template <int W>
 struct T2Smem {
@@ -126,7 +137,7 @@ __device__ __forceinline__ bool dominated_by_partner(const T2Smem<W> &S, int g, 
 }
 
 template <int W>
-__global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int rank_lo, int rank_hi) {
+__global__ void __launch_bounds__(T2_THREADS, T2_MINB) k_tri_tet2(EstParams P, int rank_lo, int rank_hi) {
     constexpr int PCAP = 64 * W;
     extern __shared__ __align__(16) unsigned char s_raw2[];
     T2Smem<W> &S = *reinterpret_cast<T2Smem<W> *>(s_raw2);
@@ -150,16 +161,16 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_tri_tet2(EstParams P, int ran
             S.gdeg[tid] = d;
         }
         __syncthreads();
-        // slot / pair prefixes of the whole window (warp 0, four generators per lane)
+        // slot / pair prefixes of the whole window (warp 0, T2_GPL generators per lane)
         if (tid < 32) {
-            int d[4], ls = 0, lp = 0;
+            int d[T2_GPL], ls = 0, lp = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) { d[k] = S.gdeg[4 * tid + k]; ls += d[k]; lp += d[k] * (d[k] - 1) / 2; }
+            for (int k = 0; k < T2_GPL; ++k) { d[k] = S.gdeg[T2_GPL * tid + k]; ls += d[k]; lp += d[k] * (d[k] - 1) / 2; }
             const int is = warp_incl_scan(ls), ip = warp_incl_scan(lp);
             int es = is - ls, ep = ip - lp;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                S.sp[4 * tid + k] = es; S.pp[4 * tid + k] = ep;
+            for (int k = 0; k < T2_GPL; ++k) {
+                S.sp[T2_GPL * tid + k] = es; S.pp[T2_GPL * tid + k] = ep;
                 es += d[k]; ep += d[k] * (d[k] - 1) / 2;
             }
             if (tid == 31) { S.sp[T2_GENS] = es; S.pp[T2_GENS] = ep; S.fits = es <= T2_SCAP; }

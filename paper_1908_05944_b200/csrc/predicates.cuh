@@ -266,12 +266,96 @@ __device__ __forceinline__ bool ac2_pass(const GridView &g, const Atom *__restri
     return true;
 }
 
+// one 256-bit load per atom record (sm_100: LDG.E.256), read-only path
 __device__ __forceinline__ Atom load_atom(const Atom *__restrict__ atoms, int t) {
-    const double2 *q = reinterpret_cast<const double2 *>(atoms + t);
-    double2 xy = __ldg(q), zr = __ldg(q + 1);
     Atom a;
-    a.x = xy.x; a.y = xy.y; a.z = zr.x; a.r2 = zr.y;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a.x), "=d"(a.y), "=d"(a.z), "=d"(a.r2) : "l"(atoms + t));
     return a;
+}
+
+// ac2_pass with memory-level parallelism (dense cell table only).  The plain version above is a chain
+// of dependent round trips: row bounds -> balls of the row -> next row ...  Here (1) the bounds of all
+// nine rows of the 3x3x3 block are fetched back to back (straight-line code, clamped indices, so the 18
+// loads are in flight together) and parked in a per-thread column of shared memory, (2) the balls of
+// all rows are walked as ONE flattened sequence with AC2_DEPTH loads in flight ahead of the ball being
+// tested.  Same boolean as ac2_pass (same cells, same arithmetic, pipeline.py:286-313).
+#ifndef AC2_DEPTH
+#define AC2_DEPTH 2
+#endif
+__device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__restrict__ atoms, double cx, double cy,
+                                             double cz, double thr, double r2max, int inc0, int inc1, int inc2, int inc3,
+                                             int2 *rows, int stride) {
+    double R2 = r2max + thr;
+    if (!(R2 > 0.0)) return true;
+    R2 = R2 * (1.0 + 1e-9) + 1e-9;
+    const int ix = cell_coord(cx, g.ox, g.side, g.dx);
+    const int iy = cell_coord(cy, g.oy, g.side, g.dy);
+    const int iz = cell_coord_z(cz, g);
+    const double xa = g.ox + (double)ix * g.side, ya = g.oy + (double)iy * g.side;
+    const double za = g.oz + (double)(iz + g.z_lo) * g.side;
+    const double dxl = fmax(cx - xa, 0.0), dxh = fmax(xa + g.side - cx, 0.0);
+    const double dyl = fmax(cy - ya, 0.0), dyh = fmax(ya + g.side - cy, 0.0);
+    const double dzl = fmax(cz - za, 0.0), dzh = fmax(za + g.side - cz, 0.0);
+    const double ox2 = fmax(fmax(xa - cx, cx - (xa + g.side)), 0.0);
+    const double oy2 = fmax(fmax(ya - cy, cy - (ya + g.side)), 0.0);
+    const double oz2 = fmax(fmax(za - cz, cz - (za + g.side)), 0.0);
+    const double dxl2 = dxl * dxl, dxh2 = dxh * dxh, ox22 = ox2 * ox2;
+    int sr[9], er[9];
+#pragma unroll
+    for (int oz = -1; oz <= 1; ++oz) {
+        const int z = iz + oz;
+        const double gz = oz < 0 ? dzl : (oz > 0 ? dzh : oz2);
+        const double rem_z = R2 - gz * gz;
+        const bool zok = z >= 0 && z < g.dz && rem_z >= 0.0;
+#pragma unroll
+        for (int oy = -1; oy <= 1; ++oy) {
+            const int k = (oz + 1) * 3 + (oy + 1);
+            const int y = iy + oy;
+            const double gy = oy < 0 ? dyl : (oy > 0 ? dyh : oy2);
+            const double rem = rem_z - gy * gy;
+            bool ok = zok && y >= 0 && y < g.dy && rem >= 0.0;
+            int x0 = ix, x1 = ix;
+            if (ix > 0 && dxl2 <= rem) x0 = ix - 1;
+            if (ix < g.dx - 1 && dxh2 <= rem) x1 = ix + 1;
+            if (ox22 > rem && x0 == ix && x1 == ix) ok = false;
+            const int row = ok ? g.dx * (y + g.dy * z) : 0;
+            const int a = ok ? row + x0 : 0, b = ok ? row + x1 + 1 : 0;
+            sr[k] = (int)__ldg(g.cell_start + a);
+            er[k] = (int)__ldg(g.cell_start + b);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) rows[k * stride] = make_int2(sr[k], er[k]);
+    // flattened walk over the balls of all rows
+    int r = -1, pos = 0, end = 0;
+    auto next = [&]() -> int {
+        while (pos >= end) {
+            if (++r >= 9) { r = 9; return -1; }
+            const int2 q = rows[r * stride];
+            pos = q.x; end = q.y;
+        }
+        return pos++;
+    };
+    int tq[AC2_DEPTH];
+    Atom aq[AC2_DEPTH];
+#pragma unroll
+    for (int d = 0; d < AC2_DEPTH; ++d) {
+        tq[d] = next();
+        if (tq[d] >= 0) aq[d] = load_atom(atoms, tq[d]);
+    }
+    while (tq[0] >= 0) {
+        const int t = tq[0];
+        const Atom a = aq[0];
+#pragma unroll
+        for (int d = 0; d + 1 < AC2_DEPTH; ++d) { tq[d] = tq[d + 1]; aq[d] = aq[d + 1]; }
+        tq[AC2_DEPTH - 1] = next();
+        if (tq[AC2_DEPTH - 1] >= 0) aq[AC2_DEPTH - 1] = load_atom(atoms, tq[AC2_DEPTH - 1]);
+        if (t == inc0 || t == inc1 || t == inc2 || t == inc3) continue;
+        const double ddx = a.x - cx, ddy = a.y - cy, ddz = a.z - cz;
+        const double dp = ((ddx * ddx + ddy * ddy) + ddz * ddz) - a.r2;
+        if (dp < thr) return false;
+    }
+    return true;
 }
 #endif
 

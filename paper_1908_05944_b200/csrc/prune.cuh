@@ -85,6 +85,19 @@ __device__ __forceinline__ void note_miss(const PruneParams &P) {
 
 __device__ __forceinline__ int min3(int a, int b, int c) { return min(a, min(b, c)); }
 
+// AC2 of one simplex: the latency-tolerant walk when the dense cell table exists (rows = this thread's
+// column of a [9][blockDim.x] shared table), the plain one for the sorted sparse grid
+#ifndef AXB_AC2_MLP
+#define AXB_AC2_MLP 1
+#endif
+__device__ __forceinline__ bool ac2_check(const PruneParams &P, double cx, double cy, double cz, double thr, int inc0,
+                                          int inc1, int inc2, int inc3, int2 *rows, int stride) {
+#if AXB_AC2_MLP
+    if (P.g.cell_start) return ac2_pass_mlp(P.g, P.atoms, cx, cy, cz, thr, P.tol.r2max, inc0, inc1, inc2, inc3, rows, stride);
+#endif
+    return ac2_pass(P.g, P.atoms, cx, cy, cz, thr, P.tol.r2max, inc0, inc1, inc2, inc3);
+}
+
 // pipeline.py:496-497 (K3 = tets[AC2]) + inheritance of faces (pipeline.py:501, 509)
 // NB: when a potential list overflowed its buffer (optimistic sizing in axb_compute) the tail of the
 // buffer is garbage; every prune kernel then does nothing and the host re-runs with exact sizes.
@@ -92,7 +105,11 @@ __device__ __forceinline__ bool lists_overflowed(const PruneParams &P) {
     return P.ctr->n_pq > P.pq_cap || P.ctr->n_pt > P.pt_cap || P.ctr->n_pe > P.pe_cap;
 }
 
-__global__ void __launch_bounds__(256) k_prune_tets(PruneParams P) {
+#ifndef TETS_MINB
+#define TETS_MINB 3
+#endif
+__global__ void __launch_bounds__(256, TETS_MINB) k_prune_tets(PruneParams P) {
+    __shared__ int2 s_rows[9][256];
     if (lists_overflowed(P)) return;
     const unsigned n_pq = min(P.ctr->n_pq, P.pq_cap);
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pq; e += gridDim.x * blockDim.x) {
@@ -103,7 +120,7 @@ __global__ void __launch_bounds__(256) k_prune_tets(PruneParams P) {
         const Atom aw = load_atom(P.atoms, r.z), ax = load_atom(P.atoms, r.w);
         const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z), ox = __ldg(P.orig + r.w);
         const Ortho o = ortho_tet(ou, au, ov, av, ow, aw, ox, ax, P.tol.eps_sing);
-        if (!ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, P.tol.r2max, r.x, r.y, r.z, r.w)) continue;
+        if (!ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, r.w, &s_rows[0][threadIdx.x], 256)) continue;
         int row[4] = {ou, ov, ow, ox};
 #pragma unroll
         for (int a = 1; a < 4; ++a)
@@ -155,6 +172,9 @@ __global__ void __launch_bounds__(256) k_prune_tets(PruneParams P) {
 // already kept by inheritance, so a block first scans PRUNE_BATCH x 256 entries, queues the free
 // ones in shared memory and then runs the expensive part (ortho solve + AC2) with packed lanes.
 constexpr int PRUNE_THREADS = 256;
+#ifndef PRUNE_MINB
+#define PRUNE_MINB 4      // <= 64 registers: measured best (occupancy beats the few spilled values)
+#endif
 constexpr int PRUNE_BATCH = 4;
 
 __device__ __forceinline__ void queue_push(bool want, unsigned value, unsigned *queue, int *qn) {
@@ -169,8 +189,9 @@ __device__ __forceinline__ void queue_push(bool want, unsigned value, unsigned *
 }
 
 // pipeline.py:502-505: AC2 for the triangles no kept tet inherited
-__global__ void __launch_bounds__(PRUNE_THREADS) k_prune_tris(PruneParams P) {
+__global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_tris(PruneParams P) {
     __shared__ unsigned queue[PRUNE_THREADS * PRUNE_BATCH];
+    __shared__ int2 s_rows[9][PRUNE_THREADS];
     __shared__ int qn;
     if (lists_overflowed(P)) return;
     const unsigned n_pt = min(P.ctr->n_pt, P.pt_cap);
@@ -202,7 +223,7 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_tris(PruneParams P) {
             const Atom au = load_atom(P.atoms, r.x), av = load_atom(P.atoms, r.y), aw = load_atom(P.atoms, r.z);
             const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z);
             const Ortho o = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);
-            if (!ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, P.tol.r2max, r.x, r.y, r.z, -1)) continue;
+            if (!ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, -1, &s_rows[0][threadIdx.x], PRUNE_THREADS)) continue;
             mark_tri(P, bu + i, j, min3(ou, ov, ow));
             mark_edge(P, bu + i, min(ou, ov));
             mark_edge(P, bu + j, min(ou, ow));
@@ -215,8 +236,9 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_tris(PruneParams P) {
 }
 
 // pipeline.py:510-513: AC2 for the edges nothing inherited; kept edges mark their endpoints
-__global__ void __launch_bounds__(PRUNE_THREADS) k_prune_edges(PruneParams P) {
+__global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_edges(PruneParams P) {
     __shared__ unsigned queue[PRUNE_THREADS * PRUNE_BATCH];
+    __shared__ int2 s_rows[9][PRUNE_THREADS];
     __shared__ int qn;
     if (lists_overflowed(P)) return;
     const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
@@ -247,7 +269,7 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_edges(PruneParams P) {
             const Atom au = load_atom(P.atoms, u), av = load_atom(P.atoms, v);
             const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + v);
             const Ortho o = ortho_edge(ou, au, ov, av, P.tol.eps_sing);
-            if (ac2_pass(P.g, P.atoms, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, P.tol.r2max, u, v, -1, -1)) {
+            if (ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, u, v, -1, -1, &s_rows[0][threadIdx.x], PRUNE_THREADS)) {
                 mark_edge(P, e, min(ou, ov));
                 P.vflag[u] = 1;
                 P.vflag[v] = 1;
