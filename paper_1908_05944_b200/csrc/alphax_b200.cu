@@ -90,6 +90,7 @@ struct axb_ctx {
     int4 *cell_of_rank = nullptr;
     uint32_t *cell_start = nullptr;
     Atom *atoms = nullptr;
+    Atom *xyzr = nullptr;                   // (x, y, z, reach) per rank: the edge stage's candidate record
     double *reach = nullptr;
     uint32_t *adj_off = nullptr;
     int *deg = nullptr, *pe_u = nullptr, *pe_v = nullptr;
@@ -218,6 +219,7 @@ int bin_balls_sparse(axb_ctx *c, double side, const double lo[3], const int64_t 
     ARENA(c, c->cell_of_rank, int4, n);
     ARENA(c, c->atoms, Atom, n);
     ARENA(c, c->reach, double, n);
+    ARENA(c, c->xyzr, Atom, n);
     const size_t mark = c->arena_used;
     long long *kbuf;
     int *vbuf[2];
@@ -249,7 +251,7 @@ int bin_balls_sparse(axb_ctx *c, double side, const double lo[3], const int64_t 
         CUDA_TRY(c, cudaMemcpyAsync(c->skeys, kin, sizeof(long long) * (size_t)n, cudaMemcpyDeviceToDevice, c->stream));
     k_sparse_finalize<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->d_xyz, c->d_radii, c->skeys, vbuf[cur], g, c->prm.alpha,
                                                                c->prm.eps_abs, c->orig, c->rank, c->cell_of_rank, c->atoms,
-                                                               c->reach, c->ctr, c->dups);
+                                                               c->reach, c->xyzr, c->ctr, c->dups);
     LAUNCH_CHECK(c);
     c->arena_used = mark;
     return AXB_OK;
@@ -295,6 +297,7 @@ int bin_balls(axb_ctx *c, double side, const double lo[3], const int64_t dims[3]
     ARENA(c, c->cell_of_rank, int4, n);
     ARENA(c, c->atoms, Atom, n);
     ARENA(c, c->reach, double, n);
+    ARENA(c, c->xyzr, Atom, n);
     const size_t mark = c->arena_used;          // everything below is scratch of this function
     ARENA(c, cell_count, uint32_t, (size_t)G + 2);
     ARENA(c, arrival, int, n);
@@ -311,7 +314,7 @@ int bin_balls(axb_ctx *c, double side, const double lo[3], const int64_t dims[3]
     LAUNCH_CHECK(c);
     k_cell_finalize<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->d_xyz, c->d_radii, c->key_of_ball, c->cell_start,
                                                              arrival, c->prm.alpha, c->prm.eps_abs, c->orig, c->rank,
-                                                             c->cell_of_rank, g.dx, g.dy, c->atoms, c->reach, c->ctr, c->dups);
+                                                             c->cell_of_rank, g.dx, g.dy, c->atoms, c->reach, c->xyzr, c->ctr, c->dups);
     LAUNCH_CHECK(c);
     // the scratch is dead once the stream has passed k_cell_finalize; later stages
     // are ordered on the same stream, so it can be handed out again
@@ -350,7 +353,7 @@ int report_duplicate(axb_ctx *c, unsigned ndup) {
 EstParams est_params(axb_ctx *c, unsigned long long report_key) {
     EstParams P;
     P.g = c->g; P.tol = c->tol;
-    P.atoms = c->atoms; P.reach = c->reach; P.orig = c->orig; P.cell_of_rank = c->cell_of_rank;
+    P.atoms = c->atoms; P.xyzr = c->xyzr; P.reach = c->reach; P.orig = c->orig; P.cell_of_rank = c->cell_of_rank;
     P.adj_off = c->adj_off; P.deg = c->deg; P.pe_v = c->pe_v; P.pe_u = c->pe_u; P.pe_cap = c->pe_cap;
     P.pt = c->pt; P.pt_cap = c->pt_cap; P.pq_r = c->pq_r; P.pq_l = c->pq_l; P.pq_cap = c->pq_cap;
     P.ctr = c->ctr; P.errs = c->errs; P.report_key = report_key;
@@ -373,8 +376,10 @@ PruneParams prune_params(axb_ctx *c) {
 }
 
 int launch_edges(axb_ctx *c, const EstParams &P, int lo, int hi) {
-    const unsigned ntiles = (unsigned)std::max(1, (hi - lo + EST_TILE - 1) / EST_TILE);
-    k_edges<<<std::min(ntiles, (unsigned)c->sm_count * 4u), EST_WARPS * 32, 0, c->stream>>>(P, lo, hi);
+    const unsigned nblocks = (unsigned)std::max(1, (hi - lo + E2_GB * EST_WARPS - 1) / (E2_GB * EST_WARPS));
+    const size_t smem = sizeof(E2Warp) * EST_WARPS;
+    CUDA_TRY(c, cudaFuncSetAttribute(k_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_edges<<<std::min(nblocks, (unsigned)c->sm_count * (unsigned)E2_MINB), EST_WARPS * 32, smem, c->stream>>>(P, lo, hi);
     LAUNCH_CHECK(c);
     return AXB_OK;
 }

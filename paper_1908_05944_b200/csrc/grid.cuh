@@ -144,6 +144,7 @@ __global__ void k_cell_finalize(int n, const double *__restrict__ xyz, const dou
                                 const int *__restrict__ arrival, double alpha, double eps_abs,
                                 int *__restrict__ orig_of_rank, int *__restrict__ rank_of_orig,
                                 int4 *__restrict__ cell_of_rank, int dimx, int dimy, Atom *__restrict__ atoms, double *__restrict__ reach,
+                                Atom *__restrict__ xyzr,
                                 Counters *__restrict__ ctr, int2 *__restrict__ dup_records) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
@@ -171,7 +172,10 @@ __global__ void k_cell_finalize(int n, const double *__restrict__ xyz, const dou
     Atom a;
     a.x = x; a.y = y; a.z = z; a.r2 = r2;
     atoms[pos] = a;
-    reach[pos] = (lim >= 0.0) ? sqrt(fmax(lim, 0.0)) : -1.0;   // pipeline.py:323-324
+    const double rch = (lim >= 0.0) ? sqrt(fmax(lim, 0.0)) : -1.0;   // pipeline.py:323-324
+    reach[pos] = rch;
+    a.r2 = rch;                                            // (x, y, z, reach): one 32-byte load per edge candidate
+    xyzr[pos] = a;
     orig_of_rank[pos] = i;
     rank_of_orig[i] = pos;
     const int rest = key / dimx;                           // (cx, cy, cz, key): k_edges wants the coordinates

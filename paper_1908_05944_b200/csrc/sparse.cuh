@@ -86,8 +86,8 @@ __global__ void k_sparse_finalize(int n, const double *__restrict__ xyz, const d
                                   const long long *__restrict__ skeys, const int *__restrict__ order, GridView g,
                                   double alpha, double eps_abs, int *__restrict__ orig_of_rank,
                                   int *__restrict__ rank_of_orig, int4 *__restrict__ cell_of_rank,
-                                  Atom *__restrict__ atoms, double *__restrict__ reach, Counters *__restrict__ ctr,
-                                  int2 *__restrict__ dup_records) {
+                                  Atom *__restrict__ atoms, double *__restrict__ reach, Atom *__restrict__ xyzr,
+                                  Counters *__restrict__ ctr, int2 *__restrict__ dup_records) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     const int i = order[t];
@@ -107,7 +107,10 @@ __global__ void k_sparse_finalize(int n, const double *__restrict__ xyz, const d
     Atom a;
     a.x = x; a.y = y; a.z = z; a.r2 = r2;
     atoms[t] = a;
-    reach[t] = (lim >= 0.0) ? sqrt(fmax(lim, 0.0)) : -1.0;
+    const double rch = (lim >= 0.0) ? sqrt(fmax(lim, 0.0)) : -1.0;
+    reach[t] = rch;
+    a.r2 = rch;
+    xyzr[t] = a;
     orig_of_rank[t] = i;
     rank_of_orig[i] = t;
     const long long rest = key / g.dx;

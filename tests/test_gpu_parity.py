@@ -205,6 +205,20 @@ def test_adversarial_density_against_oracle():
     assert_same_complex(k, ref, "adversarial")
 
 
+def test_dense_blob_crowded_edge_batches_against_oracle():
+    """~60 potential-edge partners per ball: a warp batch of 8 generators overflows its pair queue, so
+    k_edges has to halve batches (and k_tri_tet2 runs its wide W=4 variant)."""
+    rng = np.random.default_rng(11)
+    c = rng.uniform(0.0, 11.0, size=(500, 3))
+    r = rng.uniform(1.2, 1.9, size=500)
+    tol = ax.TolerancePolicy(1e-9, 1e-300)
+    for alpha in (1.0, 0.0):
+        k = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=alpha, tolerance=tol))
+        ref = oracle.compute(c, r, alpha, eps_singular=1e-300, threads=os.cpu_count(), chunk=16)
+        assert ref.status == oracle.OK
+        assert_same_complex(k, ref, f"dense blob alpha={alpha}")
+
+
 def test_device_path_equals_host_path_and_is_deterministic():
     import torch
 
