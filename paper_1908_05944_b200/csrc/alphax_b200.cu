@@ -8,6 +8,7 @@
 #include "common.cuh"
 #include "estimate.cuh"
 #include "estimate2.cuh"
+#include "estimate3.cuh"
 #include "grid.cuh"
 #include "predicates.cuh"
 #include "prune.cuh"
@@ -387,6 +388,26 @@ int launch_edges(axb_ctx *c, const EstParams &P, int lo, int hi) {
 int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
     EstParams P = est_params(c, report_key);
     const int ngen = c->rank_hi - c->rank_lo;
+#ifndef AXB_T3
+#define AXB_T3 1
+#endif
+#if AXB_T3
+    {   // warp-autonomous tiles (estimate3.cuh)
+        CUDA_TRY(c, cudaMemsetAsync(&c->ctr->tile_next, 0, sizeof(unsigned int), c->stream));
+        const unsigned nblocks = (unsigned)std::max(1, (ngen + T3_GENS * T3_WARPS - 1) / (T3_GENS * T3_WARPS));
+        if (c->W == 1) {
+            const size_t smem = sizeof(T3Warp<1>) * T3_WARPS;
+            CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_tri_tet3<1><<<std::min(nblocks, (unsigned)c->sm_count * (unsigned)T3_MINB), T3_WARPS * 32, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
+        } else {
+            const size_t smem = sizeof(T3Warp<4>) * T3_WARPS;
+            CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet3<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_tri_tet3<4><<<std::min(nblocks, (unsigned)c->sm_count * 2u), T3_WARPS * 32, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
+        }
+        LAUNCH_CHECK(c);
+        return AXB_OK;
+    }
+#endif
     const unsigned ntiles = (unsigned)std::max(1, (ngen + T2_GENS - 1) / T2_GENS);
     if (c->W == 1) {
         const size_t smem = sizeof(T2Smem<1>);

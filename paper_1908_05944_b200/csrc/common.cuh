@@ -52,7 +52,8 @@ struct Counters {
     unsigned int overflow;             // bit0: partner cap, bit1: PT cap, bit2: PQ cap, bit3: lookup miss
     unsigned int first_bad;            // first non-finite ball index (0xffffffff = none)
     unsigned int lookup_miss;          // inherited faces whose generator row has no such partner
-    unsigned int pad[2];
+    unsigned int tile_next;            // k_tri_tet3: next unclaimed tile (dynamic scheduling)
+    unsigned int pad[1];
 };
 
 constexpr int ERR_CAP = 1024;          // singular records kept per run

@@ -1,0 +1,397 @@
+// estimate3.cuh -- potential triangles and tetrahedra, warp-autonomous tiles
+// (reference pipeline.py:373-479).
+//
+// estimate2.cuh ran a block per tile of 64-128 generators with ~16 block barriers per tile; its
+// profile showed a quarter of all stall cycles at those barriers and a tet compaction that parked
+// the whole block behind one global atomic.  Here every WARP owns a tile of 16 consecutive
+// generators and its own slice of shared memory; nothing but __syncwarp separates the phases, so
+// the four warps of a block (and the blocks of an SM) drift apart and hide each other's fp64
+// dependency chains:
+//   A  stage the partner atoms of the tile (generators and partners share ONE index space in
+//      shared memory, so "sort the vertices by ball index" is a sort of four small integers
+//      followed by loads in sorted order -- no 32-byte records are swapped in registers)
+//   B  lane = partner slot i, round r pairs it with slot i + r of the same generator: reach
+//      pre-filter (pipeline.py:398-401), passing pairs queued with ballot/popc; the queue is solved
+//      a full warp at a time: ortho2 -> bit matrix M ("pair is a potential edge", pipeline.py:412-415),
+//      ortho3 -> bit matrix T (potential triangle, pipeline.py:417-420)
+//   C  warp scan over the T rows numbers the tile's triangles (one contiguous run of the global
+//      list per tile); every partner slot expands its own row and counts its tet candidates
+//      M[i] & M[j] & (bits > j)  (pipeline.py:447, 455-466: both new edges must be potential)
+//   D  warp scan numbers the candidates; one lane per candidate runs ortho4 (pipeline.py:475-478);
+//      kept tets are compacted with ballot/popc and ONE global atomic per warp round.
+// Cull mode: see dominated_by_partner3.
+#pragma once
+
+#include "common.cuh"
+#include "estimate.cuh"
+#include "estimate2.cuh"      // owner_of, nth_bit_multi
+#include "predicates.cuh"
+
+namespace axb {
+
+#ifndef T3_WARPS_V
+#define T3_WARPS_V 4
+#endif
+#ifndef T3_MINB
+#define T3_MINB 4
+#endif
+constexpr int T3_WARPS = T3_WARPS_V;      // warps per block (each one is independent)
+constexpr int T3_GENS = 16;               // generators per warp tile
+constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved as soon as 256 are waiting)
+
+template <int W>
+struct T3Cfg {
+    static constexpr int SCAP = W == 1 ? 128 : 256;     // partner slots per sub-pass (>= 64 * W: one generator always fits)
+    static constexpr int TCAP = W == 1 ? 224 : 512;     // triangles per round
+    static constexpr int NA = SCAP + T3_GENS;           // atom index space: partner slots, then the tile's generators
+};
+
+template <int W>
+struct T3Warp {
+    using C = T3Cfg<W>;
+    double ax[C::NA], ay[C::NA], az[C::NA], ar2[C::NA];
+    double sreach[C::SCAP];
+    unsigned long long M[C::SCAP * W];
+    unsigned long long T[C::SCAP * W];
+    unsigned long long D[C::SCAP * W];         // potential triangles already known to be dominated (cull mode)
+    int aorig[C::NA];
+    int srank[C::SCAP];
+    int rowpre[C::SCAP + 1];
+    int gdeg[T3_GENS];
+    unsigned gadj[T3_GENS];
+    int sp[T3_GENS + 1];                       // slot prefix over the whole tile
+    union {
+        unsigned wq[T3_WQCAP];                 // phase B: queue of reach-passing pairs (slot i | slot j << 16)
+        struct {
+            unsigned short tri_si[C::TCAP], tri_sj[C::TCAP];
+            int cpre[C::TCAP + 1];
+        } t;
+    } u;
+    unsigned char sgen[C::SCAP], sli[C::SCAP];
+};
+
+// exclusive scan of a[0..n) in place by one warp; a[n] = total; returns the total
+__device__ __forceinline__ int warp_scan_excl(int *a, int n) {
+    const int lane = lane_id();
+    int carry = 0;
+    for (int b = 0; b < n; b += 32) {
+        const int i = b + lane;
+        const int v = i < n ? a[i] : 0;
+        const int incl = warp_incl_scan(v);
+        if (i < n) a[i] = carry + incl - v;
+        carry += __shfl_sync(FULL, incl, 31);
+    }
+    if (lane == 0) a[n] = carry;
+    __syncwarp();
+    return carry;
+}
+
+template <int W>
+__device__ __forceinline__ Atom atom_at(const T3Warp<W> &S, int a) {
+    Atom p;
+    p.x = S.ax[a]; p.y = S.ay[a]; p.z = S.az[a]; p.r2 = S.ar2[a];
+    return p;
+}
+
+__device__ __forceinline__ void cswap_idx(int &oa, int &ia, int &ob, int &ib) {
+    if (oa > ob) { int t = oa; oa = ob; ob = t; t = ia; ia = ib; ib = t; }
+}
+
+// ortho solves on atoms named by their shared-memory index: sort (ball index, slot) pairs, then load in order
+template <int W>
+__device__ __forceinline__ Ortho ortho_edge_s(const T3Warp<W> &S, int a, int b, double eps_sing) {
+    int oa = S.aorig[a], ob = S.aorig[b];
+    cswap_idx(oa, a, ob, b);
+    return ortho2(atom_at(S, a), atom_at(S, b), eps_sing);
+}
+
+template <int W>
+__device__ __forceinline__ Ortho ortho_tri_s(const T3Warp<W> &S, int a, int b, int c, double eps_sing) {
+    int oa = S.aorig[a], ob = S.aorig[b], oc = S.aorig[c];
+    cswap_idx(oa, a, ob, b);
+    cswap_idx(ob, b, oc, c);
+    cswap_idx(oa, a, ob, b);
+    const Atom p[3] = {atom_at(S, a), atom_at(S, b), atom_at(S, c)};
+    return orthoN<3>(p, eps_sing);
+}
+
+template <int W>
+__device__ __forceinline__ Ortho ortho_tet_s(const T3Warp<W> &S, int a, int b, int c, int d, double eps_sing) {
+    int oa = S.aorig[a], ob = S.aorig[b], oc = S.aorig[c], od = S.aorig[d];
+    cswap_idx(oa, a, ob, b);
+    cswap_idx(oc, c, od, d);
+    cswap_idx(oa, a, oc, c);
+    cswap_idx(ob, b, od, d);
+    cswap_idx(ob, b, oc, c);
+    const Atom p[4] = {atom_at(S, a), atom_at(S, b), atom_at(S, c), atom_at(S, d)};
+    return orthoN<4>(p, eps_sing);
+}
+
+// Cull mode (the one-call path; the standalone stage API needs the complete potential lists and
+// switches it off): a simplex whose ortho-centre is dominated by another partner of its generator
+// fails the domination check of the pruning stage for certain -- a dominating ball is closer than
+// one cell side to the centre (pipeline.py:288-289), so it is one of the 27-cell candidates, and the
+// power distance below is evaluated exactly like pipeline.py:308-309.  The partners are already in
+// shared memory, so most dominated simplices are settled here and never reach the AC2 kernels.
+template <int W>
+__device__ __forceinline__ bool dominated_by_partner3(const T3Warp<W> &S, int sb, int se, int s0, int s1, int s2,
+                                                      double cx, double cy, double cz, double thr) {
+    for (int s = sb; s < se; ++s) {
+        if (s == s0 || s == s1 || s == s2) continue;
+        const double ddx = S.ax[s] - cx, ddy = S.ay[s] - cy, ddz = S.az[s] - cz;
+        const double dp = ((ddx * ddx + ddy * ddy) + ddz * ddz) - S.ar2[s];
+        if (dp < thr) return true;
+    }
+    return false;
+}
+
+template <int W>
+__global__ void __launch_bounds__(T3_WARPS * 32, T3_MINB) k_tri_tet3(EstParams P, int rank_lo, int rank_hi) {
+    using C = T3Cfg<W>;
+    constexpr int PCAP = 64 * W;
+    constexpr int SCAP = C::SCAP, TCAP = C::TCAP;
+    extern __shared__ __align__(16) unsigned char s_raw3[];
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    T3Warp<W> &S = reinterpret_cast<T3Warp<W> *>(s_raw3)[warp];
+    const int ntiles = (rank_hi - rank_lo + T3_GENS - 1) / T3_GENS;
+
+    // Tiles are claimed from a global counter (dense regions make tiles very unequal); the claim for the
+    // NEXT tile is issued before the current one is processed, so its round trip is hidden.
+    int tile_n = 0;
+    if (lane == 0) tile_n = (int)atomicAdd(&P.ctr->tile_next, 1u);
+    for (;;) {
+        const int tile = __shfl_sync(FULL, tile_n, 0);
+        if (tile >= ntiles) break;
+        if (lane == 0) tile_n = (int)atomicAdd(&P.ctr->tile_next, 1u);
+        const int t0 = rank_lo + tile * T3_GENS;
+        const int ng_all = min(T3_GENS, rank_hi - t0);
+        __syncwarp();                                       // previous tile fully consumed
+        {   // generators of the tile: atom index SCAP + g
+            int d = 0;
+            if (lane < ng_all) {
+                d = min(__ldg(P.deg + t0 + lane), PCAP);
+                if (d < 2) d = 0;                           // no partner pair, nothing to do
+                S.gadj[lane] = __ldg(P.adj_off + t0 + lane);
+                const Atom a = load_atom(P.atoms, t0 + lane);
+                S.ax[SCAP + lane] = a.x; S.ay[SCAP + lane] = a.y; S.az[SCAP + lane] = a.z; S.ar2[SCAP + lane] = a.r2;
+                S.aorig[SCAP + lane] = __ldg(P.orig + t0 + lane);
+            }
+            if (lane < T3_GENS) S.gdeg[lane] = d;
+            const int incl = warp_incl_scan(d);
+            if (lane < T3_GENS) S.sp[lane + 1] = incl;
+            if (lane == 0) S.sp[0] = 0;
+        }
+        __syncwarp();
+        int g0 = 0;
+        while (g0 < ng_all) {
+            // ---- sub-pass [g0, g1): as many generators as fit the slot budget (normally the whole tile)
+            const int base = S.sp[g0];
+            int g1;
+            {
+                const bool in = lane >= g0 && lane < ng_all && S.sp[lane + 1] - base <= SCAP;
+                g1 = g0 + __popc(__ballot_sync(FULL, in));  // slot counts are monotone: the set is a prefix
+            }
+            const int nslots = S.sp[g1] - base;
+            int npairs_any = 0;
+            if (lane >= g0 && lane < g1) npairs_any = S.gdeg[lane];
+            if (__ballot_sync(FULL, npairs_any > 0) != 0u) {
+                // ---- A: stage the partner atoms (ascending rank inside a generator = pipeline.py:362-370)
+                for (int s = lane; s < nslots; s += 32) {
+                    int g = g0;                             // last generator with sp[g] - base <= s
+#pragma unroll
+                    for (int step = 8; step > 0; step >>= 1)
+                        if (g + step < g1 && S.sp[g + step] - base <= s) g += step;
+                    const int li = s - (S.sp[g] - base);
+                    const int rk = __ldg(P.pe_v + S.gadj[g] + li);
+                    const Atom a = load_atom(P.atoms, rk);
+                    S.ax[s] = a.x; S.ay[s] = a.y; S.az[s] = a.z; S.ar2[s] = a.r2;
+                    S.sreach[s] = __ldg(P.reach + rk);
+                    S.aorig[s] = __ldg(P.orig + rk);
+                    S.srank[s] = rk;
+                    S.sgen[s] = (unsigned char)g;
+                    S.sli[s] = (unsigned char)li;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) { S.M[s * W + w] = 0ull; S.T[s * W + w] = 0ull; S.D[s * W + w] = 0ull; }
+                }
+                __syncwarp();
+                // ---- B: partner pairs.  Lane = partner slot i; round r pairs it with slot i + r of the same
+                // generator (np.triu_indices order is irrelevant here: results are bits).
+                {
+                    unsigned *wq = S.u.wq;
+                    int qn = 0;                                           // warp-uniform queue fill
+                    auto solve_queue = [&](int count) {                    // dense ortho2 + ortho3 over wq[0..count)
+                        for (int x0 = 0; x0 < count; x0 += 32) {
+                            const int x = x0 + lane;
+                            if (x < count) {
+                                const unsigned pr = wq[x];
+                                const int si = (int)(pr & 0xffffu), sj = (int)(pr >> 16);
+                                const int g = S.sgen[si];
+                                const int i = S.sli[si], j = S.sli[sj];
+                                const int t = t0 + g;
+                                const int d = S.gdeg[g];
+                                const unsigned q = (unsigned)(i * (2 * d - i - 1) / 2 + (j - i - 1));   // triu ordinal
+                                const Ortho e2 = ortho_edge_s(S, si, sj, P.tol.eps_sing);                // pipeline.py:412-414
+                                if (e2.singular) record_singular(P, make_err_key(ST_VW, t, q), S.aorig[si], S.aorig[sj], -1, -1, 2);
+                                if (e2.size <= P.tol.lim_a) {                                            // pipeline.py:415
+                                    atomicOr(&S.M[si * W + (j >> 6)], 1ull << (j & 63));
+                                    atomicOr(&S.M[sj * W + (i >> 6)], 1ull << (i & 63));
+                                    const Ortho e3 = ortho_tri_s(S, SCAP + g, si, sj, P.tol.eps_sing);   // pipeline.py:417-419
+                                    if (e3.singular)
+                                        record_singular(P, make_err_key(ST_TRI, t, q), S.aorig[SCAP + g], S.aorig[si], S.aorig[sj], -1, 3);
+                                    if (e3.size <= P.tol.lim_a) {                                        // pipeline.py:420
+                                        atomicOr(&S.T[si * W + (j >> 6)], 1ull << (j & 63));
+                                        if (P.cull & 2) {
+                                            const int sb = S.sp[g] - base;
+                                            if (dominated_by_partner3(S, sb, sb + d, si, sj, -1, e3.cx, e3.cy, e3.cz, e3.size - P.tol.eps_abs))
+                                                atomicOr(&S.D[si * W + (j >> 6)], 1ull << (j & 63));
+                                        }
+                                    }
+                                }
+                            }
+                        }
+                        __syncwarp();
+                    };
+                    for (int s0 = 0; s0 < nslots; s0 += 32) {
+                        const int si = s0 + lane;
+                        int more = 0;
+                        Atom av;
+                        double rv = 0.0;
+                        av.x = av.y = av.z = av.r2 = 0.0;
+                        if (si < nslots) {
+                            more = S.gdeg[S.sgen[si]] - 1 - (int)S.sli[si];   // partners after slot i in its generator
+                            av = atom_at(S, si);
+                            rv = S.sreach[si];
+                        }
+                        int rounds = more;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) rounds = max(rounds, __shfl_xor_sync(FULL, rounds, o));
+                        for (int r = 1; r <= rounds; ++r) {
+                            bool pass = false;
+                            const int sj = si + r;
+                            if (r <= more) pass = reach_pair(av, rv, atom_at(S, sj), S.sreach[sj]);   // pipeline.py:398-401
+                            const unsigned m = __ballot_sync(FULL, pass);
+                            if (m) {
+                                if (qn + 32 > T3_WQCAP) { __syncwarp(); solve_queue(qn); qn = 0; }
+                                if (pass) wq[qn + __popc(m & lanemask_lt())] = (unsigned)si | ((unsigned)sj << 16);
+                                qn += __popc(m);
+                                __syncwarp();
+                                if (qn >= 32 * 8) { solve_queue(qn); qn = 0; }
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    solve_queue(qn);
+                }
+                // ---- C: triangle list of the tile
+                for (int s = lane; s < nslots; s += 32) {
+                    int c = 0;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) c += __popcll(S.T[s * W + w]);
+                    S.rowpre[s] = c;
+                }
+                __syncwarp();
+                const int ntri = warp_scan_excl(S.rowpre, nslots);
+                // one contiguous run of the global triangle list per tile: the prune kernel that reads it
+                // then works on one neighbourhood at a time (L1 locality)
+                unsigned pt_base = 0;
+                if (lane == 0 && ntri > 0) pt_base = atomicAdd(&P.ctr->n_pt, (unsigned)ntri);
+                pt_base = __shfl_sync(FULL, pt_base, 0);
+                for (int tc0 = 0; tc0 < ntri; tc0 += TCAP) {
+                    const int ntc = min(TCAP, ntri - tc0);
+                    // every partner slot expands its own triangles (bits of its T row) into the round's list
+                    for (int srow = lane; srow < nslots; srow += 32) {
+                        int tt = S.rowpre[srow];
+                        if (tt >= tc0 + ntc || S.rowpre[srow + 1] <= tc0) continue;
+                        const int g = S.sgen[srow];
+                        const int sg = S.sp[g] - base;
+#pragma unroll
+                        for (int w = 0; w < W; ++w) {
+                            unsigned long long bits = S.T[srow * W + w];
+                            while (bits) {
+                                const int j = 64 * w + __ffsll((long long)bits) - 1;
+                                bits &= bits - 1;
+                                const int x = tt - tc0;
+                                ++tt;
+                                if (x < 0 || x >= ntc) continue;
+                                const int sj = sg + j;
+                                S.u.t.tri_si[x] = (unsigned short)srow;
+                                S.u.t.tri_sj[x] = (unsigned short)sj;
+                                // partners above j adjacent (in M) to both: rank[x] > rank_hi (pipeline.py:447)
+                                int cnt = 0;
+#pragma unroll
+                                for (int w2 = 0; w2 < W; ++w2) {
+                                    unsigned long long m = S.M[srow * W + w2] & S.M[sj * W + w2];
+                                    const int lowbit = j + 1 - 64 * w2;
+                                    if (lowbit >= 64) m = 0ull;
+                                    else if (lowbit > 0) m &= ~0ull << lowbit;
+                                    cnt += __popcll(m);
+                                }
+                                S.u.t.cpre[x] = cnt;
+                                const unsigned pos = pt_base + (unsigned)(tc0 + x);
+                                const int dom = (int)((S.D[srow * W + (j >> 6)] >> (j & 63)) & 1ull);
+                                if (pos < P.pt_cap)
+                                    P.pt[pos] = make_int4(t0 + g, S.srank[srow], S.srank[sj],
+                                                          (int)S.sli[srow] | (j << 16) | (dom << 31));
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    const int ncand = warp_scan_excl(S.u.t.cpre, ntc);
+                    // ---- D: dense over tet candidates (pipeline.py:447-479)
+                    for (int c0 = 0; c0 < ncand; c0 += 32) {
+                        const int c = c0 + lane;
+                        bool keep = false;
+                        int4 er = make_int4(0, 0, 0, 0);
+                        int el = 0;
+                        if (c < ncand) {
+                            const int x = owner_of(S.u.t.cpre, ntc, c);
+                            const int s = S.u.t.tri_si[x], sj = S.u.t.tri_sj[x];
+                            const int j = S.sli[sj];
+                            unsigned long long cm[W];
+#pragma unroll
+                            for (int w = 0; w < W; ++w) {
+                                unsigned long long m = S.M[s * W + w] & S.M[sj * W + w];
+                                const int lowbit = j + 1 - 64 * w;
+                                if (lowbit >= 64) m = 0ull;
+                                else if (lowbit > 0) m &= ~0ull << lowbit;
+                                cm[w] = m;
+                            }
+                            const int k = nth_bit_multi<W>(cm, c - S.u.t.cpre[x]);
+                            const int g = S.sgen[s];
+                            const int sb = S.sp[g] - base;
+                            const int sk = sb + k;
+                            const int t = t0 + g;
+                            const Ortho e4 = ortho_tet_s(S, SCAP + g, s, sj, sk, P.tol.eps_sing);        // pipeline.py:475-477
+                            if (e4.singular) {
+                                const unsigned tri_ord = (unsigned)(tc0 + x - S.rowpre[sb]);             // ordinal among u's triangles
+                                record_singular(P, make_err_key(ST_TET, t, (tri_ord << 8) | (unsigned)k), S.aorig[SCAP + g],
+                                                S.aorig[s], S.aorig[sj], S.aorig[sk], 4);
+                            }
+                            keep = e4.size <= P.tol.lim_a;                                               // pipeline.py:478
+                            if (keep && (P.cull & 1) &&
+                                dominated_by_partner3(S, sb, sb + S.gdeg[g], s, sj, sk, e4.cx, e4.cy, e4.cz, e4.size - P.tol.eps_abs))
+                                keep = false;        // AC2 would fail at this partner (it lies in the 27-cell block): never kept
+                            er = make_int4(t, S.srank[s], S.srank[sj], S.srank[sk]);
+                            el = (int)S.sli[s] | (j << 8) | (k << 16);
+                        }
+                        const unsigned m = __ballot_sync(FULL, keep);
+                        if (m) {
+                            unsigned pq_base = 0;
+                            if (lane == 0) pq_base = atomicAdd(&P.ctr->n_pq, (unsigned)__popc(m));
+                            pq_base = __shfl_sync(FULL, pq_base, 0);
+                            if (keep) {
+                                const unsigned pos = pq_base + (unsigned)__popc(m & lanemask_lt());
+                                if (pos < P.pq_cap) { P.pq_r[pos] = er; P.pq_l[pos] = el; }
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+            g0 = g1;
+        }
+    }
+}
+
+}  // namespace axb
