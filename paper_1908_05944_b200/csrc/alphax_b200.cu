@@ -853,18 +853,18 @@ int alloc_prune_arrays(axb_ctx *c) {
     CUDA_TRY(c, cudaMemsetAsync(c->vkeep, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(&c->ctr->n_k3, 0, sizeof(unsigned int), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(&c->ctr->lookup_miss, 0, sizeof(unsigned int), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->ctr->work_next, 0, sizeof(c->ctr->work_next), c->stream));
     return AXB_OK;
 }
 
 // triangles, edges, vertices of the pruning stage (the tets are done by the caller)
 int run_prune_lower(axb_ctx *c) {
     PruneParams P = prune_params(c);
-    const unsigned grid = (unsigned)c->sm_count * 8u;
     int st;
-    k_prune_tris<<<grid, PRUNE_THREADS, 0, c->stream>>>(P);
+    k_prune_tris<<<(unsigned)c->sm_count * (unsigned)PRUNE_GRID, PRUNE_THREADS, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_TRIANGLES + 1)) != AXB_OK) return st;
-    k_prune_edges<<<grid, PRUNE_THREADS, 0, c->stream>>>(P);
+    k_prune_edges<<<(unsigned)c->sm_count * (unsigned)PRUNE_GRID, PRUNE_THREADS, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_EDGES + 1)) != AXB_OK) return st;
     k_prune_vertices<<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>(P, c->rank_lo, c->rank_hi);
@@ -879,7 +879,11 @@ int run_prune(axb_ctx *c) {
     int st = alloc_prune_arrays(c);
     if (st != AXB_OK) return st;
     PruneParams P = prune_params(c);
-    k_prune_tets<<<(unsigned)c->sm_count * 8u, 256, 0, c->stream>>>(P);
+    // few tets per thread: static grid-stride; many (large alpha, dense cores): dynamic 64-tet claims
+    if ((uint64_t)c->n_pq > (uint64_t)c->n + c->n / 2)
+        k_prune_tets<1><<<(unsigned)c->sm_count * (unsigned)TETS_MINB, 256, 0, c->stream>>>(P);
+    else
+        k_prune_tets<0><<<(unsigned)c->sm_count * 8u, 256, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_TETS + 1)) != AXB_OK) return st;
     return run_prune_lower(c);
@@ -1214,7 +1218,11 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
         return AXB_OK;
     };
     // tets
-    k_prune_tets<<<grid, 256, 0, c->stream>>>(P);
+    // few tets per thread: static grid-stride; many (large alpha, dense cores): dynamic 64-tet claims
+    if ((uint64_t)c->n_pq > (uint64_t)c->n + c->n / 2)
+        k_prune_tets<1><<<(unsigned)c->sm_count * (unsigned)TETS_MINB, 256, 0, c->stream>>>(P);
+    else
+        k_prune_tets<0><<<(unsigned)c->sm_count * 8u, 256, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_TETS + 1)) != AXB_OK) return st;
     if ((st = device_scan(c, c->cnt3, n, c->off3)) != AXB_OK) return st;
@@ -1225,7 +1233,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     LAUNCH_CHECK(c);
     if ((st = mark_ready(3)) != AXB_OK) return st;
     // triangles
-    k_prune_tris<<<grid, PRUNE_THREADS, 0, c->stream>>>(P);
+    k_prune_tris<<<(unsigned)c->sm_count * (unsigned)PRUNE_GRID, PRUNE_THREADS, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_TRIANGLES + 1)) != AXB_OK) return st;
     if ((st = device_scan(c, c->cnt2, n, c->off2)) != AXB_OK) return st;
@@ -1236,7 +1244,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     LAUNCH_CHECK(c);
     if ((st = mark_ready(2)) != AXB_OK) return st;
     // edges
-    k_prune_edges<<<grid, PRUNE_THREADS, 0, c->stream>>>(P);
+    k_prune_edges<<<(unsigned)c->sm_count * (unsigned)PRUNE_GRID, PRUNE_THREADS, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_EDGES + 1)) != AXB_OK) return st;
     if ((st = device_scan(c, c->cnt1, n, c->off1)) != AXB_OK) return st;

@@ -53,7 +53,7 @@ struct Counters {
     unsigned int first_bad;            // first non-finite ball index (0xffffffff = none)
     unsigned int lookup_miss;          // inherited faces whose generator row has no such partner
     unsigned int tile_next;            // k_tri_tet3: next unclaimed tile (dynamic scheduling)
-    unsigned int pad[1];
+    unsigned int work_next[3];         // prune kernels (tets, triangles, edges): next unclaimed chunk
 };
 
 constexpr int ERR_CAP = 1024;          // singular records kept per run

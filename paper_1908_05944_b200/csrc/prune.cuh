@@ -105,14 +105,41 @@ __device__ __forceinline__ bool lists_overflowed(const PruneParams &P) {
     return P.ctr->n_pq > P.pq_cap || P.ctr->n_pt > P.pt_cap || P.ctr->n_pe > P.pe_cap;
 }
 
+#ifndef PRUNE_GRID
+#define PRUNE_GRID 4        // blocks per SM launched = resident blocks (work is claimed dynamically)
+#endif
 #ifndef TETS_MINB
 #define TETS_MINB 3
 #endif
+template <int DYN>
 __global__ void __launch_bounds__(256, TETS_MINB) k_prune_tets(PruneParams P) {
     __shared__ int2 s_rows[9][256];
     if (lists_overflowed(P)) return;
     const unsigned n_pq = min(P.ctr->n_pq, P.pq_cap);
-    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pq; e += gridDim.x * blockDim.x) {
+    // a warp claims 32 tets at a time from a global counter (dense regions make tets very unequal); the
+    // next claim is issued before the current chunk is processed
+    // DYN = 0: plain grid-stride loop (best while there are only a few tets per thread).
+    // DYN = 1: a warp claims 64 tets at a time from a global counter -- dense regions make tets very
+    // unequal -- and issues the next claim before it works on the current one.  Same-address atomics are
+    // served at ~1 per ns, so claims must stay coarse (measured: 32 per claim costs more than it balances).
+    constexpr unsigned CLAIM = 64u;
+    const int lane = lane_id();
+    unsigned chunk_n = 0;
+    if (DYN && lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[0], 1u);
+    const unsigned stride = DYN ? 32u : gridDim.x * blockDim.x;
+    for (;;) {
+        unsigned e0, e1;
+        if (DYN) {
+            const unsigned chunk = __shfl_sync(FULL, chunk_n, 0);
+            if ((unsigned long long)chunk * CLAIM >= n_pq) break;
+            if (lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[0], 1u);
+            e0 = chunk * CLAIM + (unsigned)lane;
+            e1 = min(chunk * CLAIM + CLAIM, n_pq);
+        } else {
+            e0 = blockIdx.x * blockDim.x + threadIdx.x;
+            e1 = n_pq;
+        }
+      for (unsigned e = e0; e < e1; e += stride) {
         const int4 r = P.pq_r[e];
         const int l = P.pq_l[e];
         const int i = l & 0xff, j = (l >> 8) & 0xff, k = (l >> 16) & 0xff;
@@ -165,90 +192,131 @@ __global__ void __launch_bounds__(256, TETS_MINB) k_prune_tets(PruneParams P) {
         if (!e5) atomicAdd(P.cnt1 + min(ow, ox), 1u);
         if (iw < 0 || ix < 0) { note_miss(P); if (iw < 0) note_miss(P); if (ix < 0) note_miss(P); }
         if (jx < 0) note_miss(P);
+      }
+        if (!DYN) break;
     }
 }
 
-// Block-level work compaction for the two kernels below: most potential triangles / edges are
-// already kept by inheritance, so a block first scans PRUNE_BATCH x 256 entries, queues the free
-// ones in shared memory and then runs the expensive part (ortho solve + AC2) with packed lanes.
 constexpr int PRUNE_THREADS = 256;
 #ifndef PRUNE_MINB
 #define PRUNE_MINB 4      // <= 64 registers: measured best (occupancy beats the few spilled values)
 #endif
-constexpr int PRUNE_BATCH = 4;
 
-__device__ __forceinline__ void queue_push(bool want, unsigned value, unsigned *queue, int *qn) {
-    const unsigned m = __ballot_sync(FULL, want);
-    if (m) {
-        int base = 0;
-        const int leader = __ffs(m) - 1;
-        if (lane_id() == leader) base = atomicAdd(qn, __popc(m));
-        base = __shfl_sync(FULL, base, leader);
-        if (want) queue[base + __popc(m & lanemask_lt())] = value;
-    }
-}
+// Warp-autonomous work compaction for the two kernels below: most potential triangles / edges are
+// already kept by inheritance, so a warp claims chunks of the list from a global counter, pushes the
+// FREE entries onto its own shared-memory stack and runs the expensive part (ortho solve + AC2) whenever
+// 32 are waiting -- packed lanes, no block barriers, and dense regions do not leave other warps idle.
+constexpr int PRUNE_WARPS = PRUNE_THREADS / 32;
+#ifndef PRUNE_CLAIM_V
+#define PRUNE_CLAIM_V 2
+#endif
+constexpr int PRUNE_CLAIM = PRUNE_CLAIM_V;               // list entries per lane and claim (256 per warp)
+constexpr int PRUNE_STACK = 64;              // free entries parked per warp (processed as soon as 32 are waiting)
 
 // pipeline.py:502-505: AC2 for the triangles no kept tet inherited
 __global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_tris(PruneParams P) {
-    __shared__ unsigned queue[PRUNE_THREADS * PRUNE_BATCH];
+    __shared__ unsigned s_stack[PRUNE_WARPS][PRUNE_STACK];
     __shared__ int2 s_rows[9][PRUNE_THREADS];
-    __shared__ int qn;
     if (lists_overflowed(P)) return;
     const unsigned n_pt = min(P.ctr->n_pt, P.pt_cap);
-    const unsigned span = PRUNE_THREADS * PRUNE_BATCH;
-    for (unsigned base = blockIdx.x * span; base < n_pt; base += gridDim.x * span) {
-        if (threadIdx.x == 0) qn = 0;
-        __syncthreads();
-#pragma unroll
-        for (int b = 0; b < PRUNE_BATCH; ++b) {
-            const unsigned e = base + b * PRUNE_THREADS + threadIdx.x;
+    const int lane = lane_id();
+    unsigned *stack = s_stack[threadIdx.x >> 5];
+    int sn = 0;                                       // warp-uniform stack fill
+
+    auto settle = [&](unsigned e) {                   // one free triangle per lane
+        const int4 r = P.pt[e];
+        const int i = r.w & 0xffff, j = (r.w >> 16) & 0x7fff;
+        const unsigned bu = __ldg(P.adj_off + r.x);
+        const Atom au = load_atom(P.atoms, r.x), av = load_atom(P.atoms, r.y), aw = load_atom(P.atoms, r.z);
+        const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z);
+        const Ortho o = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);
+        if (!ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, -1, &s_rows[0][threadIdx.x], PRUNE_THREADS)) return;
+        mark_tri(P, bu + i, j, min3(ou, ov, ow));
+        mark_edge(P, bu + i, min(ou, ov));
+        mark_edge(P, bu + j, min(ou, ow));
+        const unsigned bv = __ldg(P.adj_off + r.y);
+        const int iw = find_partner(P.pe_v, bv, __ldg(P.deg + r.y), r.z);
+        if (iw >= 0) mark_edge(P, bv + iw, min(ov, ow)); else note_miss(P);
+    };
+
+    // fill the stack from claimed chunks until 32 free entries wait (or the list is exhausted), then settle
+    // up to 32 of them -- ONE call site of the expensive part keeps the register allocation tight
+    const unsigned span = 32u * PRUNE_CLAIM;
+    unsigned chunk_n = 0, chunk = 0;
+    int b = PRUNE_CLAIM;                              // sub-step inside the current chunk (PRUNE_CLAIM = need a new one)
+    bool exhausted = false;
+    if (lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[1], 1u);
+    for (;;) {
+        while (sn < 32 && !exhausted) {
+            if (b == PRUNE_CLAIM) {
+                chunk = __shfl_sync(FULL, chunk_n, 0);
+                if ((unsigned long long)chunk * span >= n_pt) { exhausted = true; break; }
+                if (lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[1], 1u);
+                b = 0;
+            }
+            const unsigned e = chunk * span + (unsigned)(b * 32 + lane);
+            ++b;
             bool is_free = false;
             if (e < n_pt) {
                 const int4 r = P.pt[e];
-                if (r.w >= 0) {                               // bit 31: already known to be dominated (k_tri_tet2 cull mode)
+                if (r.w >= 0) {                               // bit 31: already known to be dominated (cull mode)
                     const int i = r.w & 0xffff, j = (r.w >> 16) & 0x7fff;
                     const unsigned bu = __ldg(P.adj_off + r.x);
                     const unsigned long long word = P.trimask[(size_t)(bu + i) * P.W + (j >> 6)];
                     is_free = !((word >> (j & 63)) & 1ull);   // not inherited from a kept tet
                 }
             }
-            queue_push(is_free, e, queue, &qn);
+            const unsigned m = __ballot_sync(FULL, is_free);
+            if (is_free) stack[sn + __popc(m & lanemask_lt())] = e;
+            sn += __popc(m);
+            __syncwarp();
         }
-        __syncthreads();
-        const int nq = qn;
-        for (int x = threadIdx.x; x < nq; x += PRUNE_THREADS) {
-            const int4 r = P.pt[queue[x]];
-            const int i = r.w & 0xffff, j = (r.w >> 16) & 0x7fff;
-            const unsigned bu = __ldg(P.adj_off + r.x);
-            const Atom au = load_atom(P.atoms, r.x), av = load_atom(P.atoms, r.y), aw = load_atom(P.atoms, r.z);
-            const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z);
-            const Ortho o = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);
-            if (!ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, -1, &s_rows[0][threadIdx.x], PRUNE_THREADS)) continue;
-            mark_tri(P, bu + i, j, min3(ou, ov, ow));
-            mark_edge(P, bu + i, min(ou, ov));
-            mark_edge(P, bu + j, min(ou, ow));
-            const unsigned bv = __ldg(P.adj_off + r.y);
-            const int iw = find_partner(P.pe_v, bv, __ldg(P.deg + r.y), r.z);
-            if (iw >= 0) mark_edge(P, bv + iw, min(ov, ow)); else note_miss(P);
-        }
-        __syncthreads();
+        if (sn == 0) break;
+        const int take = min(sn, 32);
+        sn -= take;
+        const unsigned mine = stack[sn + min(lane, take - 1)];
+        __syncwarp();
+        if (lane < take) settle(mine);
     }
 }
 
 // pipeline.py:510-513: AC2 for the edges nothing inherited; kept edges mark their endpoints
 __global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_edges(PruneParams P) {
-    __shared__ unsigned queue[PRUNE_THREADS * PRUNE_BATCH];
+    __shared__ unsigned s_stack[PRUNE_WARPS][PRUNE_STACK];
     __shared__ int2 s_rows[9][PRUNE_THREADS];
-    __shared__ int qn;
     if (lists_overflowed(P)) return;
     const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
-    const unsigned span = PRUNE_THREADS * PRUNE_BATCH;
-    for (unsigned base = blockIdx.x * span; base < n_pe; base += gridDim.x * span) {
-        if (threadIdx.x == 0) qn = 0;
-        __syncthreads();
-#pragma unroll
-        for (int b = 0; b < PRUNE_BATCH; ++b) {
-            const unsigned e = base + b * PRUNE_THREADS + threadIdx.x;
+    const int lane = lane_id();
+    unsigned *stack = s_stack[threadIdx.x >> 5];
+    int sn = 0;
+
+    auto settle = [&](unsigned e) {
+        const int u = __ldg(P.pe_u + e), v = __ldg(P.pe_v + e);
+        const Atom au = load_atom(P.atoms, u), av = load_atom(P.atoms, v);
+        const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + v);
+        const Ortho o = ortho_edge(ou, au, ov, av, P.tol.eps_sing);
+        if (ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, u, v, -1, -1, &s_rows[0][threadIdx.x], PRUNE_THREADS)) {
+            mark_edge(P, e, min(ou, ov));
+            P.vflag[u] = 1;
+            P.vflag[v] = 1;
+        }
+    };
+
+    const unsigned span = 32u * PRUNE_CLAIM;
+    unsigned chunk_n = 0, chunk = 0;
+    int b = PRUNE_CLAIM;
+    bool exhausted = false;
+    if (lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[2], 1u);
+    for (;;) {
+        while (sn < 32 && !exhausted) {
+            if (b == PRUNE_CLAIM) {
+                chunk = __shfl_sync(FULL, chunk_n, 0);
+                if ((unsigned long long)chunk * span >= n_pe) { exhausted = true; break; }
+                if (lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[2], 1u);
+                b = 0;
+            }
+            const unsigned e = chunk * span + (unsigned)(b * 32 + lane);
+            ++b;
             bool is_free = false;
             if (e < n_pe) {
                 const int u = __ldg(P.pe_u + e);
@@ -259,23 +327,17 @@ __global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_edges(Prune
                     is_free = u >= P.rank_lo && u < P.rank_hi;   // halo rows of a slab are their owner's business
                 }
             }
-            queue_push(is_free, e, queue, &qn);
+            const unsigned m = __ballot_sync(FULL, is_free);
+            if (is_free) stack[sn + __popc(m & lanemask_lt())] = e;
+            sn += __popc(m);
+            __syncwarp();
         }
-        __syncthreads();
-        const int nq = qn;
-        for (int x = threadIdx.x; x < nq; x += PRUNE_THREADS) {
-            const unsigned e = queue[x];
-            const int u = __ldg(P.pe_u + e), v = __ldg(P.pe_v + e);
-            const Atom au = load_atom(P.atoms, u), av = load_atom(P.atoms, v);
-            const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + v);
-            const Ortho o = ortho_edge(ou, au, ov, av, P.tol.eps_sing);
-            if (ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, u, v, -1, -1, &s_rows[0][threadIdx.x], PRUNE_THREADS)) {
-                mark_edge(P, e, min(ou, ov));
-                P.vflag[u] = 1;
-                P.vflag[v] = 1;
-            }
-        }
-        __syncthreads();
+        if (sn == 0) break;
+        const int take = min(sn, 32);
+        sn -= take;
+        const unsigned mine = stack[sn + min(lane, take - 1)];
+        __syncwarp();
+        if (lane < take) settle(mine);
     }
 }
 
