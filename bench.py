@@ -140,7 +140,7 @@ def algorithmic_bytes(n, G, E, T, Q, K):
 KERNEL_OF_STAGE = {
     "grid": "k_bounds+k_cell_keys+scan+k_cell_scatter+k_cell_finalize",
     "potential_edges": "k_edges",
-    "potential_triangles": "k_tri_tet2",
+    "potential_triangles": "k_tri_tet3",
     "prune_tets": "k_prune_tets",
     "prune_triangles": "k_prune_tris",
     "prune_edges": "k_prune_edges",
