@@ -1131,6 +1131,10 @@ extern "C" int axb_compute_host_begin(axb_ctx *c, int64_t n, const double *h_xyz
     return AXB_OK;
 }
 
+#ifndef AXB_WIRE_DEFAULT
+#define AXB_WIRE_DEFAULT 0
+#endif
+
 namespace {
 // A row count goes to the host as a zero-copy store from a one-thread kernel, NOT as a 4-byte
 // cudaMemcpyAsync: that would queue on the same D2H copy engine behind megabytes of row chunks and
@@ -1147,7 +1151,7 @@ struct PoolRun {                                   // every exit path closes the
     axb::WidenPool *pool;
     ~PoolRun() { if (pool) pool->finish(); }
 };
-struct PendingChunk { cudaEvent_t ev; const int32_t *src; int64_t *dst; size_t n; };
+struct PendingChunk { cudaEvent_t ev; const int32_t *src; int64_t *dst; size_t n; int dim; size_t row0; };
 }  // namespace
 
 extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, int64_t *h_t, int64_t *h_q,
@@ -1158,13 +1162,27 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     int st = alloc_prune_arrays(c);
     if (st != AXB_OK) return st;
     int64_t *h[4] = {h_v, h_e, h_t, h_q};
+    // What crosses PCIe per row: int32 values, widened by the host threads; nothing at all for the vertices
+    // when every vertex is kept.  Optional compact formats (AXB_WIRE bit 0: edges send only their second
+    // column, bit 1: triangles their last two; the owner column is rebuilt on the host from the per-owner row
+    // offsets, which travel once) cut the PCIe bytes by another third, but on the 16-core host measured here
+    // the row expansion then becomes the bottleneck (finish 2.9 ms instead of 2.4 ms at 1M atoms), so they
+    // are off by default.
+    const int wire_mode = getenv("AXB_WIRE") ? atoi(getenv("AXB_WIRE")) : AXB_WIRE_DEFAULT;
+    const bool compact1 = (wire_mode & 1) != 0, compact2 = (wire_mode & 2) != 0;
+    const int wire_width[4] = {1, compact1 ? 1 : 2, compact2 ? 2 : 3, 4};
     int32_t *d_out[4];
     size_t stage_off[4], stage_elems = 0;
     for (int d = 0; d < 4; ++d) {
-        const size_t elems = (size_t)std::max<int64_t>(c->host_cap[d], 1) * (d + 1);
+        const size_t elems = (size_t)std::max<int64_t>(c->host_cap[d], 1) * wire_width[d];
         ARENA(c, d_out[d], int32_t, elems);
         stage_off[d] = stage_elems;
         stage_elems += (elems + 63) / 64 * 64;
+    }
+    size_t stage_offsets[3] = {0, 0, 0};              // staged copies of off1 / off2 (index = dimension)
+    for (int d = 1; d <= 2; ++d) {
+        stage_offsets[d] = stage_elems;
+        stage_elems += (n + 2 + 63) / 64 * 64;
     }
     ARENA(c, c->off1, uint32_t, n + 2);
     ARENA(c, c->off2, uint32_t, n + 2);
@@ -1184,7 +1202,9 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     }
     if (!c->pool) {
         unsigned hw = std::thread::hardware_concurrency();
-        unsigned workers = std::max(1u, std::min(16u, hw ? hw : 4u)) - 1u;      // the calling thread helps too
+        // the calling thread helps too; two cores stay free for the CUDA driver's own threads (measured:
+        // 14 of 16 beats 16 of 16, which gets preempted in the middle of tasks)
+        unsigned workers = std::max(3u, std::min(32u, hw ? hw : 4u)) - 3u;
         if (const char *e = getenv("AXB_WIDEN_THREADS")) workers = (unsigned)std::max(0, atoi(e) - 1);
         c->pool = new (std::nothrow) axb::WidenPool(workers);
         if (!c->pool) return fail(c, AXB_ERR_INTERNAL, "cannot create the widening threads");
@@ -1240,7 +1260,8 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(2, c->off2 + n)) != AXB_OK) return st;
     k_scatter_tris<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[2]);
     LAUNCH_CHECK(c);
-    k_emit_tris<int32_t><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, d_out[2], c->ctr);
+    if (compact2) k_emit_tris<int32_t, true><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, d_out[2], c->ctr);
+    else k_emit_tris<int32_t, false><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, d_out[2], c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(2)) != AXB_OK) return st;
     // edges
@@ -1251,7 +1272,8 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(1, c->off1 + n)) != AXB_OK) return st;
     k_scatter_edges<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[1]);
     LAUNCH_CHECK(c);
-    k_emit_edges<int32_t><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, d_out[1], c->ctr);
+    if (compact1) k_emit_edges<int32_t, true><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, d_out[1], c->ctr);
+    else k_emit_edges<int32_t, false><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, d_out[1], c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(1)) != AXB_OK) return st;
     // vertices
@@ -1270,7 +1292,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     auto now_ms = []() { timespec t; clock_gettime(CLOCK_MONOTONIC, &t); return t.tv_sec * 1e3 + t.tv_nsec * 1e-6; };
     const double t_q = now_ms();
     double t_dim[4] = {0, 0, 0, 0};
-    c->pool->begin(stage_elems / WIDEN_PIECE + max_chunks + 8);
+    c->pool->begin(2 * (stage_elems / WIDEN_PIECE) + 2 * max_chunks + n / WIDEN_PIECE + 16);
     PoolRun run{c->pool};
     std::vector<PendingChunk> chunks;
     chunks.reserve(max_chunks);
@@ -1282,7 +1304,14 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
             cudaError_t e = block ? cudaEventSynchronize(k.ev) : cudaEventQuery(k.ev);
             if (e == cudaErrorNotReady) return AXB_OK;
             if (e != cudaSuccess) return fail(c, AXB_ERR_CUDA, "D2H chunk failed: %s", cudaGetErrorString(e));
-            c->pool->publish(k.src, k.dst, k.n, WIDEN_PIECE);
+            if (k.dim == 1 && compact1)
+                c->pool->publish(axb::WK_EDGE_ROWS, k.src, k.dst, k.n, WIDEN_PIECE, 1, 2,
+                                 reinterpret_cast<const uint32_t *>(c->h_stage + stage_offsets[1]), n, k.row0);
+            else if (k.dim == 2 && compact2)
+                c->pool->publish(axb::WK_TRI_ROWS, k.src, k.dst, k.n, WIDEN_PIECE / 2, 2, 3,
+                                 reinterpret_cast<const uint32_t *>(c->h_stage + stage_offsets[2]), n, k.row0);
+            else
+                c->pool->publish(axb::WK_WIDEN, k.src, k.dst, k.n, WIDEN_PIECE, 1, 1, nullptr, 0, 0);
             ++pumped;
         }
         return AXB_OK;
@@ -1303,18 +1332,34 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
                         d, (long long)c->counts[d], (long long)c->host_cap[d]);
         }
         if (h[d] && c->counts[d]) {
-            const size_t elems = (size_t)c->counts[d] * (d + 1);
+            if (d == 0 && c->counts[0] == (int64_t)n) {       // every vertex kept: 0, 1, ..., n - 1
+                c->pool->publish(axb::WK_IOTA, nullptr, h[0], n, WIDEN_PIECE, 0, 1, nullptr, 0, 0);
+                continue;
+            }
+            const size_t rows = (size_t)c->counts[d];
+            const size_t w = (size_t)wire_width[d];
+            const size_t rows_per_chunk = std::max<size_t>(1, D2H_CHUNK / w);
             int32_t *stage = c->h_stage + stage_off[d];
+            const bool compact = (d == 1 && compact1) || (d == 2 && compact2);
+            if (compact) {                                    // the row offsets per owner were final before the count was
+                const uint32_t *off = d == 1 ? c->off1 : c->off2;
+                CUDA_TRY(c, cudaMemcpyAsync(c->h_stage + stage_offsets[d], off, (n + 1) * sizeof(uint32_t),
+                                            cudaMemcpyDeviceToHost, c->copy_stream));
+                c->last_d2h_bytes += (int64_t)((n + 1) * sizeof(uint32_t));
+            }
             CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->dim_ready[d], 0));
-            for (size_t lo = 0; lo < elems; lo += D2H_CHUNK) {
-                const size_t m = std::min(D2H_CHUNK, elems - lo);
+            for (size_t lo = 0; lo < rows; lo += rows_per_chunk) {
+                const size_t m = std::min(rows_per_chunk, rows - lo);
                 if (chunks.size() >= c->chunk_ev.size()) return fail(c, AXB_ERR_INTERNAL, "chunk event pool exhausted");
                 cudaEvent_t ev = c->chunk_ev[chunks.size()];
-                CUDA_TRY(c, cudaMemcpyAsync(stage + lo, d_out[d] + lo, m * sizeof(int32_t), cudaMemcpyDeviceToHost, c->copy_stream));
+                CUDA_TRY(c, cudaMemcpyAsync(stage + lo * w, d_out[d] + lo * w, m * w * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                            c->copy_stream));
                 CUDA_TRY(c, cudaEventRecord(ev, c->copy_stream));
-                chunks.push_back(PendingChunk{ev, stage + lo, h[d] + lo, m});
+                // plain dimensions are widened value by value, edges / triangles row by row
+                if (compact) chunks.push_back(PendingChunk{ev, stage + lo * w, h[d] + lo * (d + 1), m, d, lo});
+                else chunks.push_back(PendingChunk{ev, stage + lo * w, h[d] + lo * w, m * w, d, 0});
             }
-            c->last_d2h_bytes += (int64_t)(elems * sizeof(int32_t));
+            c->last_d2h_bytes += (int64_t)(rows * w * sizeof(int32_t));
         }
     }
     if ((st = pump(true)) != AXB_OK) return st;

@@ -120,7 +120,8 @@ __device__ __forceinline__ int64_t mapped(const int64_t *__restrict__ map, int v
 // PCIe bytes, widened to int64 by host threads while the next chunk is in flight).
 // `total_dev` (optional) = device-side row count (the last entry of the offset array): lets the caller
 // launch without knowing the count on the host.
-template <class OutT>
+// SKIP0: write only the columns after the owner (the host rebuilds column 0 from the offsets)
+template <class OutT, bool SKIP0 = false>
 __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                     unsigned total, const uint32_t *__restrict__ total_dev,
                                                     const int64_t *__restrict__ map, OutT *__restrict__ out, Counters *ctr) {
@@ -134,12 +135,16 @@ __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp
         if (b < me.y) ++pos;
         else if (b == me.y && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
-    out[2 * (size_t)pos] = (OutT)mapped(map, me.x);
-    out[2 * (size_t)pos + 1] = (OutT)mapped(map, me.y);
+    if (SKIP0) {
+        out[pos] = (OutT)mapped(map, me.y);
+    } else {
+        out[2 * (size_t)pos] = (OutT)mapped(map, me.x);
+        out[2 * (size_t)pos + 1] = (OutT)mapped(map, me.y);
+    }
     }
 }
 
-template <class OutT>
+template <class OutT, bool SKIP0 = false>
 __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                    unsigned total, const uint32_t *__restrict__ total_dev,
                                                    const int64_t *__restrict__ map, OutT *__restrict__ out, Counters *ctr) {
@@ -153,9 +158,14 @@ __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp,
         if (o.y < me.y || (o.y == me.y && o.z < me.z)) ++pos;
         else if (o.y == me.y && o.z == me.z && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
-    out[3 * (size_t)pos] = (OutT)mapped(map, me.x);
-    out[3 * (size_t)pos + 1] = (OutT)mapped(map, me.y);
-    out[3 * (size_t)pos + 2] = (OutT)mapped(map, me.z);
+    if (SKIP0) {
+        out[2 * (size_t)pos] = (OutT)mapped(map, me.y);
+        out[2 * (size_t)pos + 1] = (OutT)mapped(map, me.z);
+    } else {
+        out[3 * (size_t)pos] = (OutT)mapped(map, me.x);
+        out[3 * (size_t)pos + 1] = (OutT)mapped(map, me.y);
+        out[3 * (size_t)pos + 2] = (OutT)mapped(map, me.z);
+    }
     }
 }
 

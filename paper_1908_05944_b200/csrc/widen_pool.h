@@ -12,6 +12,7 @@
 
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 #include <condition_variable>
 #include <mutex>
@@ -24,10 +25,23 @@
 
 namespace axb {
 
+// What a task produces (dst is always int64):
+//   WIDEN     n values copied 1:1
+//   EDGE_ROWS rows [row0, row0 + n) of the edge list: (owner, src[r]); owner of row r = the ball a with
+//             off[a] <= r < off[a + 1]  (the rows are sorted by their first column, so the device sends
+//             only the second column plus the n_index + 1 offsets -- 4 instead of 8 bytes per edge)
+//   TRI_ROWS  same for triangles: (owner, src[2r], src[2r + 1]) -- 8 instead of 12 bytes per triangle
+//   IOTA      n consecutive values starting at row0 (all vertices kept: nothing crosses PCIe)
+enum WidenKind { WK_WIDEN = 0, WK_EDGE_ROWS = 1, WK_TRI_ROWS = 2, WK_IOTA = 3 };
+
 struct WidenTask {
     const int32_t *src;
     int64_t *dst;
     size_t n;
+    int kind;
+    const uint32_t *off;      // EDGE_ROWS / TRI_ROWS: row offsets per owner (n_index + 1 entries)
+    size_t n_index;
+    size_t row0;
 };
 
 #if defined(__x86_64__)
@@ -52,6 +66,122 @@ inline void widen_rows(const int32_t *src, int64_t *dst, size_t n) {
     if (have_avx2) { widen_avx2(src, dst, n); return; }
 #endif
     for (size_t i = 0; i < n; ++i) dst[i] = src[i];
+}
+
+inline void stream_i64(int64_t *p, int64_t v) {
+#if defined(__x86_64__)
+    _mm_stream_si64(reinterpret_cast<long long *>(p), (long long)v);
+#else
+    *p = v;
+#endif
+}
+
+// owner of row r: the last a with off[a] <= r (owners without rows share their successor's offset)
+inline size_t owner_of_row(const uint32_t *off, size_t n_index, size_t r) {
+    size_t lo = 0, hi = n_index;                 // invariant: off[lo] <= r < off[hi]
+    while (hi - lo > 1) {
+        const size_t mid = (lo + hi) >> 1;
+        if (off[mid] <= r) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// owner column of rows [row0, row0 + m) into tmp (runs of equal values: ~4 rows per owner)
+inline void fill_owners(const uint32_t *off, size_t n_index, size_t row0, size_t m, int32_t *tmp) {
+    size_t a = owner_of_row(off, n_index, row0);
+    size_t k = 0;
+    while (k < m) {
+        const size_t end = std::min<size_t>(off[a + 1], row0 + m) - row0;    // rows of owner a inside the block
+        for (; k < end; ++k) tmp[k] = (int32_t)a;
+        ++a;
+    }
+}
+
+#if defined(__x86_64__)
+// (owner, b) -> int64 rows, 4 rows per iteration
+__attribute__((target("avx2"))) inline void interleave2_avx2(const int32_t *own, const int32_t *b, int64_t *dst, size_t m) {
+    size_t k = 0;
+    if (reinterpret_cast<uintptr_t>(dst) & 31u) {                 // rows are 16 bytes: at most one scalar row to align
+        if (m) { dst[0] = own[0]; dst[1] = b[0]; k = 1; }
+    }
+    for (; k + 4 <= m; k += 4) {
+        const __m256i o = _mm256_cvtepi32_epi64(_mm_loadu_si128(reinterpret_cast<const __m128i *>(own + k)));   // o0 o1 o2 o3
+        const __m256i v = _mm256_cvtepi32_epi64(_mm_loadu_si128(reinterpret_cast<const __m128i *>(b + k)));     // b0 b1 b2 b3
+        const __m256i lo = _mm256_unpacklo_epi64(o, v);           // o0 b0 o2 b2
+        const __m256i hi = _mm256_unpackhi_epi64(o, v);           // o1 b1 o3 b3
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + 2 * k), _mm256_permute2x128_si256(lo, hi, 0x20));       // o0 b0 o1 b1
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + 2 * k + 4), _mm256_permute2x128_si256(lo, hi, 0x31));   // o2 b2 o3 b3
+    }
+    for (; k < m; ++k) { dst[2 * k] = own[k]; dst[2 * k + 1] = b[k]; }
+}
+
+// (owner, b, c) -> int64 rows, 4 rows (12 values, three 32-byte stores) per iteration
+__attribute__((target("avx2"))) inline void interleave3_avx2(const int32_t *own, const int32_t *bc, int64_t *dst, size_t m) {
+    size_t k = 0;
+    while (k < m && (reinterpret_cast<uintptr_t>(dst + 3 * k) & 31u)) {   // 24-byte rows: aligned again after at most 3 rows
+        dst[3 * k] = own[k]; dst[3 * k + 1] = bc[2 * k]; dst[3 * k + 2] = bc[2 * k + 1];
+        ++k;
+    }
+    for (; k + 4 <= m; k += 4) {
+        const __m256i o = _mm256_cvtepi32_epi64(_mm_loadu_si128(reinterpret_cast<const __m128i *>(own + k)));        // a0 a1 a2 a3
+        const __m256i p = _mm256_cvtepi32_epi64(_mm_loadu_si128(reinterpret_cast<const __m128i *>(bc + 2 * k)));     // b0 c0 b1 c1
+        const __m256i q = _mm256_cvtepi32_epi64(_mm_loadu_si128(reinterpret_cast<const __m128i *>(bc + 2 * k + 4))); // b2 c2 b3 c3
+        // v0 = a0 b0 c0 a1 ; v1 = b1 c1 a2 b2 ; v2 = c2 a3 b3 c3
+        const __m256i v0 = _mm256_blend_epi32(_mm256_permute4x64_epi64(o, 0x40 /* a0 a0 a0 a1 */),
+                                              _mm256_permute4x64_epi64(p, 0x10 /* b0 b0 c0 b0 */), 0x3c);
+        const __m256i v1 = _mm256_blend_epi32(_mm256_blend_epi32(_mm256_permute4x64_epi64(p, 0x0e /* b1 c1 b0 b0 */),
+                                                                 _mm256_permute4x64_epi64(o, 0x20 /* a0 a0 a2 a0 */), 0x30),
+                                              _mm256_permute4x64_epi64(q, 0x00 /* b2 b2 b2 b2 */), 0xc0);
+        const __m256i v2 = _mm256_blend_epi32(_mm256_permute4x64_epi64(q, 0xe5 /* c2 c2 b3 c3 */),
+                                              _mm256_permute4x64_epi64(o, 0x0c /* a0 a3 a0 a0 */), 0x0c);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + 3 * k), v0);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + 3 * k + 4), v1);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + 3 * k + 8), v2);
+    }
+    for (; k < m; ++k) { dst[3 * k] = own[k]; dst[3 * k + 1] = bc[2 * k]; dst[3 * k + 2] = bc[2 * k + 1]; }
+}
+#endif
+
+inline void interleave_rows(int width, const int32_t *own, const int32_t *src, int64_t *dst, size_t m) {
+#if defined(__x86_64__)
+    static const bool have_avx2 = __builtin_cpu_supports("avx2");
+    if (have_avx2) {
+        if (width == 2) interleave2_avx2(own, src, dst, m); else interleave3_avx2(own, src, dst, m);
+        return;
+    }
+#endif
+    if (width == 2) {
+        for (size_t k = 0; k < m; ++k) { dst[2 * k] = own[k]; dst[2 * k + 1] = src[k]; }
+    } else {
+        for (size_t k = 0; k < m; ++k) { dst[3 * k] = own[k]; dst[3 * k + 1] = src[2 * k]; dst[3 * k + 2] = src[2 * k + 1]; }
+    }
+}
+
+inline void run_task(const WidenTask &t) {
+    switch (t.kind) {
+    case WK_WIDEN:
+        widen_rows(t.src, t.dst, t.n);
+        break;
+    case WK_IOTA:
+        for (size_t i = 0; i < t.n; ++i) stream_i64(t.dst + i, (int64_t)(t.row0 + i));
+        break;
+    case WK_EDGE_ROWS:
+    case WK_TRI_ROWS: {
+        // blocks of 2,048 rows: owner column into a cache-resident buffer, then a vectorised interleave
+        constexpr size_t BLOCK = 2048;
+        int32_t own[BLOCK];
+        const int width = t.kind == WK_EDGE_ROWS ? 2 : 3;
+        for (size_t lo = 0; lo < t.n; lo += BLOCK) {
+            const size_t m = std::min(BLOCK, t.n - lo);
+            fill_owners(t.off, t.n_index, t.row0 + lo, m, own);
+            interleave_rows(width, own, t.src + lo * (width - 1), t.dst + lo * width, m);
+        }
+        break;
+    }
+    }
+#if defined(__x86_64__)
+    _mm_sfence();
+#endif
 }
 
 class WidenPool {
@@ -83,11 +213,14 @@ public:
         }
         cv_.notify_all();
     }
-    // split [src, src + n) into pieces and publish them (producer thread only)
-    void publish(const int32_t *src, int64_t *dst, size_t n, size_t piece) {
+    // split n items (values or rows) into pieces and publish them (producer thread only);
+    // src_width / dst_width = int32 values per item in src / int64 values per item in dst
+    void publish(int kind, const int32_t *src, int64_t *dst, size_t n, size_t piece, int src_width, int dst_width,
+                 const uint32_t *off, size_t n_index, size_t row0) {
         size_t p = published_.load(std::memory_order_relaxed);
         for (size_t lo = 0; lo < n && p < tasks_.size(); lo += piece) {
-            tasks_[p++] = WidenTask{src + lo, dst + lo, n - lo < piece ? n - lo : piece};
+            tasks_[p++] = WidenTask{src ? src + lo * src_width : nullptr, dst + lo * dst_width, n - lo < piece ? n - lo : piece,
+                                    kind, off, n_index, row0 + lo};
             published_.store(p, std::memory_order_release);
         }
     }
@@ -111,7 +244,7 @@ private:
         while (i < published_.load(std::memory_order_acquire)) {
             if (next_.compare_exchange_weak(i, i + 1, std::memory_order_acq_rel)) {
                 const WidenTask t = tasks_[i];
-                widen_rows(t.src, t.dst, t.n);
+                run_task(t);
                 done_.fetch_add(1, std::memory_order_release);
                 return true;
             }

@@ -346,6 +346,29 @@ def test_sparse_grid_mode(monkeypatch):
         ax.compute_alpha_complex_arrays(dup, np.array([1, 1, 1.5]), ax.PipelineConfig(alpha=0.0))
 
 
+def test_compact_wire_formats_of_the_host_path(monkeypatch):
+    """AXB_WIRE=3: edges / triangles cross PCIe without their owner column and are rebuilt by the host
+    threads from the per-owner offsets; the int64 arrays must be identical to the default format."""
+    eng = ax.default_engine()
+    c, r = synth.jittered_lattice(120_000, 5)
+    cfg = ax.PipelineConfig(alpha=0.7)
+    plain = eng.compute_host(c, r, cfg)
+    for mode in ("1", "2", "3"):
+        monkeypatch.setenv("AXB_WIRE", mode)
+        compact = eng.compute_host(c, r, cfg)
+        for a, b in zip(plain, compact):
+            assert a.dtype == np.int64 and np.array_equal(a, b), f"AXB_WIRE={mode}"
+    monkeypatch.delenv("AXB_WIRE")
+    # vertices dropped by the general vertex step (not every vertex kept): the plain int32 path for dimension 0
+    rng = np.random.default_rng(3)
+    c2 = rng.uniform(0, 30, size=(3000, 3))
+    r2 = rng.uniform(0.1, 2.5, size=3000)
+    k = ax.compute_alpha_complex_arrays(c2, r2, ax.PipelineConfig(alpha=0.0, tolerance=ax.TolerancePolicy(1e-9, 1e-300)))
+    ref = oracle.compute(c2, r2, 0.0, eps_singular=1e-300, threads=os.cpu_count(), chunk=64)
+    assert ref.status == oracle.OK and k.vertices.shape[0] < 3000
+    assert_same_complex(k, ref, "engulfed vertices")
+
+
 def test_pipelined_host_path_equals_two_call_path():
     eng = ax.default_engine()
     cases = [(synth.jittered_lattice(120_000, 3), 0.0, 1e-300),
