@@ -392,18 +392,21 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
 #define AXB_T3 1
 #endif
 #if AXB_T3
-    {   // warp-autonomous tiles (estimate3.cuh)
+    {   // warp-autonomous tiles (estimate3.cuh); the tile shape follows the work per generator
         CUDA_TRY(c, cudaMemsetAsync(&c->ctr->tile_next, 0, sizeof(unsigned int), c->stream));
-        const unsigned nblocks = (unsigned)std::max(1, (ngen + T3_GENS * T3_WARPS - 1) / (T3_GENS * T3_WARPS));
-        if (c->W == 1) {
-            const size_t smem = sizeof(T3Warp<1>) * T3_WARPS;
-            CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_tri_tet3<1><<<std::min(nblocks, (unsigned)c->sm_count * (unsigned)T3_MINB), T3_WARPS * 32, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
-        } else {
-            const size_t smem = sizeof(T3Warp<4>) * T3_WARPS;
-            CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet3<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_tri_tet3<4><<<std::min(nblocks, (unsigned)c->sm_count * 2u), T3_WARPS * 32, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
-        }
+        auto launch = [&](auto kernel, size_t warp_bytes, int gens, int minb) -> int {
+            const size_t smem = warp_bytes * T3_WARPS;
+            const unsigned nblocks = (unsigned)std::max(1, (ngen + gens * T3_WARPS - 1) / (gens * T3_WARPS));
+            CUDA_TRY(c, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            kernel<<<std::min(nblocks, (unsigned)c->sm_count * (unsigned)minb), T3_WARPS * 32, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
+            return AXB_OK;
+        };
+        int st;
+        const bool heavy = c->h->ctr.pair_bound > 20ull * (unsigned long long)std::max(ngen, 1);   // > 20 partner pairs per generator
+        if (c->W != 1) st = launch(k_tri_tet3<4, T3_LIGHT>, sizeof(T3Warp<4, T3_LIGHT>), T3Cfg<4, T3_LIGHT>::GENS, 1);
+        else if (heavy) st = launch(k_tri_tet3<1, T3_HEAVY>, sizeof(T3Warp<1, T3_HEAVY>), T3Cfg<1, T3_HEAVY>::GENS, T3Cfg<1, T3_HEAVY>::MINB);
+        else st = launch(k_tri_tet3<1, T3_LIGHT>, sizeof(T3Warp<1, T3_LIGHT>), T3Cfg<1, T3_LIGHT>::GENS, T3Cfg<1, T3_LIGHT>::MINB);
+        if (st != AXB_OK) return st;
         LAUNCH_CHECK(c);
         return AXB_OK;
     }

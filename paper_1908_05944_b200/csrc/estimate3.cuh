@@ -32,23 +32,26 @@ namespace axb {
 #ifndef T3_WARPS_V
 #define T3_WARPS_V 4
 #endif
-#ifndef T3_MINB
-#define T3_MINB 4
-#endif
 constexpr int T3_WARPS = T3_WARPS_V;      // warps per block (each one is independent)
-constexpr int T3_GENS = 16;               // generators per warp tile
+// Tile shapes (template parameter SHAPE): the light shape packs lanes best when a generator has ~11 partner
+// pairs (alpha = 0); the heavy shape halves the tile so that 24 instead of 16 warps fit an SM (80 registers,
+// 6.5 KB of shared memory per warp) -- measured 8-10 % faster once generators have 40+ pairs (alpha = 1.4,
+// dense cores), 9 % slower at alpha = 0.
+enum { T3_LIGHT = 0, T3_HEAVY = 1 };
 constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved as soon as 256 are waiting)
 
-template <int W>
+template <int W, int SHAPE>
 struct T3Cfg {
-    static constexpr int SCAP = W == 1 ? 128 : 256;     // partner slots per sub-pass (>= 64 * W: one generator always fits)
-    static constexpr int TCAP = W == 1 ? 224 : 512;     // triangles per round
-    static constexpr int NA = SCAP + T3_GENS;           // atom index space: partner slots, then the tile's generators
+    static constexpr int GENS = (W == 1 && SHAPE == T3_HEAVY) ? 8 : 16;                      // generators per warp tile (<= 16)
+    static constexpr int SCAP = W == 1 ? (SHAPE == T3_HEAVY ? 64 : 128) : 256;   // partner slots per sub-pass (>= 64 * W)
+    static constexpr int TCAP = W == 1 ? (SHAPE == T3_HEAVY ? 112 : 224) : 512;  // triangles per round
+    static constexpr int MINB = W == 1 ? (SHAPE == T3_HEAVY ? 6 : 4) : 1;        // resident blocks per SM the registers must allow
+    static constexpr int NA = SCAP + GENS;              // atom index space: partner slots, then the tile's generators
 };
 
-template <int W>
+template <int W, int SHAPE>
 struct T3Warp {
-    using C = T3Cfg<W>;
+    using C = T3Cfg<W, SHAPE>;
     double ax[C::NA], ay[C::NA], az[C::NA], ar2[C::NA];
     double sreach[C::SCAP];
     unsigned long long M[C::SCAP * W];
@@ -57,9 +60,9 @@ struct T3Warp {
     int aorig[C::NA];
     int srank[C::SCAP];
     int rowpre[C::SCAP + 1];
-    int gdeg[T3_GENS];
-    unsigned gadj[T3_GENS];
-    int sp[T3_GENS + 1];                       // slot prefix over the whole tile
+    int gdeg[C::GENS];
+    unsigned gadj[C::GENS];
+    int sp[C::GENS + 1];                       // slot prefix over the whole tile
     union {
         unsigned wq[T3_WQCAP];                 // phase B: queue of reach-passing pairs (slot i | slot j << 16)
         struct {
@@ -86,8 +89,8 @@ __device__ __forceinline__ int warp_scan_excl(int *a, int n) {
     return carry;
 }
 
-template <int W>
-__device__ __forceinline__ Atom atom_at(const T3Warp<W> &S, int a) {
+template <class SW>
+__device__ __forceinline__ Atom atom_at(const SW &S, int a) {
     Atom p;
     p.x = S.ax[a]; p.y = S.ay[a]; p.z = S.az[a]; p.r2 = S.ar2[a];
     return p;
@@ -98,15 +101,15 @@ __device__ __forceinline__ void cswap_idx(int &oa, int &ia, int &ob, int &ib) {
 }
 
 // ortho solves on atoms named by their shared-memory index: sort (ball index, slot) pairs, then load in order
-template <int W>
-__device__ __forceinline__ Ortho ortho_edge_s(const T3Warp<W> &S, int a, int b, double eps_sing) {
+template <class SW>
+__device__ __forceinline__ Ortho ortho_edge_s(const SW &S, int a, int b, double eps_sing) {
     int oa = S.aorig[a], ob = S.aorig[b];
     cswap_idx(oa, a, ob, b);
     return ortho2(atom_at(S, a), atom_at(S, b), eps_sing);
 }
 
-template <int W>
-__device__ __forceinline__ Ortho ortho_tri_s(const T3Warp<W> &S, int a, int b, int c, double eps_sing) {
+template <class SW>
+__device__ __forceinline__ Ortho ortho_tri_s(const SW &S, int a, int b, int c, double eps_sing) {
     int oa = S.aorig[a], ob = S.aorig[b], oc = S.aorig[c];
     cswap_idx(oa, a, ob, b);
     cswap_idx(ob, b, oc, c);
@@ -115,8 +118,8 @@ __device__ __forceinline__ Ortho ortho_tri_s(const T3Warp<W> &S, int a, int b, i
     return orthoN<3>(p, eps_sing);
 }
 
-template <int W>
-__device__ __forceinline__ Ortho ortho_tet_s(const T3Warp<W> &S, int a, int b, int c, int d, double eps_sing) {
+template <class SW>
+__device__ __forceinline__ Ortho ortho_tet_s(const SW &S, int a, int b, int c, int d, double eps_sing) {
     int oa = S.aorig[a], ob = S.aorig[b], oc = S.aorig[c], od = S.aorig[d];
     cswap_idx(oa, a, ob, b);
     cswap_idx(oc, c, od, d);
@@ -133,8 +136,8 @@ __device__ __forceinline__ Ortho ortho_tet_s(const T3Warp<W> &S, int a, int b, i
 // one cell side to the centre (pipeline.py:288-289), so it is one of the 27-cell candidates, and the
 // power distance below is evaluated exactly like pipeline.py:308-309.  The partners are already in
 // shared memory, so most dominated simplices are settled here and never reach the AC2 kernels.
-template <int W>
-__device__ __forceinline__ bool dominated_by_partner3(const T3Warp<W> &S, int sb, int se, int s0, int s1, int s2,
+template <class SW>
+__device__ __forceinline__ bool dominated_by_partner3(const SW &S, int sb, int se, int s0, int s1, int s2,
                                                       double cx, double cy, double cz, double thr) {
     for (int s = sb; s < se; ++s) {
         if (s == s0 || s == s1 || s == s2) continue;
@@ -145,14 +148,15 @@ __device__ __forceinline__ bool dominated_by_partner3(const T3Warp<W> &S, int sb
     return false;
 }
 
-template <int W>
-__global__ void __launch_bounds__(T3_WARPS * 32, T3_MINB) k_tri_tet3(EstParams P, int rank_lo, int rank_hi) {
-    using C = T3Cfg<W>;
+template <int W, int SHAPE>
+__global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_tet3(EstParams P, int rank_lo, int rank_hi) {
+    using C = T3Cfg<W, SHAPE>;
+    constexpr int T3_GENS = C::GENS;
     constexpr int PCAP = 64 * W;
     constexpr int SCAP = C::SCAP, TCAP = C::TCAP;
     extern __shared__ __align__(16) unsigned char s_raw3[];
     const int warp = threadIdx.x >> 5, lane = lane_id();
-    T3Warp<W> &S = reinterpret_cast<T3Warp<W> *>(s_raw3)[warp];
+    T3Warp<W, SHAPE> &S = reinterpret_cast<T3Warp<W, SHAPE> *>(s_raw3)[warp];
     const int ntiles = (rank_hi - rank_lo + T3_GENS - 1) / T3_GENS;
 
     // Tiles are claimed from a global counter (dense regions make tiles very unequal); the claim for the
