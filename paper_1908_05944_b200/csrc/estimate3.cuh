@@ -96,6 +96,11 @@ __device__ __forceinline__ Atom atom_at(const SW &S, int a) {
     return p;
 }
 
+// bit j of a row of 64-bit words, as a native 32-bit shared-memory atomic (little endian: word j >> 5)
+__device__ __forceinline__ void set_bit(unsigned long long *row, int j) {
+    atomicOr(reinterpret_cast<unsigned int *>(row) + (j >> 5), 1u << (j & 31));
+}
+
 __device__ __forceinline__ void cswap_idx(int &oa, int &ia, int &ob, int &ib) {
     if (oa > ob) { int t = oa; oa = ob; ob = t; t = ia; ia = ib; ib = t; }
 }
@@ -237,17 +242,17 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                                 const Ortho e2 = ortho_edge_s(S, si, sj, P.tol.eps_sing);                // pipeline.py:412-414
                                 if (e2.singular) record_singular(P, make_err_key(ST_VW, t, q), S.aorig[si], S.aorig[sj], -1, -1, 2);
                                 if (e2.size <= P.tol.lim_a) {                                            // pipeline.py:415
-                                    atomicOr(&S.M[si * W + (j >> 6)], 1ull << (j & 63));
-                                    atomicOr(&S.M[sj * W + (i >> 6)], 1ull << (i & 63));
+                                    set_bit(&S.M[si * W], j);
+                                    set_bit(&S.M[sj * W], i);
                                     const Ortho e3 = ortho_tri_s(S, SCAP + g, si, sj, P.tol.eps_sing);   // pipeline.py:417-419
                                     if (e3.singular)
                                         record_singular(P, make_err_key(ST_TRI, t, q), S.aorig[SCAP + g], S.aorig[si], S.aorig[sj], -1, 3);
                                     if (e3.size <= P.tol.lim_a) {                                        // pipeline.py:420
-                                        atomicOr(&S.T[si * W + (j >> 6)], 1ull << (j & 63));
+                                        set_bit(&S.T[si * W], j);
                                         if (P.cull & 2) {
                                             const int sb = S.sp[g] - base;
                                             if (dominated_by_partner3(S, sb, sb + d, si, sj, -1, e3.cx, e3.cy, e3.cz, e3.size - P.tol.eps_abs))
-                                                atomicOr(&S.D[si * W + (j >> 6)], 1ull << (j & 63));
+                                                set_bit(&S.D[si * W], j);
                                         }
                                     }
                                 }
