@@ -37,7 +37,8 @@ from .pipeline import (
     compute_alpha_complex_arrays,
     default_engine,
 )
-from .io import read_complex, stats_csv, write_complex
+from .io import (format_xyzr, format_xyzr_arrays, parse_xyzr, parse_xyzr_arrays, read_complex, stats_csv,
+                 write_complex)
 from .stages import (CellKey, Grid, PotentialLevel, PotentialSets, build_grid, potential_edges, potential_tets,
                      potential_triangles, prune)
 from . import synth
@@ -49,5 +50,6 @@ __all__ = [
     "STAGE_NAMES", "SimplexKey", "TolerancePolicy", "as_ball_arrays", "closure_ok", "complex_stats",
     "compute_alpha_complex", "compute_alpha_complex_arrays", "default_engine", "simplex_compare", "synth",
     "CellKey", "Grid", "PotentialLevel", "PotentialSets", "build_grid", "potential_edges", "potential_triangles",
-    "potential_tets", "prune", "read_complex", "stats_csv", "write_complex",
+    "potential_tets", "prune", "read_complex", "stats_csv", "write_complex", "parse_xyzr", "parse_xyzr_arrays",
+    "format_xyzr", "format_xyzr_arrays",
 ]
