@@ -57,6 +57,8 @@ struct axb_ctx {
     // host path: rows cross PCIe as int32 into this pinned staging area and are widened by the pool
     int32_t *h_stage = nullptr;
     size_t h_stage_elems = 0;
+    char *h_in = nullptr;                   // pinned staging area for pageable inputs
+    size_t h_in_bytes = 0;
     axb::WidenPool *pool = nullptr;
     std::vector<cudaEvent_t> chunk_ev;
     int64_t last_d2h_bytes = 0;
@@ -526,6 +528,7 @@ extern "C" void axb_ctx_destroy(axb_ctx *c) {
     for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->h_in) cudaFreeHost(c->h_in);
     if (c->h) cudaFreeHost(c->h);
     delete c;
 }
@@ -1073,6 +1076,77 @@ extern "C" int axb_compute_slab(axb_ctx *c, int64_t n, const double *d_xyz, cons
     return st;
 }
 
+namespace {
+
+int ensure_pool(axb_ctx *c) {
+    if (c->pool) return AXB_OK;
+    unsigned hw = std::thread::hardware_concurrency();
+    // the calling thread helps too; two cores stay free for the CUDA driver's own threads (measured:
+    // 14 of 16 beats 16 of 16, which gets preempted in the middle of tasks)
+    unsigned workers = std::max(3u, std::min(32u, hw ? hw : 4u)) - 3u;
+    if (const char *e = getenv("AXB_WIDEN_THREADS")) workers = (unsigned)std::max(0, atoi(e) - 1);
+    c->pool = new (std::nothrow) axb::WidenPool(workers);
+    if (!c->pool) return fail(c, AXB_ERR_INTERNAL, "cannot create the host worker threads");
+    return AXB_OK;
+}
+
+bool is_pinned(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return at.type != cudaMemoryTypeUnregistered;
+}
+
+// Inputs to the device.  Pinned buffers go straight to the copy engine.  Pageable ones (a plain numpy array)
+// would make the driver stage them through its own bounce buffer on ONE thread (~10 GB/s: 3 ms per million
+// balls); instead the host threads copy them into a pinned staging area in 8 MiB slices and each slice is handed to
+// the copy engine as soon as it is complete, so the DMA of one slice overlaps the memcpy of the next.
+int upload_inputs(axb_ctx *c, int64_t n, const double *h_xyz, const double *h_radii, double *d_in) {
+    const size_t bx = (size_t)n * 3 * sizeof(double), br = (size_t)n * sizeof(double);
+    if (is_pinned(h_xyz) && is_pinned(h_radii)) {
+        CUDA_TRY(c, cudaMemcpyAsync(d_in, h_xyz, bx, cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(c, cudaMemcpyAsync(d_in + 3 * (size_t)n, h_radii, br, cudaMemcpyHostToDevice, c->stream));
+        return AXB_OK;
+    }
+    int st = ensure_pool(c);
+    if (st != AXB_OK) return st;
+    if (c->h_in_bytes < bx + br) {
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));      // a previous upload may still read the old area
+        if (c->h_in) cudaFreeHost(c->h_in);
+        c->h_in = nullptr;
+        c->h_in_bytes = 0;
+        const size_t want = (bx + br) + (bx + br) / 4;
+        CUDA_TRY(c, cudaHostAlloc(reinterpret_cast<void **>(&c->h_in), want, cudaHostAllocDefault));
+        c->h_in_bytes = want;
+    } else {
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));      // the area is reused: the previous run's DMA must be over
+    }
+    timespec ts0;
+    clock_gettime(CLOCK_MONOTONIC, &ts0);
+    const size_t slice = getenv("AXB_UPLOAD_SLICE") ? (size_t)atol(getenv("AXB_UPLOAD_SLICE")) : ((size_t)8 << 20);
+    const char *src[2] = {reinterpret_cast<const char *>(h_xyz), reinterpret_cast<const char *>(h_radii)};
+    const size_t len[2] = {bx, br};
+    size_t off = 0;
+    for (int part = 0; part < 2; ++part) {
+        for (size_t lo = 0; lo < len[part]; lo += slice) {
+            const size_t m = std::min(slice, len[part] - lo);
+            c->pool->begin(m / ((size_t)256 << 10) + 4);
+            c->pool->publish_copy(src[part] + lo, c->h_in + off + lo, m, (size_t)256 << 10);
+            c->pool->finish();
+            CUDA_TRY(c, cudaMemcpyAsync(reinterpret_cast<char *>(d_in) + off + lo, c->h_in + off + lo, m, cudaMemcpyHostToDevice, c->stream));
+        }
+        off += len[part];
+    }
+    if (getenv("AXB_TRACE")) {
+        timespec ts1;
+        clock_gettime(CLOCK_MONOTONIC, &ts1);
+        fprintf(stderr, "[axb] staged upload of %zu bytes queued after %.3f ms\n", bx + br,
+                (ts1.tv_sec - ts0.tv_sec) * 1e3 + (ts1.tv_nsec - ts0.tv_nsec) * 1e-6);
+    }
+    return AXB_OK;
+}
+
+}  // namespace
+
 extern "C" int axb_compute_host(axb_ctx *c, int64_t n, const double *h_xyz, const double *h_radii, const axb_params *prm,
                                 int64_t counts[4]) {
     if (!c) return AXB_ERR_BAD_ARG;
@@ -1086,8 +1160,10 @@ extern "C" int axb_compute_host(axb_ctx *c, int64_t n, const double *h_xyz, cons
     }
     double *d_in = reinterpret_cast<double *>(c->arena + c->arena_bytes - in_bytes);
     CUDA_TRY(c, cudaSetDevice(c->device));
-    CUDA_TRY(c, cudaMemcpyAsync(d_in, h_xyz, (size_t)n * 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(d_in + 3 * (size_t)n, h_radii, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    {
+        int up = upload_inputs(c, n, h_xyz, h_radii, d_in);
+        if (up != AXB_OK) return up;
+    }
     const size_t full = c->arena_bytes;
     c->arena_bytes = full - in_bytes;
     int st = axb_compute(c, n, d_in, d_in + 3 * (size_t)n, prm, counts);
@@ -1113,16 +1189,22 @@ extern "C" int axb_compute_host_begin(axb_ctx *c, int64_t n, const double *h_xyz
     }
     double *d_in = reinterpret_cast<double *>(c->arena + c->arena_bytes - in_bytes);
     CUDA_TRY(c, cudaSetDevice(c->device));
-    CUDA_TRY(c, cudaMemcpyAsync(d_in, h_xyz, (size_t)n * 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(d_in + 3 * (size_t)n, h_radii, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    {
+        int up = upload_inputs(c, n, h_xyz, h_radii, d_in);
+        if (up != AXB_OK) return up;
+    }
     const size_t full = c->arena_bytes;
     c->arena_bytes = full - in_bytes;
+    auto now_ms = []() { timespec t; clock_gettime(CLOCK_MONOTONIC, &t); return t.tv_sec * 1e3 + t.tv_nsec * 1e-6; };
+    const double tb0 = now_ms();
     int st = axb_grid_build(c, n, d_in, d_in + 3 * (size_t)n, prm);
+    const double tb1 = now_ms();
     if (st == AXB_OK) {
         c->cull = true;
         st = run_potential(c, 0, n);
         c->cull = false;
     }
+    if (getenv("AXB_TRACE")) fprintf(stderr, "[axb] begin: grid (incl. upload wait) %.3f ms, potential %.3f ms\n", tb1 - tb0, now_ms() - tb1);
     c->arena_bytes = full;
     if (st == AXB_ERR_ARENA) c->arena_needed += in_bytes;
     if (st != AXB_OK) return st;
@@ -1203,15 +1285,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
         CUDA_TRY(c, cudaHostAlloc(reinterpret_cast<void **>(&c->h_stage), want * sizeof(int32_t), cudaHostAllocDefault));
         c->h_stage_elems = want;
     }
-    if (!c->pool) {
-        unsigned hw = std::thread::hardware_concurrency();
-        // the calling thread helps too; two cores stay free for the CUDA driver's own threads (measured:
-        // 14 of 16 beats 16 of 16, which gets preempted in the middle of tasks)
-        unsigned workers = std::max(3u, std::min(32u, hw ? hw : 4u)) - 3u;
-        if (const char *e = getenv("AXB_WIDEN_THREADS")) workers = (unsigned)std::max(0, atoi(e) - 1);
-        c->pool = new (std::nothrow) axb::WidenPool(workers);
-        if (!c->pool) return fail(c, AXB_ERR_INTERNAL, "cannot create the widening threads");
-    }
+    if ((st = ensure_pool(c)) != AXB_OK) return st;
     if (const char *e = getenv("AXB_D2H_CHUNK")) D2H_CHUNK = std::max<size_t>(1 << 14, (size_t)atol(e));
     const size_t max_chunks = stage_elems / D2H_CHUNK + 8;
     while (c->chunk_ev.size() < max_chunks) {

@@ -11,6 +11,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <string.h>
 
 #include <algorithm>
 #include <atomic>
@@ -32,7 +33,8 @@ namespace axb {
 //             only the second column plus the n_index + 1 offsets -- 4 instead of 8 bytes per edge)
 //   TRI_ROWS  same for triangles: (owner, src[2r], src[2r + 1]) -- 8 instead of 12 bytes per triangle
 //   IOTA      n consecutive values starting at row0 (all vertices kept: nothing crosses PCIe)
-enum WidenKind { WK_WIDEN = 0, WK_EDGE_ROWS = 1, WK_TRI_ROWS = 2, WK_IOTA = 3 };
+//   COPY      n int32 values copied verbatim (pageable input -> pinned staging, in parallel)
+enum WidenKind { WK_WIDEN = 0, WK_EDGE_ROWS = 1, WK_TRI_ROWS = 2, WK_IOTA = 3, WK_COPY = 4 };
 
 struct WidenTask {
     const int32_t *src;
@@ -66,6 +68,31 @@ inline void widen_rows(const int32_t *src, int64_t *dst, size_t n) {
     if (have_avx2) { widen_avx2(src, dst, n); return; }
 #endif
     for (size_t i = 0; i < n; ++i) dst[i] = src[i];
+}
+
+// copy with non-temporal stores: the destination is a DMA source next, and a copy engine reading lines that
+// sit dirty in sixteen cores' caches runs at a quarter of its speed (measured 13 vs 54 GB/s)
+#if defined(__x86_64__)
+__attribute__((target("avx2"))) inline void copy_stream_avx2(const char *src, char *dst, size_t bytes) {
+    size_t i = 0;
+    while (i < bytes && (reinterpret_cast<uintptr_t>(dst + i) & 31u)) { dst[i] = src[i]; ++i; }
+    for (; i + 64 <= bytes; i += 64) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i + 32));
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i), a);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i + 32), b);
+    }
+    for (; i < bytes; ++i) dst[i] = src[i];
+    _mm_sfence();
+}
+#endif
+
+inline void copy_for_dma(const void *src, void *dst, size_t bytes) {
+#if defined(__x86_64__)
+    static const bool have_avx2 = __builtin_cpu_supports("avx2");
+    if (have_avx2) { copy_stream_avx2(static_cast<const char *>(src), static_cast<char *>(dst), bytes); return; }
+#endif
+    memcpy(dst, src, bytes);
 }
 
 inline void stream_i64(int64_t *p, int64_t v) {
@@ -165,6 +192,9 @@ inline void run_task(const WidenTask &t) {
     case WK_IOTA:
         for (size_t i = 0; i < t.n; ++i) stream_i64(t.dst + i, (int64_t)(t.row0 + i));
         break;
+    case WK_COPY:
+        copy_for_dma(t.src, t.dst, t.n * sizeof(int32_t));
+        break;
     case WK_EDGE_ROWS:
     case WK_TRI_ROWS: {
         // blocks of 2,048 rows: owner column into a cache-resident buffer, then a vectorised interleave
@@ -221,6 +251,17 @@ public:
         for (size_t lo = 0; lo < n && p < tasks_.size(); lo += piece) {
             tasks_[p++] = WidenTask{src ? src + lo * src_width : nullptr, dst + lo * dst_width, n - lo < piece ? n - lo : piece,
                                     kind, off, n_index, row0 + lo};
+            published_.store(p, std::memory_order_release);
+        }
+    }
+    // parallel memcpy of `bytes` (a multiple of 8) from src to dst in pieces of piece_bytes
+    void publish_copy(const void *src, void *dst, size_t bytes, size_t piece_bytes) {
+        size_t p = published_.load(std::memory_order_relaxed);
+        for (size_t lo = 0; lo < bytes && p < tasks_.size(); lo += piece_bytes) {
+            const size_t m = bytes - lo < piece_bytes ? bytes - lo : piece_bytes;
+            tasks_[p++] = WidenTask{reinterpret_cast<const int32_t *>(static_cast<const char *>(src) + lo),
+                                    reinterpret_cast<int64_t *>(static_cast<char *>(dst) + lo), m / sizeof(int32_t), WK_COPY,
+                                    nullptr, 0, 0};
             published_.store(p, std::memory_order_release);
         }
     }

@@ -30,6 +30,14 @@ def main():
             out = eng.compute_host(hc, hr, cfg, pipelined=mode)
             del out
         print(f"compute_host pipelined={mode}: {(time.perf_counter() - t0) * 100:.3f} ms/call")
+    # pageable inputs (a plain numpy array): staged through pinned memory by the host threads
+    for _ in range(3):
+        eng.compute_host(c, r, cfg)
+    t0 = time.perf_counter()
+    for _ in range(10):
+        out = eng.compute_host(c, r, cfg)
+        del out
+    print(f"compute_host pageable inputs: {(time.perf_counter() - t0) * 100:.3f} ms/call")
     # raw phases of the pipelined path
     lib, h = eng.lib, eng.handle
     prm = eng._params(cfg)
@@ -47,6 +55,19 @@ def main():
         tb += t1 - t0; ta += t2 - t1; tf += t3 - t2
         del outs
     print(f"begin {tb * 100:.3f} ms, pinned alloc {ta * 100:.3f} ms, finish {tf * 100:.3f} ms  caps {list(cap)} counts {list(counts)}")
+    tb = ta = tf = 0.0
+    for _ in range(10):
+        t0 = time.perf_counter()
+        assert lib.axb_compute_host_begin(h, len(r), c.ctypes.data, r.ctypes.data, C.byref(prm), cap) == 0
+        t1 = time.perf_counter()
+        outs = [torch.empty((int(cap[d]),) if d == 0 else (int(cap[d]), d + 1), dtype=torch.int64, pin_memory=True).numpy()
+                for d in range(4)]
+        t2 = time.perf_counter()
+        assert lib.axb_compute_host_finish(h, *(o.ctypes.data for o in outs), counts) == 0
+        t3 = time.perf_counter()
+        tb += t1 - t0; ta += t2 - t1; tf += t3 - t2
+        del outs
+    print(f"pageable inputs: begin {tb * 100:.3f} ms, pinned alloc {ta * 100:.3f} ms, finish {tf * 100:.3f} ms")
     # pure copies for reference
     d = torch.empty(181658136 // 8, dtype=torch.int64, device="cuda")
     hp = torch.empty(181658136 // 8, dtype=torch.int64, pin_memory=True)
