@@ -842,24 +842,19 @@ int run_potential(axb_ctx *c, int64_t lo, int64_t hi) {
 int alloc_prune_arrays(axb_ctx *c) {
     const int n = (int)c->n;
     const size_t rows = (size_t)std::max<uint32_t>(c->n_pe, 1);
+    ARENA(c, c->k3, int4, std::max<uint32_t>(c->k3_cap, 1));
+    // the zero-initialised arrays are carved back to back, so ONE memset clears them (nine tiny memsets cost
+    // ~20 us of stream time between the potential and the pruning stage)
+    const size_t zero_from = c->arena_used;
     ARENA(c, c->trimask, unsigned long long, rows * c->W);
     ARENA(c, c->eflag, unsigned int, rows);
     ARENA(c, c->vflag, unsigned char, n);
-    ARENA(c, c->k3, int4, std::max<uint32_t>(c->k3_cap, 1));
     ARENA(c, c->cnt1, uint32_t, (size_t)n + 1);
     ARENA(c, c->cnt2, uint32_t, (size_t)n + 1);
     ARENA(c, c->cnt3, uint32_t, (size_t)n + 1);
     ARENA(c, c->vkeep, uint32_t, (size_t)n + 1);
-    CUDA_TRY(c, cudaMemsetAsync(c->trimask, 0, sizeof(unsigned long long) * rows * c->W, c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->eflag, 0, sizeof(unsigned int) * rows, c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->vflag, 0, (size_t)n, c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->cnt1, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->cnt2, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->cnt3, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->vkeep, 0, sizeof(uint32_t) * ((size_t)n + 1), c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(&c->ctr->n_k3, 0, sizeof(unsigned int), c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(&c->ctr->lookup_miss, 0, sizeof(unsigned int), c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->ctr->work_next, 0, sizeof(c->ctr->work_next), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->arena + zero_from, 0, c->arena_used - zero_from, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(&c->ctr->n_k3, 0, sizeof(unsigned int) * PRUNE_COUNTER_WORDS, c->stream));
     return AXB_OK;
 }
 

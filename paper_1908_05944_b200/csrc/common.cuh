@@ -45,16 +45,18 @@ struct Counters {
     unsigned int n_pe;                 // potential edges
     unsigned int n_pt;                 // potential triangles
     unsigned int n_pq;                 // potential tets
-    unsigned int n_k3;                 // kept tets
     unsigned int max_deg;
     unsigned int err_count;            // singular records appended
     unsigned int dup_count;            // duplicate-centre records appended
     unsigned int overflow;             // bit0: partner cap, bit1: PT cap, bit2: PQ cap, bit3: lookup miss
     unsigned int first_bad;            // first non-finite ball index (0xffffffff = none)
-    unsigned int lookup_miss;          // inherited faces whose generator row has no such partner
     unsigned int tile_next;            // k_tri_tet3: next unclaimed tile (dynamic scheduling)
+    // --- the pruning stage's own counters: adjacent, zeroed with one memset per prune run
+    unsigned int n_k3;                 // kept tets
+    unsigned int lookup_miss;          // inherited faces whose generator row has no such partner
     unsigned int work_next[3];         // prune kernels (tets, triangles, edges): next unclaimed chunk
 };
+constexpr int PRUNE_COUNTER_WORDS = 5; // n_k3 .. work_next[2]
 
 constexpr int ERR_CAP = 1024;          // singular records kept per run
 constexpr int DUP_CAP = 4096;
