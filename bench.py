@@ -211,13 +211,22 @@ def bench_b200(args, rank, world, local_rank):
 
     import paper_1908_05944_b200 as ax
 
+    # developer hooks for a one-GPU box: AXB_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 and
+    # AXB_BENCH_BACKEND=gloo replaces the transport (NCCL refuses two ranks on one device), so the whole
+    # multi-rank path (slab planning, per-rank slabs, gather, merge) can be exercised and verified
+    if os.environ.get("AXB_BENCH_SAME_DEVICE") == "1":
+        local_rank = 0
+    backend = os.environ.get("AXB_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist_mod
 
         dist = dist_mod
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        else:
+            dist.init_process_group(backend)
     eng = ax.default_engine(local_rank)
     tol = ax.TolerancePolicy(1e-9, args.eps_singular)
     cfg = ax.PipelineConfig(alpha=args.alpha, tolerance=tol)
@@ -251,6 +260,14 @@ def bench_b200(args, rank, world, local_rank):
     for _ in range(args.warmup):
         outs = device_step()
     counts = tuple(int(o.shape[0]) for o in outs) if outs is not None else (0, 0, 0, 0)
+    if args.verify and job is not None and rank == 0:
+        # the merged complex of the sharded run against ONE unsharded pass over the whole input on this GPU
+        whole = eng.compute_device(torch.as_tensor(centers, device="cuda"), torch.as_tensor(radii, device="cuda"), cfg)
+        same = all(bool(torch.equal(a, b)) for a, b in zip(outs, whole))
+        print(f"[verify] {world} slabs merged == single pass over {n_total} atoms: {same}", file=sys.stderr)
+        if not same:
+            raise SystemExit("sharded result differs from the single-pass result")
+        del whole
     stage_acc = {}
     launches0 = eng.kernel_launches
     sampler = ClockSampler(local_rank)
@@ -394,6 +411,7 @@ def main():
     ap.add_argument("--alpha", type=float, default=0.0)
     ap.add_argument("--eps-singular", type=float, default=1e-12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--verify", action="store_true", help="N>1: check the merged complex against one unsharded pass on rank 0")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
