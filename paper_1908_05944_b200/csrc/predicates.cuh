@@ -254,12 +254,13 @@ __device__ __forceinline__ bool ac2_pass(const GridView &g, const Atom *__restri
             int s, e;
             row_range(g, x0, x1, y, z, s, e);
             for (int t = s; t < e; ++t) {
-                if (t == inc0 || t == inc1 || t == inc2 || t == inc3) continue;
                 const double2 *q = reinterpret_cast<const double2 *>(atoms + t);
                 double2 xy = __ldg(q), zr = __ldg(q + 1);
                 double ddx = xy.x - cx, ddy = xy.y - cy, ddz = zr.x - cz;
                 double dp = ((ddx * ddx + ddy * ddy) + ddz * ddz) - zr.y;
-                if (dp < thr) return false;
+                // incident balls are masked out (pipeline.py:306-307); they sit at dp == size > thr up to rounding, so
+                // the mask is only consulted in the rare branch
+                if (dp < thr && !(t == inc0 || t == inc1 || t == inc2 || t == inc3)) return false;
             }
         }
     }
@@ -350,10 +351,9 @@ __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__re
         for (int d = 0; d + 1 < AC2_DEPTH; ++d) { tq[d] = tq[d + 1]; aq[d] = aq[d + 1]; }
         tq[AC2_DEPTH - 1] = next();
         if (tq[AC2_DEPTH - 1] >= 0) aq[AC2_DEPTH - 1] = load_atom(atoms, tq[AC2_DEPTH - 1]);
-        if (t == inc0 || t == inc1 || t == inc2 || t == inc3) continue;
         const double ddx = a.x - cx, ddy = a.y - cy, ddz = a.z - cz;
         const double dp = ((ddx * ddx + ddy * ddy) + ddz * ddz) - a.r2;
-        if (dp < thr) return false;
+        if (dp < thr && !(t == inc0 || t == inc1 || t == inc2 || t == inc3)) return false;   // incident balls are masked (pipeline.py:306-307)
     }
     return true;
 }
