@@ -101,9 +101,11 @@ def numpy_merge(parts: list, k: int) -> np.ndarray:
 
 
 def gather_rows(local: list, dist, group=None, device="cpu"):
-    """Gather the four row lists of every rank on rank 0 (counts first, then padded rows).
+    """Gather the four row lists of every rank on rank 0: one all_gather of the counts, then every rank
+    sends its exact rows (no padding) and rank 0 receives them straight into per-rank slices of ONE
+    buffer per dimension, so the concatenation the merge needs already exists when the transfers end.
     `local` = [vertices (k0,), edges (k1,2), triangles (k2,3), tets (k3,4)] torch int64 tensors.
-    Returns on rank 0: list over dims of lists over ranks; elsewhere None."""
+    Returns on rank 0: list over dims of (m_d, d+1) tensors (rank-major concatenation); elsewhere None."""
     import torch
 
     world = dist.get_world_size(group)
@@ -112,18 +114,31 @@ def gather_rows(local: list, dist, group=None, device="cpu"):
     all_counts = [torch.empty_like(counts) for _ in range(world)]
     dist.all_gather(all_counts, counts, group=group)           # the collective on counts
     all_counts = torch.stack(all_counts).cpu().numpy()         # (world, 4)
-    gathered = []
+    # gloo (the CPU test / one-GPU developer transport) cannot send device memory: stage through the host there;
+    # NCCL sends and receives the CUDA tensors directly over NVLink
+    via_host = dist.get_backend(group) == "gloo" and str(device).startswith("cuda")
+    tdev = "cpu" if via_host else device
+    ops, bufs = [], []
     for d in range(4):
         width = d + 1
-        cap = int(all_counts[:, d].max())
-        pad = torch.zeros((max(cap, 1), width), dtype=torch.int64, device=device)
-        mine = local[d].reshape(-1, width)
-        pad[: mine.shape[0]] = mine
-        bins = [torch.empty_like(pad) for _ in range(world)] if rank == 0 else None
-        dist.gather(pad, bins, dst=0, group=group)             # the collective on rows
+        mine = local[d].reshape(-1, width).contiguous().to(tdev)
         if rank == 0:
-            gathered.append([bins[r][: int(all_counts[r, d])] for r in range(world)])
-    return gathered if rank == 0 else None
+            total = int(all_counts[:, d].sum())
+            buf = torch.empty((total, width), dtype=torch.int64, device=tdev)
+            offs = np.concatenate([[0], np.cumsum(all_counts[:, d])]).astype(np.int64)
+            buf[: mine.shape[0]] = mine
+            for r in range(1, world):
+                if all_counts[r, d]:
+                    ops.append(dist.P2POp(dist.irecv, buf[int(offs[r]): int(offs[r + 1])], r, group))
+            bufs.append(buf)
+        elif mine.shape[0]:
+            ops.append(dist.P2POp(dist.isend, mine, 0, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):                # the transfer of the rows (grouped NCCL send/recv)
+            req.wait()
+    if rank != 0:
+        return None
+    return [b.to(device) for b in bufs] if via_host else bufs
 
 
 class ShardedJob:
@@ -171,7 +186,7 @@ class ShardedJob:
         torch = self.torch
         merged = []
         for d in range(4):
-            cat = torch.cat([p.reshape(-1, d + 1) for p in parts[d]], dim=0)
+            cat = parts[d] if torch.is_tensor(parts[d]) else torch.cat([p.reshape(-1, d + 1) for p in parts[d]], dim=0)
             merged.append(self.engine.merge_rows(cat, d + 1, self.n_global))
         return merged
 

@@ -93,7 +93,7 @@ def _worker(rank, world, port, out_dir):
         local = [torch.as_tensor(a) for a in arrays(res)]
         gathered = sharding.gather_rows(local, dist, device="cpu")
         if rank == 0:
-            merged = [sharding.numpy_merge([t.numpy() for t in gathered[d]], d + 1) for d in range(4)]
+            merged = [sharding.numpy_merge([gathered[d].numpy()], d + 1) for d in range(4)]
             np.savez(os.path.join(out_dir, "merged.npz"), *merged)
         else:
             assert gathered is None
