@@ -219,6 +219,31 @@ def test_dense_blob_crowded_edge_batches_against_oracle():
         assert_same_complex(k, ref, f"dense blob alpha={alpha}")
 
 
+def test_randomised_shapes_against_oracle():
+    """tools/gpu_fuzz.py as a test: 120 small inputs of many shapes (clusters, near-lattices with ties, far-away
+    offsets, flat slabs, lines; wide radii, negative alpha, both vertex modes, both pivot thresholds): same
+    arrays, and the same DegenerateSimplex vertices where the reference raises."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("gpu_fuzz", os.path.join(os.path.dirname(GOLD), "..", "tools", "gpu_fuzz.py"))
+    fuzz = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(fuzz)
+    rng = np.random.default_rng(12345)
+    raised = 0
+    for i in range(120):
+        c, r, alpha, bio, eps_sing = fuzz.make_case(rng)
+        ref = oracle.compute(c, r, alpha, eps_singular=eps_sing, biomolecule=bio, threads=4, chunk=64)
+        cfg = ax.PipelineConfig(alpha=alpha, biomolecule_mode=bio, tolerance=ax.TolerancePolicy(1e-9, eps_sing))
+        if ref.status == oracle.DEGENERATE:
+            raised += 1
+            with pytest.raises(ax.DegenerateSimplex) as info:
+                ax.compute_alpha_complex_arrays(c, r, cfg)
+            assert tuple(info.value.vertices) == tuple(ref.error_vertices), f"case {i}"
+        else:
+            assert ref.status == oracle.OK
+            assert_same_complex(ax.compute_alpha_complex_arrays(c, r, cfg), ref, f"fuzz case {i}")
+
+
 def test_device_path_equals_host_path_and_is_deterministic():
     import torch
 

@@ -1,0 +1,85 @@
+#!/usr/bin/env python
+"""Randomised parity fuzz on a GPU box: small inputs of many shapes (clusters, lattices with ties, wide radii,
+negative alpha, far-away offsets, both vertex modes) through the CUDA path and the CPU oracle; reports any
+difference in the four arrays or in the raised error.
+
+    python tools/gpu_fuzz.py [cases] [seed]
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import paper_1908_05944_b200 as ax  # noqa: E402
+
+
+def make_case(rng):
+    kind = rng.integers(0, 6)
+    n = int(rng.integers(1, 400))
+    if kind == 0:      # uniform box at protein density
+        side = (12.0 * n) ** (1 / 3)
+        c = rng.uniform(0, side, (n, 3))
+    elif kind == 1:    # tight clusters
+        k = max(1, n // 40)
+        centres = rng.uniform(0, 40, (k, 3))
+        c = centres[rng.integers(0, k, n)] + rng.normal(0, 1.5, (n, 3))
+    elif kind == 2:    # exact lattice (ties in cell assignment, cospherical points)
+        m = int(np.ceil(n ** (1 / 3)))
+        g = np.stack(np.meshgrid(*[np.arange(m)] * 3, indexing="ij"), -1).reshape(-1, 3)[:n]
+        c = g * rng.choice([1.5, 1.9, 2.0, 2.5]) + rng.normal(0, 1e-3, (n, 3))
+    elif kind == 3:    # far from the origin
+        side = (12.0 * n) ** (1 / 3)
+        c = rng.uniform(0, side, (n, 3)) + rng.choice([1e3, -5e4, 1e6])
+    elif kind == 4:    # flat slab (2D-ish)
+        side = (20.0 * n) ** 0.5
+        c = np.concatenate([rng.uniform(0, side, (n, 2)), rng.uniform(0, 2.0, (n, 1))], 1)
+    else:              # a line of balls
+        c = np.stack([np.arange(n) * rng.uniform(1.0, 3.0), rng.normal(0, 0.3, n), rng.normal(0, 0.3, n)], 1)
+    c = np.unique(np.ascontiguousarray(c, dtype=np.float64), axis=0)
+    rng.shuffle(c)
+    n = c.shape[0]
+    rk = rng.integers(0, 3)
+    r = rng.uniform(1.2, 1.9, n) if rk == 0 else (rng.uniform(0.05, 3.0, n) if rk == 1 else np.full(n, 1.5))
+    alpha = float(rng.choice([0.0, 0.5, 1.4, 3.0, -0.05, -1.0]))
+    bio = bool(rng.integers(0, 2)) and alpha >= 0
+    eps_sing = float(rng.choice([1e-12, 1e-300]))
+    return c, r, alpha, bio, eps_sing
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 300
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    bad = 0
+    raised = 0
+    for i in range(cases):
+        c, r, alpha, bio, eps_sing = make_case(rng)
+        ref = oracle.compute(c, r, alpha, eps_singular=eps_sing, biomolecule=bio, threads=4, chunk=64)
+        try:
+            k = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=alpha, biomolecule_mode=bio,
+                                                                        tolerance=ax.TolerancePolicy(1e-9, eps_sing)))
+            got = (k.vertices, k.edges, k.triangles, k.tets)
+            err = None
+        except ax.DegenerateSimplex as exc:
+            got, err = None, ("DegenerateSimplex", tuple(exc.vertices))
+        except ValueError as exc:
+            got, err = None, ("ValueError", str(exc)[:40])
+        if ref.status != oracle.OK:
+            raised += 1
+            ok = err is not None and (err[0] != "DegenerateSimplex" or tuple(ref.error_vertices) == err[1])
+        else:
+            ok = err is None and all(np.array_equal(a, b) for a, b in zip(got, (ref.vertices, ref.edges, ref.triangles, ref.tets)))
+        if not ok:
+            bad += 1
+            print(f"case {i}: n={len(r)} alpha={alpha} bio={bio} eps_sing={eps_sing} MISMATCH oracle_status={ref.status} "
+                  f"oracle_err={getattr(ref, 'error_vertices', None)} gpu_err={err} "
+                  f"counts gpu={None if got is None else [len(a) for a in got]} oracle={ref.counts() if ref.status == oracle.OK else None}")
+    print(f"{cases} cases, {raised} raised on both sides, {bad} mismatches")
+    return 1 if bad else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
