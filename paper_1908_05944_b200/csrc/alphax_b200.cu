@@ -116,6 +116,8 @@ struct axb_ctx {
     int cull_mask = 1;                    // bit 0: tets, bit 1: triangles (A/B switch AXB_CULL=0..3)
     bool cull = false;                    // one-call path: k_tri_tet2 settles partner-dominated simplices itself
     bool slab_mode = false;               // grid geometry fixed by the caller (one z-slab of a global grid)
+    bool defer_dup = false;               // one-call paths: the duplicate-centre check rides on the edge stage's host sync
+    bool dup_pending = false;
     const int64_t *gidx = nullptr;        // slab mode: global ball index per local ball (ascending)
 };
 
@@ -674,9 +676,12 @@ int grid_build_common(axb_ctx *c, int64_t n, const double *d_xyz, const double *
         st = bin_balls(c, side, b.lo, dims, 0, dims[2]);
     }
     if (st != AXB_OK) return st;
-    st = fetch_counters(c);
-    if (st != AXB_OK) return st;
-    if (c->h->ctr.dup_count) return report_duplicate(c, c->h->ctr.dup_count);
+    c->dup_pending = c->defer_dup && !bad_side;
+    if (!c->dup_pending) {
+        st = fetch_counters(c);
+        if (st != AXB_OK) return st;
+        if (c->h->ctr.dup_count) return report_duplicate(c, c->h->ctr.dup_count);
+    }
     if (bad_side)
         return fail(c, AXB_ERR_BAD_SIDE, "alpha=%.17g gives non-positive squared cell side (r_max=%.17g)", prm->alpha, b.rmax);
     st = mark_event(c, AXB_ST_GRID + 1);
@@ -754,7 +759,9 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
     memset(&c->h->ctr, 0, sizeof(Counters));
     c->h->ctr.err_key = ~0ull;
     c->h->ctr.first_bad = 0xffffffffu;
-    CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
+    // (with a pending duplicate check the device counters are still the grid stage's: all zero but dup_count)
+    if (!c->dup_pending)
+        CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
     if ((st = mark_event(c, AXB_ST_POT_EDGES)) != AXB_OK) return st;
     ARENA(c, c->adj_off, uint32_t, n);
     ARENA(c, c->deg, int, n);
@@ -779,6 +786,10 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
         if (st != AXB_OK) return st;
         st = fetch_counters(c);
         if (st != AXB_OK) return st;
+        if (c->dup_pending) {              // pipeline.py:238-244 comes before any edge is looked at
+            c->dup_pending = false;
+            if (c->h->ctr.dup_count) return report_duplicate(c, c->h->ctr.dup_count);
+        }
         if (c->h->ctr.n_pe <= c->pe_cap) break;
         if (attempt >= 2) return fail(c, AXB_ERR_INTERNAL, "potential-edge buffer still too small after resize");
         want = (uint64_t)c->h->ctr.n_pe + 1024;
@@ -1040,7 +1051,9 @@ extern "C" int axb_sync_check(axb_ctx *c) {
 extern "C" int axb_compute(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *prm,
                            int64_t counts[4]) {
     if (!c) return AXB_ERR_BAD_ARG;
+    c->defer_dup = true;
     int st = axb_grid_build(c, n, d_xyz, d_radii, prm);
+    c->defer_dup = false;
     if (st != AXB_OK) return st;
     c->cull = true;
     if (const char *e = getenv("AXB_CULL")) c->cull_mask = atoi(e);
@@ -1192,7 +1205,9 @@ extern "C" int axb_compute_host_begin(axb_ctx *c, int64_t n, const double *h_xyz
     c->arena_bytes = full - in_bytes;
     auto now_ms = []() { timespec t; clock_gettime(CLOCK_MONOTONIC, &t); return t.tv_sec * 1e3 + t.tv_nsec * 1e-6; };
     const double tb0 = now_ms();
+    c->defer_dup = true;
     int st = axb_grid_build(c, n, d_in, d_in + 3 * (size_t)n, prm);
+    c->defer_dup = false;
     const double tb1 = now_ms();
     if (st == AXB_OK) {
         c->cull = true;
