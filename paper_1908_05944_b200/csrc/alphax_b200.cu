@@ -116,6 +116,7 @@ struct axb_ctx {
     int cull_mask = 1;                    // bit 0: tets, bit 1: triangles (A/B switch AXB_CULL=0..3)
     bool cull = false;                    // one-call path: k_tri_tet2 settles partner-dominated simplices itself
     bool slab_mode = false;               // grid geometry fixed by the caller (one z-slab of a global grid)
+    bool many_tets = false;               // > 20 partner pairs per generator: heavy tile shape, claimed tet chunks
     bool defer_dup = false;               // one-call paths: the duplicate-centre check rides on the edge stage's host sync
     bool dup_pending = false;
     const int64_t *gidx = nullptr;        // slab mode: global ball index per local ball (ascending)
@@ -407,6 +408,7 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
         };
         int st;
         const bool heavy = c->h->ctr.pair_bound > 20ull * (unsigned long long)std::max(ngen, 1);   // > 20 partner pairs per generator
+        c->many_tets = heavy;
         if (c->W != 1) st = launch(k_tri_tet3<4, T3_LIGHT>, sizeof(T3Warp<4, T3_LIGHT>), T3Cfg<4, T3_LIGHT>::GENS, 1);
         else if (heavy) st = launch(k_tri_tet3<1, T3_HEAVY>, sizeof(T3Warp<1, T3_HEAVY>), T3Cfg<1, T3_HEAVY>::GENS, T3Cfg<1, T3_HEAVY>::MINB);
         else st = launch(k_tri_tet3<1, T3_LIGHT>, sizeof(T3Warp<1, T3_LIGHT>), T3Cfg<1, T3_LIGHT>::GENS, T3Cfg<1, T3_LIGHT>::MINB);
@@ -806,11 +808,19 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
 }
 
 // potential triangles + tets into global lists (the standalone stage path); synchronises
-int run_tri_tet_lists(axb_ctx *c) {
+// optimistic = true (axb_compute): no host round trip after the kernel; the list sizes are a guess that almost
+// always holds, the pruning kernels check it on the device (lists_overflowed) and run_canonicalize reports it, upon
+// which the caller redoes the stage with optimistic = false (exact sizes, one sync)
+int run_tri_tet_lists(axb_ctx *c, bool optimistic = false, bool redo = false) {
     int st;
     uint64_t pt_want = c->h->ctr.pair_bound + 32;           // every potential triangle is a partner pair
     uint64_t pq_want = c->h->ctr.pair_bound + 4096;         // first guess; re-run on overflow
-    for (int attempt = 0;; ++attempt) {
+    if (!redo && getenv("AXB_TEST_SMALL_PQ")) pq_want = 64;   // test hook: make the first guess fail
+    if (redo) {                                             // the counters of the failed optimistic run are on the host
+        pq_want = std::max<uint64_t>(pq_want, (uint64_t)c->h->ctr.n_pq + 1024);
+        pt_want = std::max<uint64_t>(pt_want, (uint64_t)c->h->ctr.n_pt + 32);
+    }
+    for (int attempt = redo ? 1 : 0;; ++attempt) {
         if (pt_want > 0xfffffff0ull || pq_want > 0xfffffff0ull)
             return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential triangles or tetrahedra");
         c->arena_used = c->mark_after_edges;
@@ -826,10 +836,19 @@ int run_tri_tet_lists(axb_ctx *c) {
         }
         st = launch_tri_tet(c, 0);
         if (st != AXB_OK) return st;
+        if (optimistic && attempt == 0) {
+            if ((st = mark_event(c, AXB_ST_POT_TRIANGLES + 1)) != AXB_OK) return st;
+            if ((st = mark_event(c, AXB_ST_POT_TETS + 1)) != AXB_OK) return st;
+            c->n_pt = c->pt_cap;                            // upper bounds until run_canonicalize reads the counters
+            c->n_pq = c->many_tets ? c->pq_cap : 0;         // only its size class matters (k_prune_tets variant)
+            c->k3_cap = c->pq_cap;
+            c->state = S_POTENTIAL;
+            return AXB_OK;
+        }
         st = fetch_counters(c);
         if (st != AXB_OK) return st;
         if (c->h->ctr.n_pq <= c->pq_cap && c->h->ctr.n_pt <= c->pt_cap) break;
-        if (attempt >= 2) return fail(c, AXB_ERR_INTERNAL, "potential-tet buffer still too small after resize");
+        if (attempt >= 3) return fail(c, AXB_ERR_INTERNAL, "potential-tet buffer still too small after resize");
         pq_want = (uint64_t)c->h->ctr.n_pq + 1024;
         pt_want = std::max<uint64_t>(pt_want, (uint64_t)c->h->ctr.n_pt + 32);
     }
@@ -843,10 +862,10 @@ int run_tri_tet_lists(axb_ctx *c) {
     return AXB_OK;
 }
 
-int run_potential(axb_ctx *c, int64_t lo, int64_t hi) {
+int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool optimistic = false) {
     int st = run_edges(c, lo, hi);
     if (st != AXB_OK) return st;
-    return run_tri_tet_lists(c);
+    return run_tri_tet_lists(c, optimistic);
 }
 
 // kept-simplex state of the pruning stage (prune.cuh), zeroed
@@ -1057,12 +1076,16 @@ extern "C" int axb_compute(axb_ctx *c, int64_t n, const double *d_xyz, const dou
     if (st != AXB_OK) return st;
     c->cull = true;
     if (const char *e = getenv("AXB_CULL")) c->cull_mask = atoi(e);
-    st = run_potential(c, 0, n);
+    st = run_potential(c, 0, n, /*optimistic=*/true);
+    if (st == AXB_OK) st = run_prune(c);
+    if (st == AXB_OK) st = run_canonicalize(c, counts);
+    if (st == AXB_ERR_ARENA + 1000) {                       // a guessed list size did not hold: redo the stage with exact sizes
+        st = run_tri_tet_lists(c, false, /*redo=*/true);
+        if (st == AXB_OK) st = run_prune(c);
+        if (st == AXB_OK) st = run_canonicalize(c, counts);
+        if (st == AXB_ERR_ARENA + 1000) st = fail(c, AXB_ERR_INTERNAL, "a potential list overflowed after it was sized exactly");
+    }
     c->cull = false;
-    if (st != AXB_OK) return st;
-    if ((st = run_prune(c)) != AXB_OK) return st;
-    st = run_canonicalize(c, counts);
-    if (st == AXB_ERR_ARENA + 1000) return fail(c, AXB_ERR_INTERNAL, "a potential list overflowed after it was sized exactly");
     return st;
 }
 

@@ -244,6 +244,23 @@ def test_randomised_shapes_against_oracle():
             assert_same_complex(ax.compute_alpha_complex_arrays(c, r, cfg), ref, f"fuzz case {i}")
 
 
+def test_optimistic_list_sizes_are_redone_when_they_do_not_hold(monkeypatch):
+    """axb_compute sizes the potential-tet list by a guess and checks it only at the end (no host round trip after
+    the triangle/tet kernel); AXB_TEST_SMALL_PQ makes the guess fail so the redo path (and the host path's
+    retry loop) must produce the same complex."""
+    import torch
+
+    eng = ax.default_engine()
+    c, r = synth.jittered_lattice(60_000, 4)
+    cfg = ax.PipelineConfig(alpha=1.0)
+    want = eng.compute_host(c, r, cfg)
+    monkeypatch.setenv("AXB_TEST_SMALL_PQ", "1")
+    dev = [t.cpu().numpy() for t in eng.compute_device(torch.as_tensor(c, device="cuda"), torch.as_tensor(r, device="cuda"), cfg)]
+    host = eng.compute_host(c, r, cfg)
+    for a, b, h in zip(want, dev, host):
+        assert np.array_equal(a, b) and np.array_equal(a, h)
+
+
 def test_device_path_equals_host_path_and_is_deterministic():
     import torch
 
