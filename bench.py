@@ -12,8 +12,9 @@ synthetic protein-density point set (generator G2 of SURVEY.md 8(d)).
 Workload at N=1: SURVEY.md 8(d) config 3 -- 1,000,000 atoms, seed 0, alpha 0.
 At N>1 every rank owns one z-slab of 1,000,000 atoms of an N x 1,000,000-atom
 set (weak scaling; N=8 is an 8M-atom assembly; `--atoms-per-gpu 1250000` gives
-the 10M-atom config 4), halo atoms replicated, no data-path collective; the
-only collective is the final gather of counts.
+the 10M-atom config 4), halo atoms replicated; the slab kernels need no
+collective, the union across slabs is one all_to_all of rows by owner range, a
+parallel merge, and the final gather of counts and rows to rank 0.
 
 Prints ONE JSON line (see the task contract): `value` = device-resident
 throughput (inputs already in HBM, outputs left in HBM), `e2e` = the same
@@ -203,7 +204,7 @@ def workload_config(args, n_local):
                         f"1 atom/12 A^3, radii U[1.2,1.9] A, alpha={args.alpha} A^2",
             "atoms_per_gpu": n_local, "alpha": args.alpha, "eps_singular": args.eps_singular,
             "l2": "flushed (256 MiB write) between timed steps; per-step working set ~1.5 GB also exceeds L2",
-            "sharding": "one z-slab per rank, 2-cell halo replicated" if args.gpus > 1 else "single GPU"}
+            "sharding": "one z-slab per rank, 2-cell halo replicated; all_to_all by owner range + parallel merge + gather to rank 0" if args.gpus > 1 else "single GPU"}
 
 
 def bench_b200(args, rank, world, local_rank):

@@ -10,9 +10,12 @@ GPUs.  Why 2 layers suffice with no exchange: every simplex incident to an
 owned ball has all vertices within 2 cells of it, its ortho-centre within 1
 cell, and the domination candidates within 1 cell of the centre
 (pipeline.py:288-289, 316-320).  Like a reference chunk, a slab also emits the
-faces its kept simplices inherit even when a neighbour owns them, so the only
-collective is the final gather of counts and rows to rank 0, which takes the
-sorted duplicate-free union (pipeline.py:611-614) on its GPU.
+faces its kept simplices inherit even when a neighbour owns them, so the
+sorted duplicate-free union (pipeline.py:611-614) has to be taken across
+slabs: rows are exchanged by owner-index range (one all_to_all), every rank
+merges its range on its GPU, and the final gather of counts and rows to rank 0
+is a concatenation in rank order.  (`ShardedJob.step(parallel_merge=False)`
+keeps the simpler form: gather everything, merge on rank 0 alone.)
 
 `local_compute` / `merge` are injectable so the plumbing is testable on CPU
 with the gloo backend (tests/test_sharding.py).
@@ -141,6 +144,41 @@ def gather_rows(local: list, dist, group=None, device="cpu"):
     return [b.to(device) for b in bufs] if via_host else bufs
 
 
+def exchange_by_owner(local: list, n_global: int, dist, group=None, device="cpu"):
+    """Range-partitioned exchange: rank q becomes responsible for the rows whose first column (the owner =
+    minimum ball index of the simplex) lies in [q * n / world, (q + 1) * n / world).  Every rank cuts its
+    (canonical, hence owner-sorted) row lists at those boundaries and one all_to_all per dimension moves the
+    pieces; afterwards each rank merges ITS range (1 / world of all rows) in parallel, and the final gather
+    to rank 0 is a plain concatenation in rank order -- rank 0 no longer merges everything alone.
+    `local` as in gather_rows.  Returns the four received row tensors (rank-major concatenation, unmerged)."""
+    import torch
+
+    world = dist.get_world_size(group)
+    via_host = dist.get_backend(group) == "gloo" and str(device).startswith("cuda")
+    tdev = "cpu" if via_host else device
+    edges = torch.tensor([(q * n_global) // world for q in range(world + 1)], dtype=torch.int64, device=device)
+    rows, send = [], []
+    for d in range(4):
+        r = local[d].reshape(-1, d + 1).contiguous()
+        cut = torch.searchsorted(r[:, 0].contiguous(), edges)          # rows are sorted by owner
+        cut[0], cut[-1] = 0, r.shape[0]
+        rows.append(r)
+        send.append(cut[1:] - cut[:-1])
+    send_counts = torch.stack(send, dim=1).to(tdev).contiguous()         # (world, 4): rows for destination q, dimension d
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)        # the collective on counts
+    send_np, recv_np = send_counts.cpu().numpy(), recv_counts.cpu().numpy()
+    out = []
+    for d in range(4):
+        width = d + 1
+        src = rows[d].to(tdev)
+        dst = torch.empty((int(recv_np[:, d].sum()), width), dtype=torch.int64, device=tdev)
+        dist.all_to_all_single(dst, src, output_split_sizes=[int(v) for v in recv_np[:, d]],
+                               input_split_sizes=[int(v) for v in send_np[:, d]], group=group)   # the rows
+        out.append(dst.to(device) if via_host else dst)
+    return out
+
+
 class ShardedJob:
     """One rank's share of a sharded run: owns the local inputs on its GPU; step() computes the
     slab, gathers everything on rank 0 and merges there."""
@@ -174,9 +212,18 @@ class ShardedJob:
             return [torch.empty((0,) if d == 0 else (0, d + 1), dtype=torch.int64, device=self.device) for d in range(4)]
         return self.engine.compute_slab_device(self.d_c, self.d_r, self.d_g, self.cfg, self.plan, self.slab)
 
-    def step(self):
-        """Returns the four merged CUDA tensors on rank 0, None elsewhere."""
+    def step(self, parallel_merge: bool = True):
+        """Returns the four merged CUDA tensors on rank 0, None elsewhere.
+        parallel_merge: exchange rows by owner range, merge 1 / world of them on every rank, gather the sorted
+        pieces (default); otherwise gather everything and merge on rank 0 alone."""
         outs = self.local()
+        if self.world > 1 and parallel_merge:
+            mine = exchange_by_owner(outs, self.n_global, self.dist, self.group, device=self.device)
+            merged = [self.engine.merge_rows(mine[d], d + 1, self.n_global) for d in range(4)]
+            parts = gather_rows(merged, self.dist, self.group, device=self.device)
+            if parts is None:
+                return None
+            return [p.reshape(-1) if d == 0 else p for d, p in enumerate(parts)]     # owner ranges ascend with the rank
         if self.world == 1:
             parts = [[o] for o in outs]
         else:

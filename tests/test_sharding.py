@@ -97,17 +97,30 @@ def _worker(rank, world, port, out_dir):
             np.savez(os.path.join(out_dir, "merged.npz"), *merged)
         else:
             assert gathered is None
+        # range-partitioned form: exchange by owner, merge the own range, gather the sorted pieces
+        mine = sharding.exchange_by_owner(local, len(r), dist, device="cpu")
+        lo, hi = rank * len(r) // world, (rank + 1) * len(r) // world
+        own = []
+        for d in range(4):
+            rows = mine[d].numpy().reshape(-1, d + 1)
+            assert rows.shape[0] == 0 or (rows[:, 0].min() >= lo and rows[:, 0].max() < hi)
+            own.append(torch.as_tensor(sharding.numpy_merge([rows], d + 1)))
+        pieces = sharding.gather_rows(own, dist, device="cpu")
+        if rank == 0:
+            np.savez(os.path.join(out_dir, "merged_parallel.npz"), *[p.numpy() for p in pieces])
     finally:
         dist.destroy_process_group()
 
 
-def test_gather_and_merge_over_gloo_world2(tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_and_merge_over_gloo(tmp_path, world):
     import torch.multiprocessing as mp
 
-    world = 2
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     got = np.load(os.path.join(str(tmp_path), "merged.npz"))
     c, r = synth.jittered_lattice(3000, 9)
     full = oracle.compute(c, r, 0.6)
+    par = np.load(os.path.join(str(tmp_path), "merged_parallel.npz"))
     for d in range(4):
         assert np.array_equal(got[f"arr_{d}"], arrays(full)[d])
+        assert np.array_equal(par[f"arr_{d}"].reshape(arrays(full)[d].shape), arrays(full)[d])
