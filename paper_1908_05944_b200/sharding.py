@@ -103,14 +103,17 @@ def numpy_merge(parts: list, k: int) -> np.ndarray:
     return out.reshape(-1) if k == 1 else out
 
 
-def gather_rows(local: list, dist, group=None, device="cpu"):
+def gather_rows(local: list, dist, group=None, device="cpu", narrow: bool = False):
     """Gather the four row lists of every rank on rank 0: one all_gather of the counts, then every rank
     sends its exact rows (no padding) and rank 0 receives them straight into per-rank slices of ONE
     buffer per dimension, so the concatenation the merge needs already exists when the transfers end.
     `local` = [vertices (k0,), edges (k1,2), triangles (k2,3), tets (k3,4)] torch int64 tensors.
+    narrow: the rows travel as int32 (the caller guarantees indices < 2^31) and rank 0 widens them back to the
+    reference's int64 -- half the bytes into the one GPU everything converges on.
     Returns on rank 0: list over dims of (m_d, d+1) tensors (rank-major concatenation); elsewhere None."""
     import torch
 
+    wire = torch.int32 if narrow else torch.int64
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     counts = torch.tensor([int(t.shape[0]) for t in local], dtype=torch.int64, device=device)
@@ -124,10 +127,10 @@ def gather_rows(local: list, dist, group=None, device="cpu"):
     ops, bufs = [], []
     for d in range(4):
         width = d + 1
-        mine = local[d].reshape(-1, width).contiguous().to(tdev)
+        mine = local[d].reshape(-1, width).contiguous().to(device=tdev, dtype=wire)
         if rank == 0:
             total = int(all_counts[:, d].sum())
-            buf = torch.empty((total, width), dtype=torch.int64, device=tdev)
+            buf = torch.empty((total, width), dtype=wire, device=tdev)
             offs = np.concatenate([[0], np.cumsum(all_counts[:, d])]).astype(np.int64)
             buf[: mine.shape[0]] = mine
             for r in range(1, world):
@@ -141,7 +144,7 @@ def gather_rows(local: list, dist, group=None, device="cpu"):
             req.wait()
     if rank != 0:
         return None
-    return [b.to(device) for b in bufs] if via_host else bufs
+    return [b.to(device=device, dtype=torch.int64) for b in bufs]
 
 
 def exchange_by_owner(local: list, n_global: int, dist, group=None, device="cpu"):
@@ -220,7 +223,7 @@ class ShardedJob:
         if self.world > 1 and parallel_merge:
             mine = exchange_by_owner(outs, self.n_global, self.dist, self.group, device=self.device)
             merged = [self.engine.merge_rows(mine[d], d + 1, self.n_global) for d in range(4)]
-            parts = gather_rows(merged, self.dist, self.group, device=self.device)
+            parts = gather_rows(merged, self.dist, self.group, device=self.device, narrow=self.n_global < 2 ** 31)
             if parts is None:
                 return None
             return [p.reshape(-1) if d == 0 else p for d, p in enumerate(parts)]     # owner ranges ascend with the rank
