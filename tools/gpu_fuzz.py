@@ -3,7 +3,7 @@
 negative alpha, far-away offsets, both vertex modes) through the CUDA path and the CPU oracle; reports any
 difference in the four arrays or in the raised error.
 
-    python tools/gpu_fuzz.py [cases] [seed]
+    python tools/gpu_fuzz.py [cases] [seed] [n_max]
 """
 import os
 import sys
@@ -17,9 +17,9 @@ import oracle  # noqa: E402
 import paper_1908_05944_b200 as ax  # noqa: E402
 
 
-def make_case(rng):
+def make_case(rng, n_max=400):
     kind = rng.integers(0, 6)
-    n = int(rng.integers(1, 400))
+    n = int(rng.integers(1, n_max))
     if kind == 0:      # uniform box at protein density
         side = (12.0 * n) ** (1 / 3)
         c = rng.uniform(0, side, (n, 3))
@@ -53,11 +53,13 @@ def make_case(rng):
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 300
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    n_max = int(sys.argv[3]) if len(sys.argv) > 3 else 400
     bad = 0
     raised = 0
+    limit = 0
     for i in range(cases):
-        c, r, alpha, bio, eps_sing = make_case(rng)
-        ref = oracle.compute(c, r, alpha, eps_singular=eps_sing, biomolecule=bio, threads=4, chunk=64)
+        c, r, alpha, bio, eps_sing = make_case(rng, n_max)
+        ref = oracle.compute(c, r, alpha, eps_singular=eps_sing, biomolecule=bio, threads=os.cpu_count(), chunk=256)
         try:
             k = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=alpha, biomolecule_mode=bio,
                                                                         tolerance=ax.TolerancePolicy(1e-9, eps_sing)))
@@ -67,6 +69,11 @@ def main():
             got, err = None, ("DegenerateSimplex", tuple(exc.vertices))
         except ValueError as exc:
             got, err = None, ("ValueError", str(exc)[:40])
+        except ax.AlphaxError as exc:
+            if "AXB_ERR_DENSITY" in str(exc):       # documented limit (> 256 potential-edge partners per ball): loud, not wrong
+                limit += 1
+                continue
+            raise
         if ref.status != oracle.OK:
             raised += 1
             ok = err is not None and (err[0] != "DegenerateSimplex" or tuple(ref.error_vertices) == err[1])
@@ -77,7 +84,7 @@ def main():
             print(f"case {i}: n={len(r)} alpha={alpha} bio={bio} eps_sing={eps_sing} MISMATCH oracle_status={ref.status} "
                   f"oracle_err={getattr(ref, 'error_vertices', None)} gpu_err={err} "
                   f"counts gpu={None if got is None else [len(a) for a in got]} oracle={ref.counts() if ref.status == oracle.OK else None}")
-    print(f"{cases} cases, {raised} raised on both sides, {bad} mismatches")
+    print(f"{cases} cases, {raised} raised on both sides, {limit} beyond the density limit, {bad} mismatches")
     return 1 if bad else 0
 
 
