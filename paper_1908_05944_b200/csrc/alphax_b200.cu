@@ -194,6 +194,25 @@ int device_scan(axb_ctx *c, const uint32_t *in, size_t n, uint32_t *out) {
     return AXB_OK;
 }
 
+// four exclusive scans of equally long arrays in three launches
+int device_scan4(axb_ctx *c, const uint32_t *const in[4], size_t n, uint32_t *const out[4]) {
+    size_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (ntiles == 0) ntiles = 1;
+    Scan4 a;
+    for (int k = 0; k < 4; ++k) {
+        a.in[k] = in[k];
+        a.out[k] = out[k];
+        ARENA(c, a.sums[k], uint32_t, ntiles + 1);
+    }
+    k_scan4_tile_sums<<<dim3((unsigned)ntiles, 4), SCAN_THREADS, 0, c->stream>>>(a, n);
+    LAUNCH_CHECK(c);
+    k_scan4_of_sums<<<4, SCAN_THREADS, 0, c->stream>>>(a, ntiles);
+    LAUNCH_CHECK(c);
+    k_scan4_apply<<<dim3((unsigned)ntiles, 4), SCAN_THREADS, 0, c->stream>>>(a, n);
+    LAUNCH_CHECK(c);
+    return AXB_OK;
+}
+
 int fetch_counters(axb_ctx *c) {
     CUDA_TRY(c, cudaMemcpyAsync(&c->h->ctr, c->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -928,10 +947,11 @@ int run_canonicalize(axb_ctx *c, int64_t counts[4]) {
     ARENA(c, c->off2, uint32_t, n + 2);
     ARENA(c, c->off3, uint32_t, n + 2);
     ARENA(c, c->voff, uint32_t, n + 2);
-    if ((st = device_scan(c, c->cnt1, n, c->off1)) != AXB_OK) return st;
-    if ((st = device_scan(c, c->cnt2, n, c->off2)) != AXB_OK) return st;
-    if ((st = device_scan(c, c->cnt3, n, c->off3)) != AXB_OK) return st;
-    if ((st = device_scan(c, c->vkeep, n, c->voff)) != AXB_OK) return st;
+    {
+        const uint32_t *const in[4] = {c->cnt1, c->cnt2, c->cnt3, c->vkeep};
+        uint32_t *const out[4] = {c->off1, c->off2, c->off3, c->voff};
+        if ((st = device_scan4(c, in, n, out)) != AXB_OK) return st;
+    }
     CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[0], c->voff + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[1], c->off1 + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[2], c->off2 + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));

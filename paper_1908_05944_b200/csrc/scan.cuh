@@ -92,4 +92,63 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(const uint32_t *in,
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = tile_sums[gridDim.x];
 }
 
+// ---- the same three steps over up to four equally long arrays in one go (blockIdx.y = array): the canonical
+// stage scans the per-owner counters of all four dimensions, and twelve tiny launches cost more than the work
+struct Scan4 {
+    const uint32_t *in[4];
+    uint32_t *out[4];
+    uint32_t *sums[4];       // (ntiles + 1) each
+};
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan4_tile_sums(Scan4 a, size_t n) {
+    __shared__ unsigned s_warp[33];
+    const uint32_t *in = a.in[blockIdx.y];
+    size_t base = (size_t)blockIdx.x * SCAN_TILE + (size_t)threadIdx.x * SCAN_ITEMS;
+    unsigned v = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i)
+        if (base + i < n) v += in[base + i];
+    unsigned total;
+    block_excl_scan_1024(v, s_warp, total);
+    if (threadIdx.x == 0) a.sums[blockIdx.y][blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan4_of_sums(Scan4 a, size_t ntiles) {
+    __shared__ unsigned s_warp[33];
+    uint32_t *tile_sums = a.sums[blockIdx.x];
+    unsigned carry = 0;
+    for (size_t base = 0; base < ntiles; base += SCAN_THREADS) {
+        size_t i = base + threadIdx.x;
+        unsigned v = i < ntiles ? tile_sums[i] : 0u;
+        unsigned total;
+        unsigned ex = block_excl_scan_1024(v, s_warp, total);
+        if (i < ntiles) tile_sums[i] = carry + ex;
+        carry += total;
+    }
+    if (threadIdx.x == 0) tile_sums[ntiles] = carry;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan4_apply(Scan4 a, size_t n) {
+    __shared__ unsigned s_warp[33];
+    const uint32_t *in = a.in[blockIdx.y];
+    uint32_t *out = a.out[blockIdx.y];
+    const uint32_t *tile_sums = a.sums[blockIdx.y];
+    size_t base = (size_t)blockIdx.x * SCAN_TILE + (size_t)threadIdx.x * SCAN_ITEMS;
+    unsigned item[SCAN_ITEMS];
+    unsigned v = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        item[i] = (base + i < n) ? in[base + i] : 0u;
+        v += item[i];
+    }
+    unsigned total;
+    unsigned ex = block_excl_scan_1024(v, s_warp, total) + tile_sums[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        if (base + i < n) out[base + i] = ex;
+        ex += item[i];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = tile_sums[gridDim.x];
+}
+
 }  // namespace axb
