@@ -278,10 +278,10 @@ __device__ __forceinline__ Atom load_atom(const Atom *__restrict__ atoms, int t)
 // of dependent round trips: row bounds -> balls of the row -> next row ...  Here (1) the bounds of all
 // nine rows of the 3x3x3 block are fetched back to back (straight-line code, clamped indices, so the 18
 // loads are in flight together) and parked in a per-thread column of shared memory, (2) the balls of
-// all rows are walked as ONE flattened sequence with AC2_DEPTH loads in flight ahead of the ball being
-// tested.  Same boolean as ac2_pass (same cells, same arithmetic, pipeline.py:286-313).
+// all rows are walked as ONE flattened sequence with the next AC2_DEPTH + 1 balls prefetched into L1 ahead
+// of the ball being tested.  Same boolean as ac2_pass (same cells, same arithmetic, pipeline.py:286-313).
 #ifndef AC2_DEPTH
-#define AC2_DEPTH 2
+#define AC2_DEPTH 1
 #endif
 __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__restrict__ atoms, double cx, double cy,
                                              double cz, double thr, double r2max, int inc0, int inc1, int inc2, int inc3,
@@ -337,6 +337,32 @@ __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__re
         }
         return pos++;
     };
+#ifndef AC2_PREFETCH
+#define AC2_PREFETCH 1
+#endif
+#if AC2_PREFETCH
+    // The balls ahead are requested with prefetch.global.L1 (no destination register), the ball under test is
+    // loaded when it is needed and hits L1: only two integers travel down the queue per step instead of whole
+    // 32-byte records (the record queue spent a quarter of the kernel's instructions on register moves).
+    auto prefetch = [&](int t) { asm volatile("prefetch.global.L1 [%0];" ::"l"(atoms + t)); };
+    int tq[AC2_DEPTH + 1];
+#pragma unroll
+    for (int d = 0; d <= AC2_DEPTH; ++d) {
+        tq[d] = next();
+        if (tq[d] >= 0) prefetch(tq[d]);
+    }
+    while (tq[0] >= 0) {
+        const int t = tq[0];
+        const Atom a = load_atom(atoms, t);
+#pragma unroll
+        for (int d = 0; d < AC2_DEPTH; ++d) tq[d] = tq[d + 1];
+        tq[AC2_DEPTH] = next();
+        if (tq[AC2_DEPTH] >= 0) prefetch(tq[AC2_DEPTH]);
+        const double ddx = a.x - cx, ddy = a.y - cy, ddz = a.z - cz;
+        const double dp = ((ddx * ddx + ddy * ddy) + ddz * ddz) - a.r2;
+        if (dp < thr && !(t == inc0 || t == inc1 || t == inc2 || t == inc3)) return false;   // incident balls are masked (pipeline.py:306-307)
+    }
+#else
     int tq[AC2_DEPTH];
     Atom aq[AC2_DEPTH];
 #pragma unroll
@@ -355,6 +381,7 @@ __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__re
         const double dp = ((ddx * ddx + ddy * ddy) + ddz * ddz) - a.r2;
         if (dp < thr && !(t == inc0 || t == inc1 || t == inc2 || t == inc3)) return false;   // incident balls are masked (pipeline.py:306-307)
     }
+#endif
     return true;
 }
 #endif
