@@ -325,14 +325,18 @@ __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__re
             er[k] = (int)__ldg(g.cell_start + b);
         }
     }
+    // only the non-empty rows are parked (trimming and sparse regions leave several of the nine empty), so the
+    // walk switches rows exactly once per row that holds balls
+    int nr = 0;
 #pragma unroll
-    for (int k = 0; k < 9; ++k) rows[k * stride] = make_int2(sr[k], er[k]);
+    for (int k = 0; k < 9; ++k)
+        if (er[k] > sr[k]) { rows[nr * stride] = make_int2(sr[k], er[k]); ++nr; }
     // flattened walk over the balls of all rows
     int r = -1, pos = 0, end = 0;
     auto next = [&]() -> int {
-        while (pos >= end) {
-            if (++r >= 9) { r = 9; return -1; }
-            const int2 q = rows[r * stride];
+        if (pos >= end) {
+            if (++r >= nr) { r = nr; return -1; }
+            const int2 q = rows[min(r, 8) * stride];      // (clamped: the load may be issued ahead of the test)
             pos = q.x; end = q.y;
         }
         return pos++;
