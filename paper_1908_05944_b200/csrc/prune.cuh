@@ -231,12 +231,20 @@ __global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_tris(PruneP
         const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z);
         const Ortho o = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);
         if (!ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, -1, &s_rows[0][threadIdx.x], PRUNE_THREADS)) return;
-        mark_tri(P, bu + i, j, min3(ou, ov, ow));
-        mark_edge(P, bu + i, min(ou, ov));
-        mark_edge(P, bu + j, min(ou, ow));
+        // kept: mark the triangle and its three edges.  The lookup first, then all four atomics back to back (their
+        // round trips overlap), then the owner counters of what was new (no return value needed: fire and forget)
         const unsigned bv = __ldg(P.adj_off + r.y);
         const int iw = find_partner(P.pe_v, bv, __ldg(P.deg + r.y), r.z);
-        if (iw >= 0) mark_edge(P, bv + iw, min(ov, ow)); else note_miss(P);
+        const unsigned long long bit = 1ull << (j & 63);
+        const unsigned long long t0 = atomicOr(P.trimask + (size_t)(bu + i) * P.W + (j >> 6), bit);
+        const unsigned e0 = atomicExch(P.eflag + bu + i, 1u);
+        const unsigned e1 = atomicExch(P.eflag + bu + j, 1u);
+        const unsigned e2 = iw >= 0 ? atomicExch(P.eflag + bv + iw, 1u) : 1u;
+        if (!(t0 & bit)) atomicAdd(P.cnt2 + min3(ou, ov, ow), 1u);
+        if (!e0) atomicAdd(P.cnt1 + min(ou, ov), 1u);
+        if (!e1) atomicAdd(P.cnt1 + min(ou, ow), 1u);
+        if (!e2) atomicAdd(P.cnt1 + min(ov, ow), 1u);
+        if (iw < 0) note_miss(P);
     };
 
     // fill the stack from claimed chunks until 32 free entries wait (or the list is exhausted), then settle
