@@ -305,8 +305,7 @@ __global__ void __launch_bounds__(EST_WARPS * 32, E2_MINB) k_edges(EstParams P, 
                     qn = w;
                     solved = w;
                 };
-                // ---- B: reach pre-filter over the flattened candidates; the record of the NEXT round is
-                // requested before the current one is tested (one more load in flight per lane)
+                // ---- B: reach pre-filter over the flattened candidates
                 auto lookup = [&](int p, int &cand, int &gs) {
                     int item;
                     if (p < E2_CCAP) {
@@ -322,14 +321,22 @@ __global__ void __launch_bounds__(EST_WARPS * 32, E2_MINB) k_edges(EstParams P, 
                 };
                 bool crowded = false;                       // the batch has more partners than the queue holds
                 int cand_n = 0, gs_n = 0;
-                Atom av_n;
-                av_n.x = av_n.y = av_n.z = 0.0; av_n.r2 = -1.0;
-                if (lane < total) { lookup(lane, cand_n, gs_n); av_n = load_atom(P.xyzr, cand_n); }   // (x, y, z, reach)
+                if (lane < total) {
+                    lookup(lane, cand_n, gs_n);
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(P.xyzr + cand_n));
+                }
                 for (int p0 = 0; p0 < total; p0 += 32) {
                     const int p = p0 + lane;
                     const int cand = cand_n, gs = gs_n;
-                    const Atom av = av_n;
-                    if (p + 32 < total) { lookup(p + 32, cand_n, gs_n); av_n = load_atom(P.xyzr, cand_n); }
+                    // the record of the NEXT round is requested (L1 prefetch, no destination register) before this
+                    // round's is loaded and tested
+                    if (p + 32 < total) {
+                        lookup(p + 32, cand_n, gs_n);
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(P.xyzr + cand_n));
+                    }
+                    Atom av;
+                    av.x = av.y = av.z = 0.0; av.r2 = -1.0;
+                    if (p < total) av = load_atom(P.xyzr, cand);            // (x, y, z, reach)
                     bool pass = false;
                     if (p < total) {
                         const GenSlot &q = S.g[gs];
