@@ -104,7 +104,10 @@ struct __align__(16) GenGeo {
     int cx, cy, cz;
 };
 
-constexpr int E2_GB = 8;                      // generators per warp batch
+#ifndef E2_GB_V
+#define E2_GB_V 8
+#endif
+constexpr int E2_GB = E2_GB_V;                // generators per warp batch
 constexpr int E2_ROWS = 13;                   // rows of the 5x5x5 block that can out-rank the generator
 constexpr int E2_ITEMS = E2_GB * E2_ROWS;     // 104 row items, 4 rounds of 32 lanes
 #ifndef E2_CCAP_V
