@@ -1141,6 +1141,9 @@ int ensure_pool(axb_ctx *c) {
     return AXB_OK;
 }
 
+// below this many bytes a job's host-side marshalling (input staging, row widening) runs on the calling thread
+constexpr size_t SMALL_JOB_BYTES = (size_t)1 << 20;
+
 bool is_pinned(const void *p) {
     cudaPointerAttributes at;
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
@@ -1153,7 +1156,8 @@ bool is_pinned(const void *p) {
 // the copy engine as soon as it is complete, so the DMA of one slice overlaps the memcpy of the next.
 int upload_inputs(axb_ctx *c, int64_t n, const double *h_xyz, const double *h_radii, double *d_in) {
     const size_t bx = (size_t)n * 3 * sizeof(double), br = (size_t)n * sizeof(double);
-    if (is_pinned(h_xyz) && is_pinned(h_radii)) {
+    // small inputs (one protein): the driver's own bounce buffer is faster than waking the staging threads
+    if (bx + br <= SMALL_JOB_BYTES || (is_pinned(h_xyz) && is_pinned(h_radii))) {
         CUDA_TRY(c, cudaMemcpyAsync(d_in, h_xyz, bx, cudaMemcpyHostToDevice, c->stream));
         CUDA_TRY(c, cudaMemcpyAsync(d_in + 3 * (size_t)n, h_radii, br, cudaMemcpyHostToDevice, c->stream));
         return AXB_OK;
@@ -1422,7 +1426,8 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     auto now_ms = []() { timespec t; clock_gettime(CLOCK_MONOTONIC, &t); return t.tv_sec * 1e3 + t.tv_nsec * 1e-6; };
     const double t_q = now_ms();
     double t_dim[4] = {0, 0, 0, 0};
-    c->pool->begin(2 * (stage_elems / WIDEN_PIECE) + 2 * max_chunks + n / WIDEN_PIECE + 16);
+    c->pool->begin(2 * (stage_elems / WIDEN_PIECE) + 2 * max_chunks + n / WIDEN_PIECE + 16,
+                   /*inline_run=*/stage_elems * sizeof(int32_t) <= SMALL_JOB_BYTES);
     PoolRun run{c->pool};
     std::vector<PendingChunk> chunks;
     chunks.reserve(max_chunks);

@@ -230,8 +230,12 @@ public:
     WidenPool(const WidenPool &) = delete;
     WidenPool &operator=(const WidenPool &) = delete;
 
-    // start a run that will publish at most max_tasks tasks
-    void begin(size_t max_tasks) {
+    // start a run that will publish at most max_tasks tasks.
+    // inline_run: a small job (one protein's worth of rows) -- the producer runs every task itself as it
+    // publishes it; waking a dozen sleeping threads costs more than widening a few hundred KB
+    void begin(size_t max_tasks, bool inline_run = false) {
+        inline_ = inline_run;
+        if (inline_run) return;
         if (tasks_.size() < max_tasks) tasks_.resize(max_tasks);
         closed_.store(false);
         published_.store(0);
@@ -247,6 +251,12 @@ public:
     // src_width / dst_width = int32 values per item in src / int64 values per item in dst
     void publish(int kind, const int32_t *src, int64_t *dst, size_t n, size_t piece, int src_width, int dst_width,
                  const uint32_t *off, size_t n_index, size_t row0) {
+        if (inline_) {
+            for (size_t lo = 0; lo < n; lo += piece)
+                run_task(WidenTask{src ? src + lo * src_width : nullptr, dst + lo * dst_width, n - lo < piece ? n - lo : piece,
+                                   kind, off, n_index, row0 + lo});
+            return;
+        }
         size_t p = published_.load(std::memory_order_relaxed);
         for (size_t lo = 0; lo < n && p < tasks_.size(); lo += piece) {
             tasks_[p++] = WidenTask{src ? src + lo * src_width : nullptr, dst + lo * dst_width, n - lo < piece ? n - lo : piece,
@@ -256,6 +266,11 @@ public:
     }
     // parallel memcpy of `bytes` (a multiple of 8) from src to dst in pieces of piece_bytes
     void publish_copy(const void *src, void *dst, size_t bytes, size_t piece_bytes) {
+        if (inline_) {
+            run_task(WidenTask{static_cast<const int32_t *>(src), static_cast<int64_t *>(dst), bytes / sizeof(int32_t), WK_COPY,
+                               nullptr, 0, 0});
+            return;
+        }
         size_t p = published_.load(std::memory_order_relaxed);
         for (size_t lo = 0; lo < bytes && p < tasks_.size(); lo += piece_bytes) {
             const size_t m = bytes - lo < piece_bytes ? bytes - lo : piece_bytes;
@@ -267,6 +282,7 @@ public:
     }
     // no more tasks: help with what is left and wait until every task has run
     void finish() {
+        if (inline_) { inline_ = false; return; }
         closed_.store(true);
         drain();
         while (done_.load(std::memory_order_acquire) < published_.load(std::memory_order_relaxed)) cpu_relax();
@@ -320,6 +336,7 @@ private:
     std::condition_variable cv_;
     unsigned long long epoch_ = 0;
     bool stop_ = false;
+    bool inline_ = false;              // producer-only state of the current run
     std::atomic<bool> closed_{true};
     std::atomic<size_t> published_{0}, next_{0}, done_{0};
 };
