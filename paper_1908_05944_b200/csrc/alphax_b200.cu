@@ -183,6 +183,14 @@ int mark_event(axb_ctx *c, int idx) {
 int device_scan(axb_ctx *c, const uint32_t *in, size_t n, uint32_t *out) {
     size_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
     if (ntiles == 0) ntiles = 1;
+    if (ntiles <= SCAN_SMALL_TILES) {                      // small input: one launch instead of three
+        Scan4 a{};
+        a.in[0] = in;
+        a.out[0] = out;
+        k_scan_small<<<1, SCAN_THREADS, 0, c->stream>>>(a, n);
+        LAUNCH_CHECK(c);
+        return AXB_OK;
+    }
     uint32_t *sums;
     ARENA(c, sums, uint32_t, ntiles + 1);
     k_scan_tile_sums<<<(unsigned)ntiles, SCAN_THREADS, 0, c->stream>>>(in, n, sums);
@@ -198,7 +206,13 @@ int device_scan(axb_ctx *c, const uint32_t *in, size_t n, uint32_t *out) {
 int device_scan4(axb_ctx *c, const uint32_t *const in[4], size_t n, uint32_t *const out[4]) {
     size_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
     if (ntiles == 0) ntiles = 1;
-    Scan4 a;
+    Scan4 a{};
+    if (ntiles <= SCAN_SMALL_TILES) {
+        for (int k = 0; k < 4; ++k) { a.in[k] = in[k]; a.out[k] = out[k]; }
+        k_scan_small<<<4, SCAN_THREADS, 0, c->stream>>>(a, n);
+        LAUNCH_CHECK(c);
+        return AXB_OK;
+    }
     for (int k = 0; k < 4; ++k) {
         a.in[k] = in[k];
         a.out[k] = out[k];

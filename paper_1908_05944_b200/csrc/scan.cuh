@@ -151,4 +151,34 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan4_apply(Scan4 a, size_t n)
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = tile_sums[gridDim.x];
 }
 
+// ---- small arrays (one protein: a few tiles) in ONE launch: a single block walks the tiles with a carry;
+// blockIdx.x picks the array, so the four scans of the canonical stage are still one launch
+constexpr size_t SCAN_SMALL_TILES = 4;
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_small(Scan4 a, size_t n) {
+    __shared__ unsigned s_warp[33];
+    const uint32_t *in = a.in[blockIdx.x];
+    uint32_t *out = a.out[blockIdx.x];
+    unsigned carry = 0;
+    for (size_t tile = 0; tile < n; tile += SCAN_TILE) {
+        const size_t base = tile + (size_t)threadIdx.x * SCAN_ITEMS;
+        unsigned item[SCAN_ITEMS];
+        unsigned v = 0;
+#pragma unroll
+        for (int i = 0; i < SCAN_ITEMS; ++i) {
+            item[i] = (base + i < n) ? in[base + i] : 0u;
+            v += item[i];
+        }
+        unsigned total;
+        unsigned ex = block_excl_scan_1024(v, s_warp, total) + carry;     // ends with a barrier: `in` may alias `out`
+#pragma unroll
+        for (int i = 0; i < SCAN_ITEMS; ++i) {
+            if (base + i < n) out[base + i] = ex;
+            ex += item[i];
+        }
+        carry += total;
+    }
+    if (threadIdx.x == 0) out[n] = carry;
+}
+
 }  // namespace axb
