@@ -411,6 +411,10 @@ PruneParams prune_params(axb_ctx *c) {
     P.ctr = c->ctr; P.biomolecule = c->prm.biomolecule;
     P.rank_lo = c->rank_lo; P.rank_hi = c->rank_hi;
     P.k3_cap = c->k3_cap;
+    // n_pt may still be the optimistic capacity (axb_compute); the potential triangles are ~0.8 per potential edge
+    const unsigned warps = (unsigned)c->sm_count * (unsigned)PRUNE_GRID * (unsigned)PRUNE_WARPS;
+    P.claim_tris = prune_claim(std::min<unsigned long long>(c->n_pt, c->n_pe), warps, PRUNE_CLAIM_TRIS);
+    P.claim_edges = prune_claim(c->n_pe, warps, PRUNE_CLAIM_EDGES);
     return P;
 }
 

@@ -48,6 +48,7 @@ struct PruneParams {
     int biomolecule;
     int rank_lo, rank_hi;             // generators this call owns; rows of other generators only receive marks
     uint32_t k3_cap;                  // capacity of k3
+    int claim_tris, claim_edges;      // list entries per lane and work claim (k_prune_tris / k_prune_edges)
 };
 
 // slot of `target` in a generator's partner list; four independent loads per round, no early exit
@@ -108,6 +109,9 @@ __device__ __forceinline__ bool lists_overflowed(const PruneParams &P) {
 #ifndef PRUNE_GRID
 #define PRUNE_GRID 4        // blocks per SM launched = resident blocks (work is claimed dynamically)
 #endif
+#ifndef TETS_CLAIM_V
+#define TETS_CLAIM_V 128
+#endif
 #ifndef TETS_MINB
 #define TETS_MINB 3
 #endif
@@ -119,10 +123,11 @@ __global__ void __launch_bounds__(256, TETS_MINB) k_prune_tets(PruneParams P) {
     // a warp claims 32 tets at a time from a global counter (dense regions make tets very unequal); the
     // next claim is issued before the current chunk is processed
     // DYN = 0: plain grid-stride loop (best while there are only a few tets per thread).
-    // DYN = 1: a warp claims 64 tets at a time from a global counter -- dense regions make tets very
+    // DYN = 1: a warp claims 128 tets at a time from a global counter -- dense regions make tets very
     // unequal -- and issues the next claim before it works on the current one.  Same-address atomics are
-    // served at ~1 per ns, so claims must stay coarse (measured: 32 per claim costs more than it balances).
-    constexpr unsigned CLAIM = 64u;
+    // served at ~1 per ns, so claims must stay coarse (measured at 1M atoms, alpha 1.4: 32 per claim 1.47 ms,
+    // 64 1.23 ms, 128 1.12 ms, 256 1.15 ms and worse in dense cores).
+    constexpr unsigned CLAIM = TETS_CLAIM_V;
     const int lane = lane_id();
     unsigned chunk_n = 0;
     if (DYN && lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[0], 1u);
@@ -207,10 +212,20 @@ constexpr int PRUNE_THREADS = 256;
 // FREE entries onto its own shared-memory stack and runs the expensive part (ortho solve + AC2) whenever
 // 32 are waiting -- packed lanes, no block barriers, and dense regions do not leave other warps idle.
 constexpr int PRUNE_WARPS = PRUNE_THREADS / 32;
-#ifndef PRUNE_CLAIM_V
-#define PRUNE_CLAIM_V 2
+// List entries per lane and claim: coarse claims keep a warp inside one neighbourhood (L1) and spare the shared
+// counter, fine ones keep every warp busy when the list is short.  Measured on B200 (tools/gpu_autotune.sh):
+// 1M atoms 4 / 6 (triangles / edges) beat 2 by 11 / 20 %, 50k atoms want 1; larger than 8 loses to tail imbalance.
+#ifndef PRUNE_CLAIM_TRIS
+#define PRUNE_CLAIM_TRIS 4
 #endif
-constexpr int PRUNE_CLAIM = PRUNE_CLAIM_V;               // list entries per lane and claim (256 per warp)
+#ifndef PRUNE_CLAIM_EDGES
+#define PRUNE_CLAIM_EDGES 6
+#endif
+// host side: the claim for a list of `entries` worked on by `warps` resident warps (at least ~4 claims per warp)
+inline int prune_claim(unsigned long long entries, unsigned warps, int large) {
+    const unsigned long long per = entries / ((unsigned long long)warps * 32ull * 4ull);
+    return (int)(per < 1 ? 1 : per > (unsigned long long)large ? (unsigned long long)large : per);
+}
 constexpr int PRUNE_STACK = 64;              // free entries parked per warp (processed as soon as 32 are waiting)
 
 // pipeline.py:502-505: AC2 for the triangles no kept tet inherited
@@ -249,14 +264,15 @@ __global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_tris(PruneP
 
     // fill the stack from claimed chunks until 32 free entries wait (or the list is exhausted), then settle
     // up to 32 of them -- ONE call site of the expensive part keeps the register allocation tight
-    const unsigned span = 32u * PRUNE_CLAIM;
+    const int claim = P.claim_tris;
+    const unsigned span = 32u * (unsigned)claim;
     unsigned chunk_n = 0, chunk = 0;
-    int b = PRUNE_CLAIM;                              // sub-step inside the current chunk (PRUNE_CLAIM = need a new one)
+    int b = claim;                                    // sub-step inside the current chunk (claim = need a new one)
     bool exhausted = false;
     if (lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[1], 1u);
     for (;;) {
         while (sn < 32 && !exhausted) {
-            if (b == PRUNE_CLAIM) {
+            if (b == claim) {
                 chunk = __shfl_sync(FULL, chunk_n, 0);
                 if ((unsigned long long)chunk * span >= n_pt) { exhausted = true; break; }
                 if (lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[1], 1u);
@@ -310,14 +326,15 @@ __global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_edges(Prune
         }
     };
 
-    const unsigned span = 32u * PRUNE_CLAIM;
+    const int claim = P.claim_edges;
+    const unsigned span = 32u * (unsigned)claim;
     unsigned chunk_n = 0, chunk = 0;
-    int b = PRUNE_CLAIM;
+    int b = claim;
     bool exhausted = false;
     if (lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[2], 1u);
     for (;;) {
         while (sn < 32 && !exhausted) {
-            if (b == PRUNE_CLAIM) {
+            if (b == claim) {
                 chunk = __shfl_sync(FULL, chunk_n, 0);
                 if ((unsigned long long)chunk * span >= n_pe) { exhausted = true; break; }
                 if (lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[2], 1u);
