@@ -86,6 +86,48 @@ def main():
         traffic["_note"] = (f"dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes), ncu --set full, bench workload "
                             f"(1M atoms, alpha 0), capture {tag}")
         json.dump(traffic, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
+    # ---- per-kernel roofline table (alpha 0 from <tag>_ncu_full_raw.csv, alpha 1.4 from <tag>_a14_ncu_full_raw.csv)
+    peak = 6548.2
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    sections = [("1M atoms, alpha = 0", os.path.join(OUT, f"{tag}_ncu_full_raw.csv")),
+                ("1M atoms, alpha = 1.4", os.path.join(OUT, f"{tag}_a14_ncu_full_raw.csv"))]
+    if any(os.path.exists(pth) for _, pth in sections):
+        with open(os.path.join(PROF, f"{tag}_kernel_table.txt"), "w") as f:
+            f.write("# Per-kernel roofline view (ncu --set full --clock-control none; one launch each; times are cold-cache ncu times)\n")
+            f.write(f"# columns: kernel | time us | DRAM MB (read+write) | DRAM GB/s | % of measured {peak:.0f} GB/s | % of nominal 8000 GB/s | "
+                    "FP64 pipe % | warps active % | lanes/instr | warp instr (M)\n")
+            for title, pth in sections:
+                if not os.path.exists(pth):
+                    continue
+                if pth.endswith("_a14_ncu_full_raw.csv"):
+                    shutil.copy(pth, os.path.join(PROF, os.path.basename(pth)))
+                rows = list(csv.reader(open(pth)))
+                hdr, units = rows[0], rows[1]
+                col = {k: hdr.index(k) for k, _ in KEYS if k in hdr}
+                ki = hdr.index("Kernel Name")
+                f.write(f"## {title}\n")
+                seen = set()
+                for r in rows[2:]:
+                    name = r[ki].split("(")[0].replace("void ", "").replace("axb::", "")
+                    if name in seen:
+                        continue
+                    seen.add(name)
+                    ti = col["gpu__time_duration.sum"]
+                    us = float(r[ti].replace(",", "")) * {"ns": 1e-3, "us": 1.0, "ms": 1e3, "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3}.get(units[ti], 1.0)
+                    i0, i1 = col["dram__bytes_read.sum"], col["dram__bytes_write.sum"]
+                    mb = (to_bytes(r[i0].replace(",", ""), units[i0]) + to_bytes(r[i1].replace(",", ""), units[i1])) / 1e6
+                    gbs = mb / us * 1e3
+                    num = lambda key: float(r[col[key]].replace(",", ""))
+                    f.write(f"{name:34s} | {us:8.1f} | {mb:7.1f} | {gbs:7.1f} | {100 * gbs / peak:5.1f} | {100 * gbs / 8000:5.1f} | "
+                            f"{num('sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active'):5.1f} | "
+                            f"{num('sm__warps_active.avg.pct_of_peak_sustained_active'):5.1f} | "
+                            f"{num('smsp__thread_inst_executed_per_inst_executed.ratio'):5.1f} | {num('smsp__inst_executed.sum') / 1e6:7.1f}\n")
+    for name in (f"{tag}_all_configs_one_gpu.jsonl",):
+        if os.path.exists(os.path.join(OUT, name)):
+            shutil.copy(os.path.join(OUT, name), os.path.join(PROF, name))
     # ---- source hot spots
     rep = os.path.join(OUT, f"{tag}_full.ncu-rep")
     if os.path.exists(rep):
