@@ -166,9 +166,10 @@ int axb_compute_host_begin(axb_ctx *ctx, int64_t n, const double *h_xyz, const d
                            const axb_params *params, int64_t capacity[4]);
 int axb_compute_host_finish(axb_ctx *ctx, int64_t *h_vertices, int64_t *h_edges, int64_t *h_triangles,
                             int64_t *h_tets, int64_t counts[4]);
-/* bytes the last axb_compute_host_finish moved device -> host: the rows cross PCIe as int32 (ball
- * indices < 2^31) and host threads widen them to the int64 rows of the reference while later
- * chunks are still in flight (AXB_WIDEN_THREADS overrides the thread count) */
+/* bytes the last axb_compute_host_finish moved device -> host: the rows cross PCIe as three bytes per
+ * value while ball indices fit 24 bits (AXB_WIRE24=0 switches that off), else as int32 (ball indices
+ * < 2^31), and host threads expand them to the int64 rows of the reference while later chunks are
+ * still in flight (AXB_WIDEN_THREADS overrides the thread count) */
 int64_t axb_last_d2h_bytes(const axb_ctx *ctx);
 /* axb_export into HOST buffers (pinned or pageable). */
 int axb_export_host(axb_ctx *ctx, int64_t *h_vertices, int64_t *h_edges, int64_t *h_triangles, int64_t *h_tets);

@@ -1084,15 +1084,15 @@ extern "C" int axb_export(axb_ctx *c, int64_t *d_v, int64_t *d_e, int64_t *d_t, 
         LAUNCH_CHECK(c);
     }
     if (d_e && c->counts[1]) {
-        k_emit_edges<int64_t><<<blocks_for((size_t)c->counts[1], 256), 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->counts[1], nullptr, c->gidx, d_e, c->ctr);
+        k_emit_edges<PlainOut<int64_t>><<<blocks_for((size_t)c->counts[1], 256), 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->counts[1], nullptr, c->gidx, PlainOut<int64_t>{d_e}, c->ctr);
         LAUNCH_CHECK(c);
     }
     if (d_t && c->counts[2]) {
-        k_emit_tris<int64_t><<<blocks_for((size_t)c->counts[2], 256), 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->counts[2], nullptr, c->gidx, d_t, c->ctr);
+        k_emit_tris<PlainOut<int64_t>><<<blocks_for((size_t)c->counts[2], 256), 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->counts[2], nullptr, c->gidx, PlainOut<int64_t>{d_t}, c->ctr);
         LAUNCH_CHECK(c);
     }
     if (d_q && c->counts[3]) {
-        k_emit_tets<int64_t><<<blocks_for((size_t)c->counts[3], 256), 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->counts[3], nullptr, c->gidx, d_q, c->ctr);
+        k_emit_tets<PlainOut<int64_t>><<<blocks_for((size_t)c->counts[3], 256), 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->counts[3], nullptr, c->gidx, PlainOut<int64_t>{d_q}, c->ctr);
         LAUNCH_CHECK(c);
     }
     return mark_event(c, AXB_ST_COUNT + 1);
@@ -1331,6 +1331,17 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     const int wire_mode = getenv("AXB_WIRE") ? atoi(getenv("AXB_WIRE")) : AXB_WIRE_DEFAULT;
     const bool compact1 = (wire_mode & 1) != 0, compact2 = (wire_mode & 2) != 0;
     const int wire_width[4] = {1, compact1 ? 1 : 2, compact2 ? 2 : 3, 4};
+    // 24-bit wire (default while every ball index fits): edges, triangles and tets cross PCIe as three bytes per
+    // value -- per D2H chunk a plane of low halves and a plane of high bytes (canon.cuh: Packed24Out) -- and the
+    // host threads unpack them straight into the int64 rows.  AXB_WIRE24=0 switches it off.
+    const bool p24 = wire_mode == 0 && n < ((size_t)1 << 24) && !(getenv("AXB_WIRE24") && atoi(getenv("AXB_WIRE24")) == 0);
+    if (const char *e = getenv("AXB_D2H_CHUNK")) D2H_CHUNK = std::max<size_t>(1 << 14, (size_t)atol(e));
+    size_t rows_per_chunk_of[4];
+    unsigned chunk_vals[4];
+    for (int d = 0; d < 4; ++d) {
+        rows_per_chunk_of[d] = std::max<size_t>(2, D2H_CHUNK / (size_t)wire_width[d]) & ~(size_t)1;    // even: planes stay aligned
+        chunk_vals[d] = (unsigned)(rows_per_chunk_of[d] * (size_t)wire_width[d]);
+    }
     int32_t *d_out[4];
     size_t stage_off[4], stage_elems = 0;
     for (int d = 0; d < 4; ++d) {
@@ -1361,7 +1372,6 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
         c->h_stage_elems = want;
     }
     if ((st = ensure_pool(c)) != AXB_OK) return st;
-    if (const char *e = getenv("AXB_D2H_CHUNK")) D2H_CHUNK = std::max<size_t>(1 << 14, (size_t)atol(e));
     const size_t max_chunks = stage_elems / D2H_CHUNK + 8;
     while (c->chunk_ev.size() < max_chunks) {
         cudaEvent_t e;
@@ -1401,7 +1411,8 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(3, c->off3 + n)) != AXB_OK) return st;
     k_scatter_tets<<<grid, 256, 0, c->stream>>>(Q);
     LAUNCH_CHECK(c);
-    k_emit_tets<int32_t><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, 0u, c->off3 + n, nullptr, d_out[3], c->ctr);
+    if (p24) k_emit_tets<Packed24Out><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, 0u, c->off3 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[3]), chunk_vals[3]}, c->ctr);
+    else k_emit_tets<PlainOut<int32_t>><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, 0u, c->off3 + n, nullptr, PlainOut<int32_t>{d_out[3]}, c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(3)) != AXB_OK) return st;
     // triangles
@@ -1412,8 +1423,9 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(2, c->off2 + n)) != AXB_OK) return st;
     k_scatter_tris<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[2]);
     LAUNCH_CHECK(c);
-    if (compact2) k_emit_tris<int32_t, true><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, d_out[2], c->ctr);
-    else k_emit_tris<int32_t, false><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, d_out[2], c->ctr);
+    if (p24) k_emit_tris<Packed24Out, false><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[2]), chunk_vals[2]}, c->ctr);
+    else if (compact2) k_emit_tris<PlainOut<int32_t>, true><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, PlainOut<int32_t>{d_out[2]}, c->ctr);
+    else k_emit_tris<PlainOut<int32_t>, false><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, PlainOut<int32_t>{d_out[2]}, c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(2)) != AXB_OK) return st;
     // edges
@@ -1424,8 +1436,9 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(1, c->off1 + n)) != AXB_OK) return st;
     k_scatter_edges<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[1]);
     LAUNCH_CHECK(c);
-    if (compact1) k_emit_edges<int32_t, true><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, d_out[1], c->ctr);
-    else k_emit_edges<int32_t, false><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, d_out[1], c->ctr);
+    if (p24) k_emit_edges<Packed24Out, false><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[1]), chunk_vals[1]}, c->ctr);
+    else if (compact1) k_emit_edges<PlainOut<int32_t>, true><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, PlainOut<int32_t>{d_out[1]}, c->ctr);
+    else k_emit_edges<PlainOut<int32_t>, false><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, PlainOut<int32_t>{d_out[1]}, c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(1)) != AXB_OK) return st;
     // vertices
@@ -1463,6 +1476,8 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
             else if (k.dim == 2 && compact2)
                 c->pool->publish(axb::WK_TRI_ROWS, k.src, k.dst, k.n, WIDEN_PIECE / 2, 2, 3,
                                  reinterpret_cast<const uint32_t *>(c->h_stage + stage_offsets[2]), n, k.row0);
+            else if (k.dim >= 1 && p24)
+                c->pool->publish(axb::WK_UNPACK24, k.src, k.dst, k.n, WIDEN_PIECE, 0, 1, nullptr, k.n, 0);
             else
                 c->pool->publish(axb::WK_WIDEN, k.src, k.dst, k.n, WIDEN_PIECE, 1, 1, nullptr, 0, 0);
             ++pumped;
@@ -1491,8 +1506,23 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
             }
             const size_t rows = (size_t)c->counts[d];
             const size_t w = (size_t)wire_width[d];
-            const size_t rows_per_chunk = std::max<size_t>(1, D2H_CHUNK / w);
+            const size_t rows_per_chunk = rows_per_chunk_of[d];
             int32_t *stage = c->h_stage + stage_off[d];
+            if (d >= 1 && p24) {                              // 3 bytes per value; chunk q starts 3 * q * chunk_vals bytes in
+                CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->dim_ready[d], 0));
+                const char *dev = reinterpret_cast<const char *>(d_out[d]);
+                char *hst = reinterpret_cast<char *>(stage);
+                for (size_t lo = 0; lo < rows; lo += rows_per_chunk) {
+                    const size_t m = std::min(rows_per_chunk, rows - lo);
+                    if (chunks.size() >= c->chunk_ev.size()) return fail(c, AXB_ERR_INTERNAL, "chunk event pool exhausted");
+                    cudaEvent_t ev = c->chunk_ev[chunks.size()];
+                    CUDA_TRY(c, cudaMemcpyAsync(hst + lo * w * 3, dev + lo * w * 3, m * w * 3, cudaMemcpyDeviceToHost, c->copy_stream));
+                    CUDA_TRY(c, cudaEventRecord(ev, c->copy_stream));
+                    chunks.push_back(PendingChunk{ev, reinterpret_cast<const int32_t *>(hst + lo * w * 3), h[d] + lo * w, m * w, d, 0});
+                }
+                c->last_d2h_bytes += (int64_t)(rows * w * 3);
+                continue;
+            }
             const bool compact = (d == 1 && compact1) || (d == 2 && compact2);
             if (compact) {                                    // the row offsets per owner were final before the count was
                 const uint32_t *off = d == 1 ? c->off1 : c->off2;

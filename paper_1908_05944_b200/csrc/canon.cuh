@@ -116,16 +116,38 @@ __global__ void __launch_bounds__(256) k_scatter_tets(CanonParams P) {
 // `map` (optional) renames local ball indices to global ones; it is ascending, so order is preserved.
 __device__ __forceinline__ int64_t mapped(const int64_t *__restrict__ map, int v) { return map ? map[v] : (int64_t)v; }
 
-// OutT = int64_t (the reference dtype, device-resident results) or int32_t (the host path: half the
-// PCIe bytes, widened to int64 by host threads while the next chunk is in flight).
+// Row writers.  PlainOut<int64_t>: the reference dtype (device-resident results).  PlainOut<int32_t>: the host
+// path -- half the PCIe bytes, widened to int64 by host threads while the next chunk is in flight.  Packed24Out:
+// the host path while ball indices fit 24 bits -- three bytes per value.  The value stream is cut into chunks of
+// `chunk_vals` values (one D2H copy each); a chunk of m values is stored as m low halves (uint16) followed by m
+// high bytes, so both planes stay aligned and the host unpacks them with plain vector loads (widen_pool.h).
+template <class T>
+struct PlainOut {
+    T *p;
+    __device__ __forceinline__ void put(size_t idx, int64_t v, size_t) const { p[idx] = (T)v; }
+};
+struct Packed24Out {
+    unsigned char *p;
+    unsigned chunk_vals;          // even
+    __device__ __forceinline__ void put(size_t idx, int64_t v, size_t nvals) const {
+        const size_t first = idx / chunk_vals * chunk_vals;                // all chunks before this one are full
+        const size_t m = min((size_t)chunk_vals, nvals - first);
+        unsigned char *b = p + first * 3;
+        const size_t within = idx - first;
+        *reinterpret_cast<unsigned short *>(b + 2 * within) = (unsigned short)(v & 0xffff);
+        b[2 * m + within] = (unsigned char)(v >> 16);
+    }
+};
+
 // `total_dev` (optional) = device-side row count (the last entry of the offset array): lets the caller
 // launch without knowing the count on the host.
 // SKIP0: write only the columns after the owner (the host rebuilds column 0 from the offsets)
-template <class OutT, bool SKIP0 = false>
+template <class Out, bool SKIP0 = false>
 __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                     unsigned total, const uint32_t *__restrict__ total_dev,
-                                                    const int64_t *__restrict__ map, OutT *__restrict__ out, Counters *ctr) {
+                                                    const int64_t *__restrict__ map, Out out, Counters *ctr) {
     if (total_dev) total = *total_dev;
+    const size_t nvals = (size_t)total * (SKIP0 ? 1 : 2);
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int2 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];
@@ -136,19 +158,20 @@ __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp
         else if (b == me.y && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
     if (SKIP0) {
-        out[pos] = (OutT)mapped(map, me.y);
+        out.put(pos, mapped(map, me.y), nvals);
     } else {
-        out[2 * (size_t)pos] = (OutT)mapped(map, me.x);
-        out[2 * (size_t)pos + 1] = (OutT)mapped(map, me.y);
+        out.put(2 * (size_t)pos, mapped(map, me.x), nvals);
+        out.put(2 * (size_t)pos + 1, mapped(map, me.y), nvals);
     }
     }
 }
 
-template <class OutT, bool SKIP0 = false>
+template <class Out, bool SKIP0 = false>
 __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                    unsigned total, const uint32_t *__restrict__ total_dev,
-                                                   const int64_t *__restrict__ map, OutT *__restrict__ out, Counters *ctr) {
+                                                   const int64_t *__restrict__ map, Out out, Counters *ctr) {
     if (total_dev) total = *total_dev;
+    const size_t nvals = (size_t)total * (SKIP0 ? 2 : 3);
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int4 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];
@@ -159,21 +182,22 @@ __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp,
         else if (o.y == me.y && o.z == me.z && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
     if (SKIP0) {
-        out[2 * (size_t)pos] = (OutT)mapped(map, me.y);
-        out[2 * (size_t)pos + 1] = (OutT)mapped(map, me.z);
+        out.put(2 * (size_t)pos, mapped(map, me.y), nvals);
+        out.put(2 * (size_t)pos + 1, mapped(map, me.z), nvals);
     } else {
-        out[3 * (size_t)pos] = (OutT)mapped(map, me.x);
-        out[3 * (size_t)pos + 1] = (OutT)mapped(map, me.y);
-        out[3 * (size_t)pos + 2] = (OutT)mapped(map, me.z);
+        out.put(3 * (size_t)pos, mapped(map, me.x), nvals);
+        out.put(3 * (size_t)pos + 1, mapped(map, me.y), nvals);
+        out.put(3 * (size_t)pos + 2, mapped(map, me.z), nvals);
     }
     }
 }
 
-template <class OutT>
+template <class Out>
 __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                    unsigned total, const uint32_t *__restrict__ total_dev,
-                                                   const int64_t *__restrict__ map, OutT *__restrict__ out, Counters *ctr) {
+                                                   const int64_t *__restrict__ map, Out out, Counters *ctr) {
     if (total_dev) total = *total_dev;
+    const size_t nvals = (size_t)total * 4;
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int4 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];
@@ -183,10 +207,10 @@ __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp,
         if (o.y < me.y || (o.y == me.y && (o.z < me.z || (o.z == me.z && o.w < me.w)))) ++pos;
         else if (o.y == me.y && o.z == me.z && o.w == me.w && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
-    out[4 * (size_t)pos] = (OutT)mapped(map, me.x);
-    out[4 * (size_t)pos + 1] = (OutT)mapped(map, me.y);
-    out[4 * (size_t)pos + 2] = (OutT)mapped(map, me.z);
-    out[4 * (size_t)pos + 3] = (OutT)mapped(map, me.w);
+    out.put(4 * (size_t)pos, mapped(map, me.x), nvals);
+    out.put(4 * (size_t)pos + 1, mapped(map, me.y), nvals);
+    out.put(4 * (size_t)pos + 2, mapped(map, me.z), nvals);
+    out.put(4 * (size_t)pos + 3, mapped(map, me.w), nvals);
     }
 }
 

@@ -34,7 +34,9 @@ namespace axb {
 //   TRI_ROWS  same for triangles: (owner, src[2r], src[2r + 1]) -- 8 instead of 12 bytes per triangle
 //   IOTA      n consecutive values starting at row0 (all vertices kept: nothing crosses PCIe)
 //   COPY      n int32 values copied verbatim (pageable input -> pinned staging, in parallel)
-enum WidenKind { WK_WIDEN = 0, WK_EDGE_ROWS = 1, WK_TRI_ROWS = 2, WK_IOTA = 3, WK_COPY = 4 };
+//   UNPACK24  n values of a 24-bit chunk: src = chunk base, n_index = values in the chunk (the high bytes start
+//             2 * n_index bytes in), row0 = first value of this task inside the chunk
+enum WidenKind { WK_WIDEN = 0, WK_EDGE_ROWS = 1, WK_TRI_ROWS = 2, WK_IOTA = 3, WK_COPY = 4, WK_UNPACK24 = 5 };
 
 struct WidenTask {
     const int32_t *src;
@@ -68,6 +70,32 @@ inline void widen_rows(const int32_t *src, int64_t *dst, size_t n) {
     if (have_avx2) { widen_avx2(src, dst, n); return; }
 #endif
     for (size_t i = 0; i < n; ++i) dst[i] = src[i];
+}
+
+// 24-bit wire format (ball indices < 2^24): a chunk of m values arrives as m low halves (uint16) followed by
+// m high bytes; three bytes per value instead of four cross PCIe
+#if defined(__x86_64__)
+__attribute__((target("avx2"))) inline void unpack24_avx2(const uint16_t *lo, const uint8_t *hi, int64_t *dst, size_t n) {
+    size_t i = 0;
+    while (i < n && (reinterpret_cast<uintptr_t>(dst + i) & 31u)) { dst[i] = (int64_t)lo[i] | ((int64_t)hi[i] << 16); ++i; }
+    for (; i + 8 <= n; i += 8) {
+        const __m256i l = _mm256_cvtepu16_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i *>(lo + i)));
+        const __m256i h = _mm256_cvtepu8_epi32(_mm_loadl_epi64(reinterpret_cast<const __m128i *>(hi + i)));
+        const __m256i v = _mm256_or_si256(l, _mm256_slli_epi32(h, 16));
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i), _mm256_cvtepi32_epi64(_mm256_castsi256_si128(v)));
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i + 4), _mm256_cvtepi32_epi64(_mm256_extracti128_si256(v, 1)));
+    }
+    for (; i < n; ++i) dst[i] = (int64_t)lo[i] | ((int64_t)hi[i] << 16);
+    _mm_sfence();
+}
+#endif
+
+inline void unpack24(const uint16_t *lo, const uint8_t *hi, int64_t *dst, size_t n) {
+#if defined(__x86_64__)
+    static const bool have_avx2 = __builtin_cpu_supports("avx2");
+    if (have_avx2) { unpack24_avx2(lo, hi, dst, n); return; }
+#endif
+    for (size_t i = 0; i < n; ++i) dst[i] = (int64_t)lo[i] | ((int64_t)hi[i] << 16);
 }
 
 // copy with non-temporal stores: the destination is a DMA source next, and a copy engine reading lines that
@@ -194,6 +222,10 @@ inline void run_task(const WidenTask &t) {
         break;
     case WK_COPY:
         copy_for_dma(t.src, t.dst, t.n * sizeof(int32_t));
+        break;
+    case WK_UNPACK24:
+        unpack24(reinterpret_cast<const uint16_t *>(t.src) + t.row0,
+                 reinterpret_cast<const uint8_t *>(t.src) + 2 * t.n_index + t.row0, t.dst, t.n);
         break;
     case WK_EDGE_ROWS:
     case WK_TRI_ROWS: {

@@ -27,10 +27,20 @@ int main() {
     int64_t *w = (int64_t *)aligned_alloc(64, ((size_t)tot * 2 + 8) * 8);
     int64_t *io = (int64_t *)aligned_alloc(64, (n + 8) * 8);
     int bad = 0;
+    const size_t m24 = 50003;                           // odd: the high-byte plane starts at an odd multiple of 2
+    std::vector<int64_t> v24(m24);
+    std::vector<unsigned char> p24(3 * m24 + 64);
+    for (size_t i = 0; i < m24; ++i) {
+        v24[i] = (int64_t)(((unsigned)rand() << 9 ^ (unsigned)rand()) & 0xffffffu);
+        const uint16_t lo16 = (uint16_t)(v24[i] & 0xffff);
+        memcpy(p24.data() + 2 * i, &lo16, 2);
+        p24[2 * m24 + i] = (unsigned char)(v24[i] >> 16);
+    }
+    int64_t *u24 = (int64_t *)aligned_alloc(64, (m24 + 8) * 8);
     WidenPool pool(3);
     for (int round = 0; round < 3; ++round) {           // the pool is reused run after run
         const size_t piece = round == 0 ? 1000 : (round == 1 ? 4099 : 70000);
-        pool.begin(4 * (tot / piece + 2) + n / piece + 8);
+        pool.begin(4 * (tot / piece + 2) + n / piece + m24 / piece + 16);
         // chunks at odd row boundaries, like the D2H chunks
         const size_t cut = tot / 3 + round;
         pool.publish(WK_EDGE_ROWS, b.data(), e, cut, piece, 1, 2, off.data(), n, 0);
@@ -39,7 +49,11 @@ int main() {
         pool.publish(WK_TRI_ROWS, bc.data() + 2 * cut, t + 3 * cut, tot - cut, piece, 2, 3, off.data(), n, cut);
         pool.publish(WK_WIDEN, bc.data(), w, (size_t)tot * 2, piece, 1, 1, nullptr, 0, 0);
         pool.publish(WK_IOTA, nullptr, io, n, piece, 0, 1, nullptr, 0, 0);
+        // a 24-bit chunk: m low halves, then m high bytes; the tasks of the chunk share its base pointer
+        pool.publish(WK_UNPACK24, reinterpret_cast<const int32_t *>(p24.data()), u24, m24, piece, 0, 1, nullptr, m24, 0);
         pool.finish();
+        for (size_t i = 0; i < m24; ++i) if (u24[i] != v24[i]) ++bad;
+        for (size_t i = 0; i < m24; ++i) u24[i] = -1;
         size_t a = 0;
         for (size_t r = 0; r < tot; ++r) {
             while (r >= off[a + 1]) ++a;

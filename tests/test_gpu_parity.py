@@ -401,6 +401,22 @@ def test_compact_wire_formats_of_the_host_path(monkeypatch):
         for a, b in zip(plain, compact):
             assert a.dtype == np.int64 and np.array_equal(a, b), f"AXB_WIRE={mode}"
     monkeypatch.delenv("AXB_WIRE")
+    # the default is the 24-bit format (ball indices < 2^24): three bytes per value, planes of low halves and high
+    # bytes per D2H chunk; AXB_WIRE24=0 sends int32.  Small chunks make the lists span many (and ragged) chunks.
+    two_call = eng.compute_host(c, r, cfg, pipelined=False)
+    for chunk in ("", "16384", "50000"):
+        if chunk:
+            monkeypatch.setenv("AXB_D2H_CHUNK", chunk)
+        for w24 in ("1", "0"):
+            monkeypatch.setenv("AXB_WIRE24", w24)
+            got = eng.compute_host(c, r, cfg)
+            wire = int(eng.lib.axb_last_d2h_bytes(eng.handle))
+            values = sum(int(a.size) for a in got[1:])
+            assert wire == values * (3 if w24 == "1" else 4), (w24, chunk)
+            for a, b in zip(two_call, got):
+                assert a.dtype == np.int64 and np.array_equal(a, b), f"AXB_WIRE24={w24} chunk={chunk}"
+    monkeypatch.delenv("AXB_WIRE24")
+    monkeypatch.setenv("AXB_D2H_CHUNK", str(1 << 19))
     # vertices dropped by the general vertex step (not every vertex kept): the plain int32 path for dimension 0
     rng = np.random.default_rng(3)
     c2 = rng.uniform(0, 30, size=(3000, 3))
