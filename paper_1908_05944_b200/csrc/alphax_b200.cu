@@ -1337,10 +1337,12 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     const bool p24 = wire_mode == 0 && n < ((size_t)1 << 24) && !(getenv("AXB_WIRE24") && atoi(getenv("AXB_WIRE24")) == 0);
     if (const char *e = getenv("AXB_D2H_CHUNK")) D2H_CHUNK = std::max<size_t>(1 << 14, (size_t)atol(e));
     size_t rows_per_chunk_of[4];
-    unsigned chunk_vals[4];
+    unsigned rows_shift[4];
     for (int d = 0; d < 4; ++d) {
-        rows_per_chunk_of[d] = std::max<size_t>(2, D2H_CHUNK / (size_t)wire_width[d]) & ~(size_t)1;    // even: planes stay aligned
-        chunk_vals[d] = (unsigned)(rows_per_chunk_of[d] * (size_t)wire_width[d]);
+        rows_per_chunk_of[d] = std::max<size_t>(1, D2H_CHUNK / (size_t)wire_width[d]);
+        rows_shift[d] = 1;                                    // 24-bit planes: a power of two of whole rows per chunk
+        while (((size_t)2 << rows_shift[d]) <= rows_per_chunk_of[d]) ++rows_shift[d];
+        if (p24 && d >= 1) rows_per_chunk_of[d] = (size_t)1 << rows_shift[d];
     }
     int32_t *d_out[4];
     size_t stage_off[4], stage_elems = 0;
@@ -1411,7 +1413,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(3, c->off3 + n)) != AXB_OK) return st;
     k_scatter_tets<<<grid, 256, 0, c->stream>>>(Q);
     LAUNCH_CHECK(c);
-    if (p24) k_emit_tets<Packed24Out><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, 0u, c->off3 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[3]), chunk_vals[3]}, c->ctr);
+    if (p24) k_emit_tets<Packed24Out><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, 0u, c->off3 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[3]), rows_shift[3]}, c->ctr);
     else k_emit_tets<PlainOut<int32_t>><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, 0u, c->off3 + n, nullptr, PlainOut<int32_t>{d_out[3]}, c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(3)) != AXB_OK) return st;
@@ -1423,7 +1425,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(2, c->off2 + n)) != AXB_OK) return st;
     k_scatter_tris<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[2]);
     LAUNCH_CHECK(c);
-    if (p24) k_emit_tris<Packed24Out, false><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[2]), chunk_vals[2]}, c->ctr);
+    if (p24) k_emit_tris<Packed24Out, false><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[2]), rows_shift[2]}, c->ctr);
     else if (compact2) k_emit_tris<PlainOut<int32_t>, true><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, PlainOut<int32_t>{d_out[2]}, c->ctr);
     else k_emit_tris<PlainOut<int32_t>, false><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, PlainOut<int32_t>{d_out[2]}, c->ctr);
     LAUNCH_CHECK(c);
@@ -1436,7 +1438,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(1, c->off1 + n)) != AXB_OK) return st;
     k_scatter_edges<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[1]);
     LAUNCH_CHECK(c);
-    if (p24) k_emit_edges<Packed24Out, false><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[1]), chunk_vals[1]}, c->ctr);
+    if (p24) k_emit_edges<Packed24Out, false><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[1]), rows_shift[1]}, c->ctr);
     else if (compact1) k_emit_edges<PlainOut<int32_t>, true><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, PlainOut<int32_t>{d_out[1]}, c->ctr);
     else k_emit_edges<PlainOut<int32_t>, false><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, PlainOut<int32_t>{d_out[1]}, c->ctr);
     LAUNCH_CHECK(c);

@@ -119,23 +119,34 @@ __device__ __forceinline__ int64_t mapped(const int64_t *__restrict__ map, int v
 // Row writers.  PlainOut<int64_t>: the reference dtype (device-resident results).  PlainOut<int32_t>: the host
 // path -- half the PCIe bytes, widened to int64 by host threads while the next chunk is in flight.  Packed24Out:
 // the host path while ball indices fit 24 bits -- three bytes per value.  The value stream is cut into chunks of
-// `chunk_vals` values (one D2H copy each); a chunk of m values is stored as m low halves (uint16) followed by m
+// whole rows (one D2H copy each); a chunk of m values is stored as m low halves (uint16) followed by m
 // high bytes, so both planes stay aligned and the host unpacks them with plain vector loads (widen_pool.h).
 template <class T>
 struct PlainOut {
     T *p;
-    __device__ __forceinline__ void put(size_t idx, int64_t v, size_t) const { p[idx] = (T)v; }
+    struct Row {
+        T *q;
+        __device__ __forceinline__ void put(int c, int64_t v) const { q[c] = (T)v; }
+    };
+    __device__ __forceinline__ Row row(size_t pos, size_t, int K) const { return Row{p + (size_t)K * pos}; }
 };
 struct Packed24Out {
     unsigned char *p;
-    unsigned chunk_vals;          // even
-    __device__ __forceinline__ void put(size_t idx, int64_t v, size_t nvals) const {
-        const size_t first = idx / chunk_vals * chunk_vals;                // all chunks before this one are full
-        const size_t m = min((size_t)chunk_vals, nvals - first);
-        unsigned char *b = p + first * 3;
-        const size_t within = idx - first;
-        *reinterpret_cast<unsigned short *>(b + 2 * within) = (unsigned short)(v & 0xffff);
-        b[2 * m + within] = (unsigned char)(v >> 16);
+    unsigned rows_shift;          // a chunk holds 1 << rows_shift whole rows (so a row never straddles two chunks)
+    struct Row {
+        unsigned short *lo;
+        unsigned char *hi;
+        __device__ __forceinline__ void put(int c, int64_t v) const {
+            lo[c] = (unsigned short)(v & 0xffff);
+            hi[c] = (unsigned char)(v >> 16);
+        }
+    };
+    __device__ __forceinline__ Row row(size_t pos, size_t total_rows, int K) const {
+        const size_t first = pos >> rows_shift << rows_shift;              // all chunks before this one are full
+        const size_t m = min((size_t)1 << rows_shift, total_rows - first) * (size_t)K;     // values in this chunk
+        unsigned char *b = p + first * (size_t)K * 3;
+        const size_t within = (pos - first) * (size_t)K;
+        return Row{reinterpret_cast<unsigned short *>(b) + within, b + 2 * m + within};
     }
 };
 
@@ -147,7 +158,6 @@ __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp
                                                     unsigned total, const uint32_t *__restrict__ total_dev,
                                                     const int64_t *__restrict__ map, Out out, Counters *ctr) {
     if (total_dev) total = *total_dev;
-    const size_t nvals = (size_t)total * (SKIP0 ? 1 : 2);
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int2 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];
@@ -158,10 +168,11 @@ __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp
         else if (b == me.y && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
     if (SKIP0) {
-        out.put(pos, mapped(map, me.y), nvals);
+        out.row(pos, total, 1).put(0, mapped(map, me.y));
     } else {
-        out.put(2 * (size_t)pos, mapped(map, me.x), nvals);
-        out.put(2 * (size_t)pos + 1, mapped(map, me.y), nvals);
+        const auto w = out.row(pos, total, 2);
+        w.put(0, mapped(map, me.x));
+        w.put(1, mapped(map, me.y));
     }
     }
 }
@@ -171,7 +182,6 @@ __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp,
                                                    unsigned total, const uint32_t *__restrict__ total_dev,
                                                    const int64_t *__restrict__ map, Out out, Counters *ctr) {
     if (total_dev) total = *total_dev;
-    const size_t nvals = (size_t)total * (SKIP0 ? 2 : 3);
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int4 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];
@@ -182,12 +192,14 @@ __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp,
         else if (o.y == me.y && o.z == me.z && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
     if (SKIP0) {
-        out.put(2 * (size_t)pos, mapped(map, me.y), nvals);
-        out.put(2 * (size_t)pos + 1, mapped(map, me.z), nvals);
+        const auto w = out.row(pos, total, 2);
+        w.put(0, mapped(map, me.y));
+        w.put(1, mapped(map, me.z));
     } else {
-        out.put(3 * (size_t)pos, mapped(map, me.x), nvals);
-        out.put(3 * (size_t)pos + 1, mapped(map, me.y), nvals);
-        out.put(3 * (size_t)pos + 2, mapped(map, me.z), nvals);
+        const auto w = out.row(pos, total, 3);
+        w.put(0, mapped(map, me.x));
+        w.put(1, mapped(map, me.y));
+        w.put(2, mapped(map, me.z));
     }
     }
 }
@@ -197,7 +209,6 @@ __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp,
                                                    unsigned total, const uint32_t *__restrict__ total_dev,
                                                    const int64_t *__restrict__ map, Out out, Counters *ctr) {
     if (total_dev) total = *total_dev;
-    const size_t nvals = (size_t)total * 4;
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int4 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];
@@ -207,10 +218,11 @@ __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp,
         if (o.y < me.y || (o.y == me.y && (o.z < me.z || (o.z == me.z && o.w < me.w)))) ++pos;
         else if (o.y == me.y && o.z == me.z && o.w == me.w && q != s) atomicOr(&ctr->overflow, 1u << 5);
     }
-    out.put(4 * (size_t)pos, mapped(map, me.x), nvals);
-    out.put(4 * (size_t)pos + 1, mapped(map, me.y), nvals);
-    out.put(4 * (size_t)pos + 2, mapped(map, me.z), nvals);
-    out.put(4 * (size_t)pos + 3, mapped(map, me.w), nvals);
+    const auto w = out.row(pos, total, 4);
+    w.put(0, mapped(map, me.x));
+    w.put(1, mapped(map, me.y));
+    w.put(2, mapped(map, me.z));
+    w.put(3, mapped(map, me.w));
     }
 }
 
