@@ -111,7 +111,7 @@ constexpr int E2_GB = E2_GB_V;                // generators per warp batch
 constexpr int E2_ROWS = 13;                   // rows of the 5x5x5 block that can out-rank the generator
 constexpr int E2_ITEMS = E2_GB * E2_ROWS;     // 104 row items, 4 rounds of 32 lanes
 #ifndef E2_CCAP_V
-#define E2_CCAP_V 384
+#define E2_CCAP_V 512
 #endif
 #ifndef E2_QCAP_V
 #define E2_QCAP_V 320
