@@ -34,18 +34,34 @@ namespace axb {
 #endif
 constexpr int T3_WARPS = T3_WARPS_V;      // warps per block (each one is independent)
 // Tile shapes (template parameter SHAPE): the light shape packs lanes best when a generator has ~11 partner
-// pairs (alpha = 0); the heavy shape halves the tile so that 24 instead of 16 warps fit an SM (80 registers,
-// 6.5 KB of shared memory per warp) -- measured 8-10 % faster once generators have 40+ pairs (alpha = 1.4,
+// pairs (alpha = 0); the heavy shape shrinks the tile (6 generators) so that 24 instead of 16 warps fit an SM (80 registers,
+// ~7 KB of shared memory per warp) -- measured 8-10 % faster once generators have 40+ pairs (alpha = 1.4,
 // dense cores), 9 % slower at alpha = 0.
 enum { T3_LIGHT = 0, T3_HEAVY = 1 };
 constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved as soon as 256 are waiting)
 
+// heavy tile shape (tuning knobs, tools/gpu_autotune.sh: 6 generators / 160 triangles per round beat 8 / 112 by 5 % at
+// 1M atoms, alpha 1.4 -- 8 generators with ~10 partners each overflow the 64 slots and split the tile -- and by 2 % in
+// dense cores; 4 generators or more slots per tile lose)
+#ifndef T3H_GENS
+#define T3H_GENS 6
+#endif
+#ifndef T3H_SCAP
+#define T3H_SCAP 64
+#endif
+#ifndef T3H_TCAP
+#define T3H_TCAP 160
+#endif
+#ifndef T3H_MINB
+#define T3H_MINB 6
+#endif
+
 template <int W, int SHAPE>
 struct T3Cfg {
-    static constexpr int GENS = (W == 1 && SHAPE == T3_HEAVY) ? 8 : 16;                      // generators per warp tile (<= 16)
-    static constexpr int SCAP = W == 1 ? (SHAPE == T3_HEAVY ? 64 : 128) : 256;   // partner slots per sub-pass (>= 64 * W)
-    static constexpr int TCAP = W == 1 ? (SHAPE == T3_HEAVY ? 112 : 224) : 512;  // triangles per round
-    static constexpr int MINB = W == 1 ? (SHAPE == T3_HEAVY ? 6 : 4) : 1;        // resident blocks per SM the registers must allow
+    static constexpr int GENS = (W == 1 && SHAPE == T3_HEAVY) ? T3H_GENS : 16;                      // generators per warp tile (<= 16)
+    static constexpr int SCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_SCAP : 128) : 256;   // partner slots per sub-pass (>= 64 * W)
+    static constexpr int TCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_TCAP : 224) : 512;  // triangles per round
+    static constexpr int MINB = W == 1 ? (SHAPE == T3_HEAVY ? T3H_MINB : 4) : 1;        // resident blocks per SM the registers must allow
     static constexpr int NA = SCAP + GENS;              // atom index space: partner slots, then the tile's generators
     static constexpr bool FLAT = W == 1 && SHAPE == T3_LIGHT;   // flattened pair enumeration (pays while degrees are small)
     static constexpr int PTAB = FLAT ? 8 * SCAP : 32;   // partner pairs of a sub-pass covered by the stamped pair table
