@@ -430,6 +430,10 @@ int launch_edges(axb_ctx *c, const EstParams &P, int lo, int hi) {
 int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
     EstParams P = est_params(c, report_key);
     const int ngen = c->rank_hi - c->rank_lo;
+#ifndef TETS_DYN_PAIRS
+#define TETS_DYN_PAIRS 20      // more partner pairs per generator than this: k_prune_tets claims chunks (1M atoms: the static
+                               // loop wins up to alpha 0.4 = 0.36 vs 0.41 ms, a tie at 0.6, claims from alpha 0.8 = 0.67 vs 0.69 ms)
+#endif
 #ifndef T3_HEAVY_PAIRS
 #define T3_HEAVY_PAIRS 25     // more partner pairs per generator than this: heavy tile shape (1M atoms: light wins up to
                               // alpha 0.6 = 0.99 vs 1.09 ms, heavy from alpha 0.8 = 1.32 vs 1.36 ms; tools/gpu_alpha_scan.py)
@@ -449,7 +453,7 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
         };
         int st;
         const bool heavy = c->h->ctr.pair_bound > (unsigned long long)T3_HEAVY_PAIRS * (unsigned long long)std::max(ngen, 1);   // partner pairs per generator
-        c->many_tets = c->h->ctr.pair_bound > 20ull * (unsigned long long)std::max(ngen, 1);     // k_prune_tets variant (tuned separately)
+        c->many_tets = c->h->ctr.pair_bound > (unsigned long long)TETS_DYN_PAIRS * (unsigned long long)std::max(ngen, 1);   // k_prune_tets variant
         if (c->W != 1) st = launch(k_tri_tet3<4, T3_LIGHT>, sizeof(T3Warp<4, T3_LIGHT>), T3Cfg<4, T3_LIGHT>::GENS, 1);
         else if (heavy) st = launch(k_tri_tet3<1, T3_HEAVY>, sizeof(T3Warp<1, T3_HEAVY>), T3Cfg<1, T3_HEAVY>::GENS, T3Cfg<1, T3_HEAVY>::MINB);
         else st = launch(k_tri_tet3<1, T3_LIGHT>, sizeof(T3Warp<1, T3_LIGHT>), T3Cfg<1, T3_LIGHT>::GENS, T3Cfg<1, T3_LIGHT>::MINB);
