@@ -7,7 +7,6 @@
 #include "canon.cuh"
 #include "common.cuh"
 #include "estimate.cuh"
-#include "estimate2.cuh"
 #include "estimate3.cuh"
 #include "grid.cuh"
 #include "predicates.cuh"
@@ -114,7 +113,7 @@ struct axb_ctx {
     int64_t host_cap[4] = {0, 0, 0, 0};
     size_t mark_after_grid = 0, mark_after_edges = 0;
     int cull_mask = 1;                    // bit 0: tets, bit 1: triangles (A/B switch AXB_CULL=0..3)
-    bool cull = false;                    // one-call path: k_tri_tet2 settles partner-dominated simplices itself
+    bool cull = false;                    // one-call path: k_tri_tet3 settles partner-dominated simplices itself
     bool slab_mode = false;               // grid geometry fixed by the caller (one z-slab of a global grid)
     bool many_tets = false;               // > 20 partner pairs per generator: heavy tile shape, claimed tet chunks
     bool defer_dup = false;               // one-call paths: the duplicate-centre check rides on the edge stage's host sync
@@ -438,10 +437,6 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
 #define T3_HEAVY_PAIRS 25     // more partner pairs per generator than this: heavy tile shape (1M atoms: light wins up to
                               // alpha 0.6 = 0.99 vs 1.09 ms, heavy from alpha 0.8 = 1.32 vs 1.36 ms; tools/gpu_alpha_scan.py)
 #endif
-#ifndef AXB_T3
-#define AXB_T3 1
-#endif
-#if AXB_T3
     {   // warp-autonomous tiles (estimate3.cuh); the tile shape follows the work per generator
         CUDA_TRY(c, cudaMemsetAsync(&c->ctr->tile_next, 0, sizeof(unsigned int), c->stream));
         auto launch = [&](auto kernel, size_t warp_bytes, int gens, int minb) -> int {
@@ -461,19 +456,6 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
         LAUNCH_CHECK(c);
         return AXB_OK;
     }
-#endif
-    const unsigned ntiles = (unsigned)std::max(1, (ngen + T2_GENS - 1) / T2_GENS);
-    if (c->W == 1) {
-        const size_t smem = sizeof(T2Smem<1>);
-        CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_tri_tet2<1><<<std::min(ntiles, (unsigned)c->sm_count * (unsigned)T2_MINB), T2_THREADS, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
-    } else {
-        const size_t smem = sizeof(T2Smem<4>);
-        CUDA_TRY(c, cudaFuncSetAttribute(k_tri_tet2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_tri_tet2<4><<<std::min(ntiles, (unsigned)c->sm_count), T2_THREADS, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
-    }
-    LAUNCH_CHECK(c);
-    return AXB_OK;
 }
 
 // turn the smallest singular key into the reference's DegenerateSimplex report

@@ -9,7 +9,7 @@
 //             tests, warp-ballot/popc compaction into the partner lists (ascending
 //             rank).  Lists are staged in warp-private shared memory and flushed with
 //             ONE global atomicAdd per ~32 generators.
-// Potential triangles and tets: estimate2.cuh.
+// Potential triangles and tets: estimate3.cuh.
 #pragma once
 
 #include "common.cuh"
@@ -46,7 +46,7 @@ struct EstParams {
     Counters *ctr;
     ErrRecord *errs;
     unsigned long long report_key;   // != 0: only the solve with this key writes errs[0]
-    int cull;                        // k_tri_tet2: drop / flag simplices dominated by a partner of their generator
+    int cull;                        // k_tri_tet3: drop / flag simplices dominated by a partner of their generator
 };
 
 __device__ __forceinline__ void sort_small(int *v, int k) {

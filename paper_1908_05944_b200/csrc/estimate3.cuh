@@ -1,12 +1,10 @@
 // estimate3.cuh -- potential triangles and tetrahedra, warp-autonomous tiles
 // (reference pipeline.py:373-479).
 //
-// estimate2.cuh ran a block per tile of 64-128 generators with ~16 block barriers per tile; its
-// profile showed a quarter of all stall cycles at those barriers and a tet compaction that parked
-// the whole block behind one global atomic.  Here every WARP owns a tile of 16 consecutive
-// generators and its own slice of shared memory; nothing but __syncwarp separates the phases, so
-// the four warps of a block (and the blocks of an SM) drift apart and hide each other's fp64
-// dependency chains:
+// Every WARP owns a tile of up to 16 consecutive generators and its own slice of shared memory;
+// nothing but __syncwarp separates the phases, so the warps of a block (and the blocks of an SM)
+// drift apart and hide each other's fp64 dependency chains (a block-per-tile predecessor spent a
+// quarter of its stall cycles at block barriers):
 //   A  stage the partner atoms of the tile (generators and partners share ONE index space in
 //      shared memory, so "sort the vertices by ball index" is a sort of four small integers
 //      followed by loads in sorted order -- no 32-byte records are swapped in registers)
@@ -24,7 +22,6 @@
 
 #include "common.cuh"
 #include "estimate.cuh"
-#include "estimate2.cuh"      // owner_of, nth_bit_multi
 #include "predicates.cuh"
 
 namespace axb {
@@ -91,6 +88,29 @@ struct T3Warp {
     unsigned char sgen[C::SCAP], sli[C::SCAP];
     unsigned char ptab[C::PTAB];               // pair number -> first slot of the pair (phase B, flattened enumeration)
 };
+
+// largest idx in [0, n) with pre[idx] <= v (pre = exclusive prefix, pre[0] = 0)
+__device__ __forceinline__ int owner_of(const int *pre, int n, int v) {
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (pre[mid] <= v) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// position of the nth set bit of a W-word row (-1 if there are fewer)
+template <int W>
+__device__ __forceinline__ int nth_bit_multi(const unsigned long long *row, int nth) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        unsigned long long m = row[w];
+        int c = __popcll(m);
+        if (nth < c) return 64 * w + nth_set_bit(m, nth);
+        nth -= c;
+    }
+    return -1;
+}
 
 // exclusive scan of a[0..n) in place by one warp; a[n] = total; returns the total
 __device__ __forceinline__ int warp_scan_excl(int *a, int n) {

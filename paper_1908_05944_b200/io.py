@@ -14,7 +14,7 @@ import ctypes as C
 
 import numpy as np
 
-import math
+import re
 
 from . import __version__, _native as N
 from .errors import AlphaxError, MalformedLine, NonFiniteValue, NonPositiveRadius
@@ -22,27 +22,30 @@ from .pipeline import AlphaComplex, complex_stats
 from .types import Ball
 
 
+def _xyzr_record(lineno: int, raw: str):
+    """One record line -> (x, y, z, r) or None for a blank / comment line; raises what the reference raises
+    for that line (io.py:85-100: field count, then numeric, then finite, then positive radius)."""
+    body = raw.partition("#")[0].split()
+    if not body:
+        return None
+    if len(body) != 4:
+        raise MalformedLine(lineno, f"expected 4 fields, got {len(body)}")
+    try:
+        rec = tuple(map(float, body))
+    except ValueError:
+        raise MalformedLine(lineno, f"non-numeric field in {raw!r}") from None
+    if not np.isfinite(rec).all():
+        raise NonFiniteValue(lineno, f"non-finite value in {raw!r}")
+    if rec[3] <= 0.0:
+        raise NonPositiveRadius(lineno, rec[3])
+    return rec
+
+
 def _xyzr_slow_scan(text: str):
-    """Line-by-line pass with the reference's checks in the reference's order (io.py:85-100);
-    only reached when the vectorised pass saw something irregular, to raise the right error."""
-    rows = []
-    for lineno, raw in enumerate(text.splitlines(), start=1):
-        line = raw.split("#", 1)[0].strip()
-        if not line:
-            continue
-        parts = line.split()
-        if len(parts) != 4:
-            raise MalformedLine(lineno, f"expected 4 fields, got {len(parts)}")
-        try:
-            x, y, z, r = (float(p) for p in parts)
-        except ValueError:
-            raise MalformedLine(lineno, f"non-numeric field in {raw!r}") from None
-        if not all(math.isfinite(v) for v in (x, y, z, r)):
-            raise NonFiniteValue(lineno, f"non-finite value in {raw!r}")
-        if r <= 0.0:
-            raise NonPositiveRadius(lineno, r)
-        rows.append((x, y, z, r))
-    return np.asarray(rows, dtype=np.float64).reshape(-1, 4)
+    """Record-by-record pass, only reached when the vectorised pass saw something irregular: it exists to
+    raise the reference's error for the FIRST offending line (same type, message and line number)."""
+    recs = (_xyzr_record(no, raw) for no, raw in enumerate(text.splitlines(), 1))
+    return np.array([r for r in recs if r is not None], dtype=np.float64).reshape(-1, 4)
 
 
 def parse_xyzr_arrays(text: str):
@@ -85,8 +88,8 @@ def format_xyzr_arrays(centers, radii) -> str:
 
 
 def format_xyzr(balls) -> str:
-    lines = [f"{b.center[0]!r} {b.center[1]!r} {b.center[2]!r} {b.radius!r}" for b in balls]
-    return "\n".join(lines) + ("\n" if lines else "")
+    """Reference signature (io.py:104-106) over the array formatter."""
+    return format_xyzr_arrays([b.center for b in balls], [b.radius for b in balls])
 
 
 def write_complex(k: AlphaComplex, version: str = __version__) -> str:
@@ -107,42 +110,67 @@ def write_complex(k: AlphaComplex, version: str = __version__) -> str:
     return header + buf.raw[: need.value].decode("ascii")
 
 
+_HEADER = re.compile(r"\s*alphax\s+\S+\s+n=(\S*)\s+alpha=(\S*)\s*\Z")
+
+
+def _complex_line_error(lineno: int, raw: str, n: int):
+    """The reference's verdict on one simplex line (io.py:258-271), in its order of checks."""
+    try:
+        dim, *verts = (int(f) for f in raw.split())
+    except ValueError:
+        return MalformedLine(lineno, f"non-integer field in {raw!r}")
+    if dim not in (0, 1, 2, 3) or len(verts) != dim + 1:
+        return MalformedLine(lineno, f"bad simplex record {raw!r}")
+    if not all(0 <= v < n for v in verts):
+        return MalformedLine(lineno, "vertex index out of range")
+    if sorted(set(verts)) != verts:
+        return MalformedLine(lineno, "vertices must be strictly increasing")
+    return None
+
+
 def read_complex(text: str) -> AlphaComplex:
-    """Inverse of ``write_complex``; validates header, arity, index range and row order."""
+    """Inverse of ``write_complex`` (reference io.py:239-280): validates header, arity, index range and
+    strictly increasing rows.  The body is parsed in bulk -- one numpy conversion of all tokens, the checks
+    as array operations per dimension -- because a 10^7-simplex document is 10^8 tokens; only when a check
+    fails are the lines re-read one by one to raise the reference's error for the first offender."""
     lines = text.splitlines()
     if not lines:
         raise MalformedLine(1, "empty document")
-    head = lines[0].split()
-    ok = len(head) == 4 and head[0] == "alphax" and head[2].startswith("n=") and head[3].startswith("alpha=")
+    head = _HEADER.match(lines[0])
     try:
-        n = int(head[2][2:]) if ok else 0
-        alpha = float(head[3][6:]) if ok else 0.0
-    except ValueError:
-        ok = False
-    if not ok:
-        raise MalformedLine(1, f"bad header {lines[0]!r}")
-    levels = ([], [], [], [])
-    for lineno, raw in enumerate(lines[1:], start=2):
-        if not raw.strip():
-            continue
-        try:
-            fields = [int(f) for f in raw.split()]
-        except ValueError:
-            raise MalformedLine(lineno, f"non-integer field in {raw!r}") from None
-        dim, verts = fields[0], fields[1:]
-        if not 0 <= dim <= 3 or len(verts) != dim + 1:
-            raise MalformedLine(lineno, f"bad simplex record {raw!r}")
-        if min(verts) < 0 or max(verts) >= n:
-            raise MalformedLine(lineno, "vertex index out of range")
-        if any(a >= b for a, b in zip(verts, verts[1:])):
-            raise MalformedLine(lineno, "vertices must be strictly increasing")
-        levels[dim].append(verts)
-    return AlphaComplex.from_rows(
-        vertices=np.asarray([v[0] for v in levels[0]], dtype=np.int64),
-        edges=np.asarray(levels[1], dtype=np.int64).reshape(-1, 2),
-        triangles=np.asarray(levels[2], dtype=np.int64).reshape(-1, 3),
-        tets=np.asarray(levels[3], dtype=np.int64).reshape(-1, 4),
-        alpha=alpha, ball_count=n)
+        n, alpha = int(head.group(1)), float(head.group(2))
+    except (AttributeError, ValueError):
+        raise MalformedLine(1, f"bad header {lines[0]!r}") from None
+    body = [(no, raw) for no, raw in enumerate(lines[1:], 2) if raw.strip()]
+    levels = None
+    try:
+        width = np.fromiter((raw.count(" ") + 1 for _, raw in body), dtype=np.int64, count=len(body))
+        flat = np.array(" ".join(raw for _, raw in body).split(), dtype=np.int64)
+        if flat.size == int(width.sum()):                 # single-space separated records, as write_complex emits them
+            start = np.cumsum(width) - width
+            dims = flat[start] if len(body) else np.empty(0, dtype=np.int64)
+            if ((dims >= 0) & (dims <= 3) & (width == dims + 2)).all():
+                levels = []
+                for d in range(4):
+                    rows = flat[(start[dims == d] + 1)[:, None] + np.arange(d + 1)[None, :]]
+                    good = (rows >= 0).all() and (rows < n).all() and (np.diff(rows, axis=1) > 0).all()
+                    if not good:
+                        levels = None
+                        break
+                    levels.append(rows)
+    except (ValueError, OverflowError):
+        levels = None
+    if levels is None:                                    # irregular spacing or a bad record: line by line
+        levels = [[], [], [], []]
+        for no, raw in body:
+            err = _complex_line_error(no, raw, n)
+            if err is not None:
+                raise err
+            dim, *verts = (int(f) for f in raw.split())
+            levels[dim].append(verts)
+        levels = [np.asarray(lv, dtype=np.int64).reshape(-1, d + 1) for d, lv in enumerate(levels)]
+    return AlphaComplex.from_rows(vertices=levels[0].reshape(-1), edges=levels[1], triangles=levels[2],
+                                  tets=levels[3], alpha=alpha, ball_count=n)
 
 
 def stats_csv(k: AlphaComplex) -> str:

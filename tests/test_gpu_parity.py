@@ -207,7 +207,7 @@ def test_adversarial_density_against_oracle():
 
 def test_dense_blob_crowded_edge_batches_against_oracle():
     """~60 potential-edge partners per ball: a warp batch of 8 generators overflows its pair queue, so
-    k_edges has to halve batches (and k_tri_tet2 runs its wide W=4 variant)."""
+    k_edges has to halve batches (and k_tri_tet3 runs its wide W=4 variant)."""
     rng = np.random.default_rng(11)
     c = rng.uniform(0.0, 11.0, size=(500, 3))
     r = rng.uniform(1.2, 1.9, size=500)
