@@ -19,9 +19,16 @@ parallel merge, and the final gather of counts and rows to rank 0.
 Prints ONE JSON line (see the task contract): `value` = device-resident
 throughput (inputs already in HBM, outputs left in HBM), `e2e` = the same
 through the public host API with pinned host buffers (H2D + D2H inside the
-timed region), `roofline` for the dominant kernel, `cpu_baseline` = the CPU
-oracle (a C port of the reference algorithm, oracle/) on the host cores.
-`--impl reference` times that CPU implementation alone.
+timed region), `roofline` for the dominant kernel, `cpu_baseline` = the real
+reference package (alphax 0.1.0, installed unmodified under baseline/_ref)
+on all host cores over a bounded spatial sample of the workload, with its
+parity digest against the GPU; `cpu_baseline_port` = the C/OpenMP port of the
+same algorithm (oracle/) on the whole workload.  `--impl reference` times the
+CPU implementation alone (the real package when importable, else the port).
+
+`--gpus N` without a torchrun environment starts the N ranks itself (one
+process per GPU, NCCL) and exits non-zero when the box has fewer than N
+devices.
 """
 from __future__ import annotations
 
@@ -157,6 +164,55 @@ def make_workload(n_total, seed=0):
     return synth.jittered_lattice(n_total, seed)
 
 
+def load_reference():
+    """The unmodified reference package: `pip install --target baseline/_ref /root/reference/pkg` (git-ignored,
+    travels to the GPU box with the snapshot) or wherever PYTHONPATH has it.  None if it is not importable."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref_dir, "alphax")) and ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    try:
+        import alphax
+
+        return alphax
+    except Exception:
+        return None
+
+
+def spatial_sample(centers, radii, m):
+    """The m atoms of the workload nearest (Chebyshev distance) to its centre: a cubic block of the SAME point set,
+    so density, radii and neighbourhood sizes are the workload's (the reference's time is linear in n: log-log
+    exponent 0.998, reference pkg/test_output.txt:45)."""
+    n = len(radii)
+    if m >= n:
+        return centers, radii
+    mid = 0.5 * (centers.min(axis=0) + centers.max(axis=0))
+    d = np.abs(centers - mid).max(axis=1)
+    keep = np.sort(np.argpartition(d, m)[:m])
+    return np.ascontiguousarray(centers[keep]), np.ascontiguousarray(radii[keep])
+
+
+def digest_rows(levels):
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in levels:
+        h.update(np.ascontiguousarray(a, dtype=np.int64).tobytes())
+    return h.hexdigest()
+
+
+def run_real_reference(alphax, centers, radii, alpha, eps_sing, workers):
+    """reference pkg/src/alphax/pipeline.py:571-628 through its public entry point, all host cores
+    (SURVEY 8(d): workers = os.cpu_count(), chunk_size = n // (8 * cores))."""
+    n = len(radii)
+    balls = [alphax.Ball(tuple(float(v) for v in c), float(r), i) for i, (c, r) in enumerate(zip(centers, radii))]
+    cfg = alphax.PipelineConfig(alpha=alpha, workers=workers, chunk_size=max(1, n // (8 * workers)),
+                                tolerance=alphax.TolerancePolicy(1e-9, eps_sing))
+    t0 = time.perf_counter()
+    k = alphax.compute_alpha_complex(balls, cfg)
+    dt = time.perf_counter() - t0
+    return dt, (k.vertices, k.edges, k.triangles, k.tets)
+
+
 def run_cpu(centers, radii, alpha, eps_sing, threads):
     import oracle
 
@@ -171,31 +227,64 @@ def run_cpu(centers, radii, alpha, eps_sing, threads):
 
 
 def bench_reference(args, rank, world):
-    """The CPU implementation of the path (oracle port of the reference algorithm) on all host threads."""
+    """The CPU implementation of the path on all host threads: the real reference package when it is importable
+    (kind "reference"), else the C/OpenMP port of oracle/ (kind "port").  Each step is a bounded sample of the
+    b200 arm's workload: the Python package needs ~1 min per million atoms and core, so a step is a cubic block of
+    --sample-atoms atoms cut out of the same point set; the port is fast enough for the whole workload."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n = args.atoms_per_gpu          # bounded sample: one GPU's share of the workload
+    n = args.atoms_per_gpu          # one GPU's share of the workload
     centers, radii = make_workload(n)
+    alphax = None if args.cpu_kind == "port" else load_reference()
+    if args.cpu_kind == "reference" and alphax is None:
+        raise SystemExit("the reference package is not importable (baseline/_ref missing)")
+    if alphax is not None:
+        m = min(args.sample_atoms, n)
+        sc, sr = spatial_sample(centers, radii, m)
+
+        def one():
+            return run_real_reference(alphax, sc, sr, args.alpha, args.eps_singular, threads)
+
+        kind = "reference"
+        sample = (f"alphax {alphax.__version__} compute_alpha_complex(workers={threads}, chunk_size={max(1, m // (8 * threads))}) on a "
+                  f"cubic block of {m} atoms cut from the centre of the workload (G2 n={n} seed=0 alpha={args.alpha})")
+    else:
+        m = n
+
+        def one():
+            dt, res = run_cpu(centers, radii, args.alpha, args.eps_singular, threads)
+            return dt, (res.vertices, res.edges, res.triangles, res.tets)
+
+        kind = "port"
+        sample = f"C/OpenMP port (oracle/), the whole workload: G2 n={n} seed=0 alpha={args.alpha}"
     for _ in range(min(args.warmup, 1)):
-        run_cpu(centers, radii, args.alpha, args.eps_singular, threads)
+        one()
     times = []
     for _ in range(args.steps):
-        dt, res = run_cpu(centers, radii, args.alpha, args.eps_singular, threads)
+        dt, levels = one()
         times.append(dt)
     total = sum(times)
-    value = n * args.steps / total
-    sample = f"G2 jittered lattice n={n} seed=0 alpha={args.alpha}, {args.steps} full passes"
+    value = m * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, n),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample + f", {args.steps} passes",
+                         "sample_atoms": m, "sha256_rows": digest_rows(levels)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "simplices_per_sec": sum(res.counts()) * args.steps / total,
+        "simplices_per_sec": sum(int(np.asarray(a).shape[0]) for a in levels) * args.steps / total,
         "gpu_launches": 0,
     }
+    if kind == "reference" and not args.no_port:
+        # the port beside it, on the SAME sample (its result must be the reference's, bit for bit) and on the whole workload
+        dt_s, res_s = run_cpu(sc, sr, args.alpha, args.eps_singular, threads)
+        dt_w, _ = run_cpu(centers, radii, args.alpha, args.eps_singular, threads)
+        line["cpu_baseline_port"] = {
+            "value": n / dt_w, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"C/OpenMP port (oracle/), the whole workload once: {dt_w:.2f} s; the reference's sample once: {dt_s:.3f} s",
+            "same_rows_as_reference_on_sample": digest_rows((res_s.vertices, res_s.edges, res_s.triangles, res_s.tets)) == line["cpu_baseline"]["sha256_rows"]}
     print(json.dumps(line))
 
 
@@ -204,7 +293,8 @@ def workload_config(args, n_local):
                         f"1 atom/12 A^3, radii U[1.2,1.9] A, alpha={args.alpha} A^2",
             "atoms_per_gpu": n_local, "alpha": args.alpha, "eps_singular": args.eps_singular,
             "l2": "flushed (256 MiB write) between timed steps; per-step working set ~1.5 GB also exceeds L2",
-            "sharding": "one z-slab per rank, 2-cell halo replicated; all_to_all by owner range + parallel merge + gather to rank 0" if args.gpus > 1 else "single GPU"}
+            "sharding": ("one z-slab per rank, 2-cell halo replicated; every slab emits the simplices it generates (disjoint lists); "
+                         "one collective: gather of counts and rows to rank 0 (NCCL send/recv), merged there") if args.gpus > 1 else "single GPU"}
 
 
 def bench_b200(args, rank, world, local_rank):
@@ -215,9 +305,14 @@ def bench_b200(args, rank, world, local_rank):
     # developer hooks for a one-GPU box: AXB_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 and
     # AXB_BENCH_BACKEND=gloo replaces the transport (NCCL refuses two ranks on one device), so the whole
     # multi-rank path (slab planning, per-rank slabs, gather, merge) can be exercised and verified
-    if os.environ.get("AXB_BENCH_SAME_DEVICE") == "1":
+    same_device = os.environ.get("AXB_BENCH_SAME_DEVICE") == "1"
+    if same_device:
         local_rank = 0
     backend = os.environ.get("AXB_BENCH_BACKEND", "nccl")
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (this package has no CPU fallback)")
+    if not same_device and torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py --gpus {world}: only {torch.cuda.device_count()} CUDA device(s) on this box")
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
@@ -360,13 +455,19 @@ def bench_b200(args, rank, world, local_rank):
     top = max(kernel_stages, key=lambda k: stage_ms[k])
     peak, peak_src = measured_peak()
     achieved = S[top] / (stage_ms[top] * 1e-3) / 1e9
-    traffic = None
+    # DRAM traffic and pipe utilisation of that kernel come from an ncu --set full capture of THIS workload committed
+    # under profiles/ (a number taken under a profiler cannot be measured inside a timed run); the source is named
+    traffic, traffic_source, secondary = None, None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(KERNEL_OF_STAGE[top])
+            tj = json.load(open(tpath))
+            traffic = tj.get(KERNEL_OF_STAGE[top])
+            traffic_source = "profiles/traffic.json: " + tj.get("_note", "")
+            secondary = tj.get("_pipes", {}).get(KERNEL_OF_STAGE[top])
         except Exception:
             traffic = None
+    dram_frac = (traffic / (stage_ms[top] * 1e-3) / 1e9 / peak) if traffic else None
     ms_per_step = dev_ms / args.steps
     line = {
         "metric": METRIC, "value": n_all * args.steps / (dev_ms * 1e-3), "unit": UNIT, "n_gpus": world,
@@ -378,8 +479,12 @@ def bench_b200(args, rank, world, local_rank):
         "e2e": {"value": n_all * args.steps / e2e_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_s / args.steps,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": KERNEL_OF_STAGE[top], "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+        # bound: the kernels move a few per cent of what HBM could deliver and keep the FP64 pipe 10-30 % busy: they are
+        # bound by instruction issue / dependent latency, not by a roofline (`secondary` = ncu's pipe view of the kernel)
+        "roofline": {"bound": "issue" if (dram_frac is not None and dram_frac < 0.10) else "hbm",
+                     "kernel": KERNEL_OF_STAGE[top], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_source,
+                     "dram_frac_of_peak": dram_frac, "secondary": secondary, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": int(S[top]), "kernel_ms": stage_ms[top],
                      "pipeline": {"algorithmic_bytes": int(b_total), "bytes_per_atom": b_total / n,
                                   "achieved": b_total / (ms_per_step * 1e-3) / 1e9,
@@ -388,41 +493,105 @@ def bench_b200(args, rank, world, local_rank):
                      "stage_gbs": {k: round(S[k] / (stage_ms[k] * 1e-3) / 1e9, 1) for k in S if stage_ms.get(k, 0) > 0}},
         "clocks": clocks,
     }
-    # ---- CPU baseline beside it (rank 0, N=1 only): the oracle port on the host cores, same workload
+    if job is not None:
+        g = job.last_gather
+        line["collectives"] = {"backend": backend, "per_step": ["all_gather of 10 status words (agreement on one error)",
+                                                                   "all_gather of the 4 row counts", "grouped send/recv of the rows to rank 0"],
+                               "rows_by_rank": g.get("rows").tolist() if g.get("rows") is not None else None,
+                               "bytes_into_rank0_per_step": int(g.get("bytes", 0)), "wire": "int32" if n_total < 2 ** 31 else "int64"}
+        if backend == "nccl":
+            line["collectives"]["nccl_version"] = ".".join(str(v) for v in torch.cuda.nccl.version())
+    # ---- CPU baselines beside it (rank 0, N=1 only)
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
+        # (a) the C/OpenMP port on the whole workload, bit-exact check of the GPU result
         dt, res = run_cpu(centers, radii, args.alpha, args.eps_singular, threads)
-        same = all(np.array_equal(a, b) for a, b in zip(
-            [o for o in eng.compute_host(centers, radii, cfg)], (res.vertices, res.edges, res.triangles, res.tets)))
-        line["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"the full step workload once ({n} atoms, alpha={args.alpha}): {dt:.2f} s",
-                                "gpu_output_bit_exact_with_cpu": bool(same)}
+        gpu_rows = eng.compute_host(centers, radii, cfg)
+        same = all(np.array_equal(a, b) for a, b in zip(gpu_rows, (res.vertices, res.edges, res.triangles, res.tets)))
+        port = {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                "sample": f"C/OpenMP port (oracle/), the whole step workload once ({n} atoms, alpha={args.alpha}): {dt:.2f} s",
+                "gpu_output_bit_exact_with_cpu": bool(same)}
+        # (b) the real reference package on a bounded sample, in its own process (its worker pool forks, which a
+        # process with a CUDA context must not do); the GPU runs the same sample for the parity digest
+        ref_line = None
+        if load_reference() is not None:
+            cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--cpu-kind", "reference", "--steps", "1",
+                   "--warmup", "0", "--no-port", "--sample-atoms", str(args.cpu_sample_atoms), "--atoms-per-gpu", str(n),
+                   "--alpha", str(args.alpha), "--eps-singular", str(args.eps_singular)]
+            env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+            try:
+                out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+                ref_line = json.loads(out.stdout.strip().splitlines()[-1])["cpu_baseline"]
+            except Exception as exc:                      # keep the bench line; say what happened
+                port["reference_unavailable"] = f"{type(exc).__name__}: {exc}"[:200]
+        if ref_line is not None:
+            sc, sr = spatial_sample(centers, radii, min(args.cpu_sample_atoms, n))
+            ref_line["gpu_output_bit_exact_with_cpu"] = digest_rows(eng.compute_host(sc, sr, cfg)) == ref_line["sha256_rows"]
+            line["cpu_baseline"] = ref_line
+            line["cpu_baseline_port"] = port
+        else:
+            line["cpu_baseline"] = port
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
 
 
+def spawn_ranks(args):
+    """`python bench.py --gpus N` from a plain shell: start the N ranks (one process per GPU) under torchrun."""
+    import socket
+
+    import torch
+
+    same_device = os.environ.get("AXB_BENCH_SAME_DEVICE") == "1"
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if not same_device and have < args.gpus:
+        print(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) on this box", file=sys.stderr)
+        return 2
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--atoms-per-gpu", type=int, default=1_000_000)
     ap.add_argument("--alpha", type=float, default=0.0)
     ap.add_argument("--eps-singular", type=float, default=1e-12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verify", action="store_true", help="N>1: check the merged complex against one unsharded pass on rank 0")
+    ap.add_argument("--cpu-kind", default="auto", choices=["auto", "reference", "port"],
+                    help="--impl reference: the real package (baseline/_ref), the C port, or the package when importable")
+    ap.add_argument("--sample-atoms", type=int, default=50_000,
+                    help="--impl reference with the real package: atoms per step (a cubic block of the workload)")
+    ap.add_argument("--cpu-sample-atoms", type=int, default=200_000,
+                    help="b200 arm: size of the sample the real reference is timed on beside the GPU (10-30 s of CPU work)")
+    ap.add_argument("--no-port", action="store_true", help="--impl reference: skip the C port beside the real package")
     args = ap.parse_args()
+    if args.impl == "reference":
+        if args.steps == 100:
+            args.steps = 3                  # default run: a few passes of the CPU implementation are minutes already
+        bench_reference(args, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and args.eps_singular == 1e-12:
-        args.eps_singular = 1e-300      # large sets trip the default pivot threshold in BOTH implementations
-    if args.impl == "reference":
-        bench_reference(args, rank, world)
-    else:
-        bench_b200(args, rank, world, local_rank)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} was started with WORLD_SIZE={world}")
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")            # the communicator's own log (rings, NVLS) goes to stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if args.eps_singular == 1e-12:
+            args.eps_singular = 1e-300      # SURVEY.md H1: large sets trip the default pivot threshold in BOTH implementations
+    bench_b200(args, rank, world, local_rank)
 
 
 from ctypes import c_int64 as C_int64  # noqa: E402

@@ -100,6 +100,13 @@ const char *axb_last_message(const axb_ctx *ctx);
 /* AXB_ERR_NONFINITE: verts[0]; AXB_ERR_DUPLICATE: verts[0..1];
  * AXB_ERR_DEGENERATE: verts[0..nverts-1] ascending ball indices. */
 int axb_last_error(const axb_ctx *ctx, int *status, int64_t verts[4], int *nverts);
+/* What ranks of a sharded run need to agree on ONE error (the one the reference would raise for the whole
+ * input, pipeline.py:238-244 / 357, 414, 419, 477).  AXB_ERR_DEGENERATE: *key = (stage << 60 | generator rank in
+ * this context's grid order << 24 | ordinal); the smallest key over all ranks -- after adding the slab's first
+ * global grid rank << 24 -- is the solve the reference meets first.  AXB_ERR_DUPLICATE: xyz = the shared centre
+ * (the reference reports the smallest one in (x, y, z) order).  Ball indices from axb_last_error are GLOBAL
+ * (mapped through d_global_index) when the context holds a slab. */
+int axb_last_error_detail(const axb_ctx *ctx, uint64_t *key, double xyz[3]);
 
 /* ---- the hot path, stage by stage ------------------------------------- */
 /* validate_input + build_grid_arrays (pipeline.py:224-245, grid.py:105-144).
@@ -147,8 +154,12 @@ int axb_sync_check(axb_ctx *ctx);
 int axb_compute(axb_ctx *ctx, int64_t n, const double *d_xyz, const double *d_radii,
                 const axb_params *params, int64_t counts[4]);
 /* One z-slab of a sharded run in one call (what one GPU of a multi-GPU job executes):
- * axb_grid_build_slab -> generators of the OWNED layers [z_own_lo, z_own_hi) -> prune -> canonicalize.
- * Rows exported afterwards carry global ball indices. */
+ * axb_grid_build_slab -> potential simplices of the lower halo and of the OWNED layers [z_own_lo, z_own_hi) ->
+ * prune -> canonicalize.  The slab emits exactly the kept simplices whose minimum-rank vertex (their generator,
+ * pipeline.py:10-15) lies in an owned layer: it decides them completely on its own -- faces inherited from kept
+ * simplices generated in the lower halo (pipeline.py:501-513) included, which is why the loaded layers must reach 2
+ * below and 2 above the owned ones -- so the slabs' row lists are DISJOINT and their plain sorted merge is the
+ * complex.  Rows exported afterwards carry global ball indices. */
 int axb_compute_slab(axb_ctx *ctx, int64_t n, const double *d_xyz, const double *d_radii,
                      const int64_t *d_global_index, const axb_params *params, const axb_slab *slab,
                      int64_t z_own_lo, int64_t z_own_hi, int64_t counts[4]);

@@ -24,7 +24,7 @@ STAGE_KEYS = ("grid", "potential_edges", "potential_triangles", "potential_tets"
 SYMBOLS = (
     "axb_version", "axb_status_name", "axb_ctx_create", "axb_ctx_destroy", "axb_ctx_set_stream",
     "axb_ctx_set_arena", "axb_arena_needed", "axb_arena_used", "axb_arena_hint", "axb_last_message",
-    "axb_last_error", "axb_grid_build", "axb_grid_build_slab", "axb_slab_rank_range", "axb_merge_rows", "axb_compute_slab",
+    "axb_last_error", "axb_last_error_detail", "axb_grid_build", "axb_grid_build_slab", "axb_slab_rank_range", "axb_merge_rows", "axb_compute_slab",
     "axb_grid_get_info", "axb_grid_export", "axb_potential",
     "axb_potential_counts", "axb_potential_export", "axb_prune", "axb_canonicalize", "axb_export",
     "axb_sync_check", "axb_compute", "axb_compute_host", "axb_export_host", "axb_compute_host_begin",
@@ -75,6 +75,7 @@ def load() -> C.CDLL:
         "axb_arena_hint": (sz, [i64, C.c_double, C.c_double]),
         "axb_last_message": (C.c_char_p, [vp]),
         "axb_last_error": (C.c_int, [vp, C.POINTER(C.c_int), pi64, C.POINTER(C.c_int)]),
+        "axb_last_error_detail": (C.c_int, [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
         "axb_grid_build": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params)]),
         "axb_grid_build_slab": (C.c_int, [vp, i64, vp, vp, vp, C.POINTER(Params), C.POINTER(Slab)]),
         "axb_slab_rank_range": (C.c_int, [vp, i64, i64, pi64, pi64]),

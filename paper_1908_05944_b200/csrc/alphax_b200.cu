@@ -69,6 +69,8 @@ struct axb_ctx {
     int last_status = AXB_OK;
     int64_t err_verts[4] = {-1, -1, -1, -1};
     int err_nverts = 0;
+    unsigned long long err_key = 0;         // AXB_ERR_DEGENERATE: the enumeration key of the reported solve
+    double err_xyz[3] = {0, 0, 0};          // AXB_ERR_DUPLICATE: the shared centre
     char msg[512] = {0};
     int64_t launches = 0;
     cudaEvent_t ev[AXB_ST_COUNT + 2] = {};      // stage boundaries 0..EXPORT, then export begin/end
@@ -83,6 +85,8 @@ struct axb_ctx {
     GridView g = {};
     Tol tol = {};
     int rank_lo = 0, rank_hi = 0;
+    int gen_lo = 0;                       // first generator whose simplices are built: rank_lo, or 0 for a slab (the lower
+                                          // halo's simplices decide the inherited faces of owned simplices)
     // device arrays (arena)
     Counters *ctr = nullptr;
     ErrRecord *errs = nullptr;
@@ -360,6 +364,18 @@ int bin_balls(axb_ctx *c, double side, const double lo[3], const int64_t dims[3]
     return AXB_OK;
 }
 
+// slab mode: the kernels name balls by their position in the slab's input; callers know them by global index
+int globalize_err_verts(axb_ctx *c) {
+    if (!c->gidx) return AXB_OK;
+    for (int a = 0; a < c->err_nverts; ++a) {
+        int64_t g = -1;
+        CUDA_TRY(c, cudaMemcpy(&g, c->gidx + c->err_verts[a], sizeof(int64_t), cudaMemcpyDeviceToHost));
+        c->err_verts[a] = g;
+    }
+    std::sort(c->err_verts, c->err_verts + c->err_nverts);     // gidx ascends, so this keeps the order anyway
+    return AXB_OK;
+}
+
 // pick the duplicate pair the reference reports (pipeline.py:238-244): first adjacent equal
 // pair in lexsort (x, y, z) order == smallest centre, then the two smallest ball indices.
 int report_duplicate(axb_ctx *c, unsigned ndup) {
@@ -384,6 +400,9 @@ int report_duplicate(axb_ctx *c, unsigned ndup) {
     c->err_verts[0] = c->h->dups[best].x;
     c->err_verts[1] = c->h->dups[best].y;
     c->err_nverts = 2;
+    for (int a = 0; a < 3; ++a) c->err_xyz[a] = bx[a];
+    int ms = globalize_err_verts(c);
+    if (ms != AXB_OK) return ms;
     return fail(c, AXB_ERR_DUPLICATE, "balls %lld and %lld share the center (%.17g, %.17g, %.17g)",
                 (long long)c->err_verts[0], (long long)c->err_verts[1], bx[0], bx[1], bx[2]);
 }
@@ -396,6 +415,9 @@ EstParams est_params(axb_ctx *c, unsigned long long report_key) {
     P.pt = c->pt; P.pt_cap = c->pt_cap; P.pq_r = c->pq_r; P.pq_l = c->pq_l; P.pq_cap = c->pq_cap;
     P.ctr = c->ctr; P.errs = c->errs; P.report_key = report_key;
     P.cull = c->cull ? c->cull_mask : 0;
+    // a slab reports singular solves only for generators whose enumeration is complete (the upper halo's is not)
+    P.err_rank_hi = c->slab_mode ? c->rank_hi : 0x7fffffff;
+    P.own_lo = c->slab_mode ? c->rank_lo : 0;
     return P;
 }
 
@@ -409,6 +431,7 @@ PruneParams prune_params(axb_ctx *c) {
     P.cnt1 = c->cnt1; P.cnt2 = c->cnt2; P.cnt3 = c->cnt3; P.vkeep = c->vkeep;
     P.ctr = c->ctr; P.biomolecule = c->prm.biomolecule;
     P.rank_lo = c->rank_lo; P.rank_hi = c->rank_hi;
+    P.own_only = c->slab_mode ? 1 : 0;
     P.k3_cap = c->k3_cap;
     // n_pt may still be the optimistic capacity (axb_compute); the potential triangles are ~0.8 per potential edge
     const unsigned warps = (unsigned)c->sm_count * (unsigned)PRUNE_GRID * (unsigned)PRUNE_WARPS;
@@ -428,7 +451,7 @@ int launch_edges(axb_ctx *c, const EstParams &P, int lo, int hi) {
 
 int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
     EstParams P = est_params(c, report_key);
-    const int ngen = c->rank_hi - c->rank_lo;
+    const int ngen = c->rank_hi - c->gen_lo;
 #ifndef TETS_DYN_PAIRS
 #define TETS_DYN_PAIRS 20      // more partner pairs per generator than this: k_prune_tets claims chunks (1M atoms: the static
                                // loop wins up to alpha 0.4 = 0.36 vs 0.41 ms, a tie at 0.6, claims from alpha 0.8 = 0.67 vs 0.69 ms)
@@ -443,7 +466,7 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
             const size_t smem = warp_bytes * T3_WARPS;
             const unsigned nblocks = (unsigned)std::max(1, (ngen + gens * T3_WARPS - 1) / (gens * T3_WARPS));
             CUDA_TRY(c, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            kernel<<<std::min(nblocks, (unsigned)c->sm_count * (unsigned)minb), T3_WARPS * 32, smem, c->stream>>>(P, c->rank_lo, c->rank_hi);
+            kernel<<<std::min(nblocks, (unsigned)c->sm_count * (unsigned)minb), T3_WARPS * 32, smem, c->stream>>>(P, c->gen_lo, c->rank_hi);
             return AXB_OK;
         };
         int st;
@@ -474,7 +497,7 @@ int report_degenerate(axb_ctx *c) {
             EstParams P = est_params(c, key);
             P.pe_cap = 0;    // count only
             const int edge_hi = c->slab_mode ? (int)c->n : c->rank_hi;
-            int st = launch_edges(c, P, c->rank_lo, edge_hi);
+            int st = launch_edges(c, P, c->gen_lo, edge_hi);
             if (st != AXB_OK) return st;
         } else {
             uint32_t pt_cap = c->pt_cap, pq_cap = c->pq_cap;
@@ -489,11 +512,16 @@ int report_degenerate(axb_ctx *c) {
     }
     c->err_nverts = hit->nverts;
     for (int a = 0; a < 4; ++a) c->err_verts[a] = a < hit->nverts ? hit->verts[a] : -1;
+    c->err_key = key;
+    {
+        int ms = globalize_err_verts(c);
+        if (ms != AXB_OK) return ms;
+    }
     static const char *what[] = {"simplex", "edge", "edge", "triangle", "tetrahedron"};
     const int stage = (int)(key >> 60);
     char vs[128];
     int w = 0;
-    for (int a = 0; a < hit->nverts; ++a) w += snprintf(vs + w, sizeof(vs) - w, a ? ", %d" : "%d", hit->verts[a]);
+    for (int a = 0; a < c->err_nverts; ++a) w += snprintf(vs + w, sizeof(vs) - w, a ? ", %lld" : "%lld", (long long)c->err_verts[a]);
     return fail(c, AXB_ERR_DEGENERATE, "%s (%s) has affinely dependent centers", what[stage <= 4 ? stage : 0], vs);
 }
 
@@ -603,6 +631,13 @@ extern "C" int axb_last_error(const axb_ctx *c, int *status, int64_t verts[4], i
     return AXB_OK;
 }
 
+extern "C" int axb_last_error_detail(const axb_ctx *c, uint64_t *key, double xyz[3]) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (key) *key = c->err_key;
+    if (xyz) for (int a = 0; a < 3; ++a) xyz[a] = c->err_xyz[a];
+    return AXB_OK;
+}
+
 extern "C" int64_t axb_kernel_launches(const axb_ctx *c) { return c ? c->launches : 0; }
 
 extern "C" int axb_stage_ms(const axb_ctx *cc, float out[AXB_ST_COUNT]) {
@@ -632,6 +667,7 @@ int grid_build_common(axb_ctx *c, int64_t n, const double *d_xyz, const double *
     c->last_status = AXB_OK;
     c->msg[0] = 0;
     c->err_nverts = 0;
+    c->err_key = 0;
     for (int a = 0; a < 4; ++a) c->err_verts[a] = -1;
     for (int i = 0; i < AXB_ST_COUNT + 2; ++i) c->ev_set[i] = false;
     c->arena_used = 0;
@@ -782,6 +818,7 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
     c->arena_used = c->mark_after_grid;
     c->rank_lo = (int)lo;
     c->rank_hi = (int)hi;
+    c->gen_lo = c->slab_mode ? 0 : (int)lo;
     const int n = (int)c->n;
     const int ngen = (int)(hi - lo);
     int st;
@@ -795,7 +832,7 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
     ARENA(c, c->adj_off, uint32_t, n);
     ARENA(c, c->deg, int, n);
     const size_t mark_pe = c->arena_used;
-    uint64_t want = (uint64_t)16 * (uint64_t)(c->slab_mode ? n - (int)lo : ngen) + 4096;
+    uint64_t want = (uint64_t)16 * (uint64_t)(c->slab_mode ? n : ngen) + 4096;
     for (int attempt = 0;; ++attempt) {
         if (want > 0xfffffff0ull) return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential edges");
         c->arena_used = mark_pe;
@@ -809,9 +846,10 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
             CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
         }
         EstParams P = est_params(c, 0);
-        // a slab also needs the partner rows of its upper halo: inherited faces of owned tets land there
+        // a slab builds the partner rows of every loaded ball: the lower halo's generate the simplices that decide the
+        // inherited faces of owned simplices, the upper halo's receive the marks of owned tets
         const int edge_hi = c->slab_mode ? n : c->rank_hi;
-        st = launch_edges(c, P, c->rank_lo, edge_hi);
+        st = launch_edges(c, P, c->gen_lo, edge_hi);
         if (st != AXB_OK) return st;
         st = fetch_counters(c);
         if (st != AXB_OK) return st;
@@ -980,6 +1018,7 @@ int run_canonicalize(axb_ctx *c, int64_t counts[4]) {
     P.W = c->W; P.trimask = c->trimask; P.eflag = c->eflag; P.k3 = c->k3;
     P.cnt1 = c->cnt1; P.cnt2 = c->cnt2; P.cnt3 = c->cnt3; P.off1 = c->off1; P.off2 = c->off2; P.off3 = c->off3;
     P.tmp1 = c->tmp1; P.tmp2 = c->tmp2; P.tmp3 = c->tmp3; P.ctr = c->ctr;
+    P.own_lo = c->slab_mode ? c->rank_lo : 0; P.own_hi = c->slab_mode ? c->rank_hi : 0x7fffffff;
     const unsigned grid = (unsigned)c->sm_count * 8u;
     k_scatter_edges_tris<<<grid, 256, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
@@ -1376,6 +1415,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     Q.W = c->W; Q.trimask = c->trimask; Q.eflag = c->eflag; Q.k3 = c->k3;
     Q.cnt1 = c->cnt1; Q.cnt2 = c->cnt2; Q.cnt3 = c->cnt3; Q.off1 = c->off1; Q.off2 = c->off2; Q.off3 = c->off3;
     Q.tmp1 = c->tmp1; Q.tmp2 = c->tmp2; Q.tmp3 = c->tmp3; Q.ctr = c->ctr;
+    Q.own_lo = 0; Q.own_hi = 0x7fffffff;
     const unsigned grid = (unsigned)c->sm_count * 8u;
     // Everything is queued up front.  After the scan of a dimension its exact row count goes to the
     // host (4 bytes + an event); the host follows those events, queues the copies of exactly the valid

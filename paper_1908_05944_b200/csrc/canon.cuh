@@ -33,12 +33,16 @@ struct CanonParams {
     int4 *tmp2;                            // (owner, b, c, -)
     int4 *tmp3;                            // (owner, b, c, d)
     Counters *ctr;
+    int own_lo, own_hi;                    // rows of generators outside [own_lo, own_hi) are not emitted (slab ownership)
 };
+
+__device__ __forceinline__ bool canon_emits(const CanonParams &P, int gen) { return gen >= P.own_lo && gen < P.own_hi; }
 
 __global__ void __launch_bounds__(256) k_scatter_edges_tris(CanonParams P) {
     const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pe; e += gridDim.x * blockDim.x) {
         const int u = __ldg(P.pe_u + e), v = __ldg(P.pe_v + e);
+        if (!canon_emits(P, u)) continue;
         const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + v);
         if (P.eflag[e]) {
             const int a = min(ou, ov), b = max(ou, ov);
@@ -69,7 +73,9 @@ __global__ void __launch_bounds__(256) k_scatter_edges(CanonParams P, unsigned c
     const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pe; e += gridDim.x * blockDim.x) {
         if (!P.eflag[e]) continue;
-        const int ou = __ldg(P.orig + __ldg(P.pe_u + e)), ov = __ldg(P.orig + __ldg(P.pe_v + e));
+        const int u = __ldg(P.pe_u + e);
+        if (!canon_emits(P, u)) continue;
+        const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + __ldg(P.pe_v + e));
         const int a = min(ou, ov), b = max(ou, ov);
         const unsigned pos = P.off1[a] + atomicSub(P.cnt1 + a, 1u) - 1u;
         if (pos < cap) P.tmp1[pos] = make_int2(a, b);
@@ -83,6 +89,7 @@ __global__ void __launch_bounds__(256) k_scatter_tris(CanonParams P, unsigned ca
         for (int w = 0; w < P.W; ++w) any |= P.trimask[(size_t)e * P.W + w];
         if (!any) continue;
         const int u = __ldg(P.pe_u + e);
+        if (!canon_emits(P, u)) continue;
         const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + __ldg(P.pe_v + e));
         const unsigned bu = __ldg(P.adj_off + u);
         for (int w = 0; w < P.W; ++w) {

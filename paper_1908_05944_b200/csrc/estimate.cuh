@@ -47,6 +47,9 @@ struct EstParams {
     ErrRecord *errs;
     unsigned long long report_key;   // != 0: only the solve with this key writes errs[0]
     int cull;                        // k_tri_tet3: drop / flag simplices dominated by a partner of their generator
+    int err_rank_hi;                 // singular solves are reported for generators below this rank only (slab: the
+                                     // upper halo's enumeration is incomplete; its owner reports it)
+    int own_lo;                      // slab: first owned rank; a lower-halo generator matters only if a partner reaches it
 };
 
 __device__ __forceinline__ void sort_small(int *v, int k) {
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(EST_WARPS * 32, E2_MINB) k_edges(EstParams P, 
                             const Atom av = load_atom(P.atoms, cand);
                             const int ov = __ldg(P.orig + cand);
                             const Ortho o = ortho_edge(q.orig, au, ov, av, P.tol.eps_sing);        // pipeline.py:355-356
-                            if (o.singular)        // ordinal = candidate number inside its generator
+                            if (o.singular && ts + gs < P.err_rank_hi)   // ordinal = candidate number inside its generator
                                 record_singular(P, make_err_key(ST_EDGE, ts + gs, (unsigned)(ord - S.row_pre[gs * E2_ROWS])), q.orig, ov, -1, -1, 2);
                             keep = o.size <= P.tol.lim_a;                                          // pipeline.py:358
                         }

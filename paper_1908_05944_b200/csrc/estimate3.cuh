@@ -220,6 +220,8 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                 d = min(__ldg(P.deg + t0 + lane), PCAP);
                 if (d < 2) d = 0;                           // no partner pair, nothing to do
                 S.gadj[lane] = __ldg(P.adj_off + t0 + lane);
+                // slab, lower halo: only simplices that reach an owned ball matter (partners ascend in rank)
+                if (d && t0 + lane < P.own_lo && __ldg(P.pe_v + S.gadj[lane] + d - 1) < P.own_lo) d = 0;
                 const Atom a = load_atom(P.atoms, t0 + lane);
                 S.ax[SCAP + lane] = a.x; S.ay[SCAP + lane] = a.y; S.az[SCAP + lane] = a.z; S.ar2[SCAP + lane] = a.r2;
                 S.aorig[SCAP + lane] = __ldg(P.orig + t0 + lane);

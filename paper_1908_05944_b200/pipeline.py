@@ -228,6 +228,12 @@ class Engine:
         self.lib.axb_last_error(self.handle, C.byref(st), verts, C.byref(nv))
         return tuple(int(verts[i]) for i in range(nv.value))
 
+    def _error_detail(self):
+        key = C.c_uint64()
+        xyz = (C.c_double * 3)()
+        self.lib.axb_last_error_detail(self.handle, C.byref(key), xyz)
+        return int(key.value), tuple(float(v) for v in xyz)
+
     def _raise(self, st: int, cfg: PipelineConfig, centers=None, radii=None):
         """Status -> the exception the reference raises for the same input."""
         if st == N.ERR_EMPTY:
@@ -236,10 +242,7 @@ class Engine:
             raise NonFiniteCoordinate(f"ball {self._error_vertices()[0]} is not finite")
         if st == N.ERR_DUPLICATE:
             i, j = self._error_vertices()
-            where = None
-            if centers is not None:
-                where = tuple(float(v) for v in _row_to_host(centers, i))
-            raise DuplicateCenter(f"balls {i} and {j} share the center {where}")
+            raise DuplicateCenter(f"balls {i} and {j} share the center {self._error_detail()[1]}")
         if st == N.ERR_DEGENERATE:
             bad = self._error_vertices()
             what = {2: "edge", 3: "triangle", 4: "tetrahedron"}.get(len(bad), "simplex")
@@ -249,6 +252,21 @@ class Engine:
             raise ValueError(f"alpha={cfg.alpha} gives non-positive squared cell side (r_max={r_max})")
         name = self.lib.axb_status_name(st).decode()
         raise AlphaxError(f"{name}: {self._message()}")
+
+    def raise_slab_error(self, rec, cfg: PipelineConfig):
+        """The exception for a `sharding.SlabError` every rank agreed on (same types and messages as _raise)."""
+        st, verts = rec.status, tuple(rec.vertices)
+        if st == N.ERR_NONFINITE:
+            raise NonFiniteCoordinate(f"ball {verts[0]} is not finite")
+        if st == N.ERR_DUPLICATE:
+            raise DuplicateCenter(f"balls {verts[0]} and {verts[1]} share the center {tuple(rec.xyz)}")
+        if st == N.ERR_DEGENERATE:
+            what = {2: "edge", 3: "triangle", 4: "tetrahedron"}.get(len(verts), "simplex")
+            raise DegenerateSimplex(f"{what} {verts} has affinely dependent centers", vertices=verts)
+        if st == N.ERR_BAD_SIDE:
+            raise ValueError(f"alpha={cfg.alpha} gives non-positive squared cell side")
+        name = self.lib.axb_status_name(st).decode()
+        raise AlphaxError(f"{name}: {rec.message or 'reported by another rank'}")
 
     def _with_arena(self, n: int, cfg: PipelineConfig, call):
         """Run ``call()`` (returns a status), growing the arena on AXB_ERR_ARENA."""
@@ -438,9 +456,11 @@ class Engine:
         return outs
 
     # -- multi-GPU building blocks (sharding.py)
-    def compute_slab_device(self, centers, radii, global_index, cfg: PipelineConfig, plan, slab):
+    def compute_slab_device(self, centers, radii, global_index, cfg: PipelineConfig, plan, slab, raise_errors: bool = True):
         """One z-slab of a global grid: CUDA tensors of the loaded balls (ascending global index) in,
-        the four row lists in GLOBAL ball indices out (what this rank contributes to the union)."""
+        the four row lists in GLOBAL ball indices out -- the kept simplices whose generator lies in an
+        owned layer, disjoint from every other slab's.  raise_errors=False returns (rows, SlabError | None)
+        instead of raising (error vertices are global ball indices, the key is shifted to global grid ranks)."""
         torch = self.torch
         n = int(radii.shape[0])
         prm = self._params(cfg)
@@ -466,9 +486,16 @@ class Engine:
             self._bind_stream()
             st = self._with_arena(n, cfg, run)
         if st != N.OK:
-            self._raise(st, cfg, centers, radii)
+            if raise_errors:
+                self._raise(st, cfg, centers, radii)
+            from .sharding import SlabError
+
+            key, xyz = self._error_detail()
+            if st == N.ERR_DEGENERATE:
+                key += int(slab.first_rank) << 24
+            return [], SlabError(status=int(st), key=key, vertices=self._error_vertices(), xyz=xyz, message=self._message())
         self._collect_stage_ms()
-        return outs
+        return outs if raise_errors else (outs, None)
 
     def merge_rows(self, rows, k: int, n_index: int):
         """Sorted duplicate-free union of canonical rows (CUDA int64 tensor (m,k) or (m,) for k=1)."""
@@ -510,12 +537,6 @@ class Engine:
         if st != N.OK:
             raise AlphaxError(self._message())
         return cen.cpu().numpy(), siz.cpu().numpy(), sg.cpu().numpy().astype(bool)
-
-
-def _row_to_host(a, i):
-    if isinstance(a, np.ndarray):
-        return a[i]
-    return a[i].detach().cpu().numpy()
 
 
 def _max_to_host(a):

@@ -23,3 +23,16 @@ def canonical_text(vertices, edges, triangles, tets, n, alpha, version="0.1.0") 
         for row in rows:
             lines.append(f"{dim} " + " ".join(str(int(v)) for v in row))
     return "\n".join(lines) + "\n"
+
+
+def rows_generated_in(levels, rank_of_ball, lo, hi):
+    """The rows of a complex (vertices, edges, triangles, tets) whose generator -- the vertex of minimum
+    grid rank, reference pipeline.py:10-15 -- has its rank in [lo, hi): what the slab that owns those
+    ranks must emit (the slabs of a sharded run partition the complex this way)."""
+    out = []
+    for d, rows in enumerate(levels):
+        rows = np.asarray(rows, dtype=np.int64).reshape(-1, d + 1)
+        gen = rank_of_ball[rows].min(axis=1) if rows.shape[0] else np.empty(0, dtype=np.int64)
+        sel = rows[(gen >= lo) & (gen < hi)]
+        out.append(sel.reshape(-1) if d == 0 else sel)
+    return out

@@ -296,24 +296,79 @@ def test_permutation_of_input_indices():
 
 
 def test_slab_sharding_on_one_gpu_equals_single_shot():
-    """All slabs of a 3- and 8-way sharded run computed one after the other on this GPU, merged on
-    the device: must equal the unsharded result bit for bit, and slabs must overlap only in inherited faces."""
+    """All slabs of a 3- and 8-way sharded run computed one after the other on this GPU: every slab must emit
+    exactly the simplices of the complex whose generator (minimum grid rank vertex) it owns -- inherited faces
+    decided from its lower halo included -- so the lists are disjoint, add up to the global counts, and their
+    merge equals the unsharded result bit for bit."""
+    from paper_1908_05944_b200 import sharding
+    from helpers import rows_generated_in
+
+    eng = ax.default_engine()
+    for (c, r), alpha, eps, bio in ((synth.jittered_lattice(60_000, 8), 0.0, 1e-12, False),
+                                    (synth.jittered_lattice(30_000, 8), 1.4, 1e-300, False),
+                                    (synth.adversarial_density(30_000, 3, shuffle=True), 0.0, 1e-300, False),
+                                    (synth.random_globule(3000, 5, 0.5, (0.2, 2.4), 0.12), 0.3, 1e-300, False),
+                                    (synth.jittered_lattice(20_000, 2), 0.6, 1e-300, True)):
+        cfg = ax.PipelineConfig(alpha=alpha, biomolecule_mode=bio, tolerance=ax.TolerancePolicy(1e-9, eps))
+        single = eng.compute_host(c, r, cfg)
+        st, g = oracle.grid_build(c, r, alpha)
+        for world in (3, 8):
+            merged, per_rank = sharding.compute_sharded_single_gpu(c, r, cfg, world, eng)
+            plan = sharding.plan_slabs(c, r, alpha, world)
+            for d in range(4):
+                assert np.array_equal(merged[d].cpu().numpy(), single[d]), (world, d)
+                assert sum(int(o[d].shape[0]) for o in per_rank) == single[d].shape[0], (world, d)   # disjoint
+            for rank, outs in enumerate(per_rank):
+                want = rows_generated_in(single, g.rank, *plan.rank_ranges[rank])
+                for d in range(4):
+                    assert np.array_equal(outs[d].cpu().numpy(), want[d]), (world, rank, d)
+
+
+def test_slab_errors_name_global_balls():
+    """A slab that meets a singular solve or a duplicate centre reports GLOBAL ball indices and the detail the
+    ranks of a sharded run need to agree on the error the reference raises for the whole input."""
     import torch
 
     from paper_1908_05944_b200 import sharding
 
     eng = ax.default_engine()
-    for (c, r), alpha, eps in ((synth.jittered_lattice(60_000, 8), 0.0, 1e-12),
-                               (synth.jittered_lattice(30_000, 8), 1.4, 1e-300),
-                               (synth.adversarial_density(30_000, 3, shuffle=True), 0.0, 1e-300)):
-        cfg = ax.PipelineConfig(alpha=alpha, tolerance=ax.TolerancePolicy(1e-9, eps))
-        single = eng.compute_host(c, r, cfg)
-        for world in (3, 8):
-            merged, per_rank = sharding.compute_sharded_single_gpu(c, r, cfg, world, eng)
-            for d in range(4):
-                assert np.array_equal(merged[d].cpu().numpy(), single[d]), (world, d)
-            assert sum(int(o[3].shape[0]) for o in per_rank) == single[3].shape[0]      # tets are never shared
-            assert sum(int(o[2].shape[0]) for o in per_rank) >= single[2].shape[0]
+    c, r = synth.jittered_lattice(20_000, 3)
+    # (a) duplicate centre far up the z axis
+    top = np.argsort(c[:, 2])[-40:]
+    c_dup = c.copy()
+    i, j = sorted((int(top[3]), int(top[17])))
+    c_dup[j] = c_dup[i]
+    cfg = ax.PipelineConfig(alpha=0.0)
+    with pytest.raises(ax.DuplicateCenter) as whole:
+        ax.compute_alpha_complex_arrays(c_dup, r, cfg)
+    jobs = [sharding.ShardedJob(c_dup, r, cfg, q, 4, eng) for q in range(4)]
+    errs = [job.local(raise_errors=False)[1] for job in jobs]
+    assert errs[0] is None and errs[3] is not None and errs[3].vertices == (i, j)
+    hit = sharding.pick_error(errs)
+    with pytest.raises(ax.DuplicateCenter) as sharded:
+        eng.raise_slab_error(hit[1], cfg)
+    assert str(sharded.value) == str(whole.value)
+    # (b) four coplanar, cocircular centres in the upper half: a singular tet solve; every slab that loads it
+    # reports the same solve under the same global key
+    c_deg, r_deg = c.copy(), r.copy()
+    mid = np.argsort(c[:, 2])[12_000:12_004]
+    base = c[mid[0]]
+    c_deg[mid] = base + np.array([[0, 0, 0], [1.6, 0, 0], [0, 1.6, 0], [1.6, 1.6, 0]])
+    r_deg[mid] = 1.5
+    cfg = ax.PipelineConfig(alpha=1.0)
+    ref = oracle.compute(c_deg, r_deg, 1.0)
+    assert ref.status == oracle.DEGENERATE
+    with pytest.raises(ax.DegenerateSimplex) as whole:
+        ax.compute_alpha_complex_arrays(c_deg, r_deg, cfg)
+    assert tuple(whole.value.vertices) == tuple(ref.error_vertices)
+    jobs = [sharding.ShardedJob(c_deg, r_deg, cfg, q, 5, eng) for q in range(5)]
+    errs = [job.local(raise_errors=False)[1] for job in jobs]
+    assert any(e is not None for e in errs)
+    hit = sharding.pick_error(errs)
+    assert tuple(hit[1].vertices) == tuple(ref.error_vertices)
+    with pytest.raises(ax.DegenerateSimplex) as sharded:
+        eng.raise_slab_error(hit[1], cfg)
+    assert str(sharded.value) == str(whole.value) and sharded.value.vertices == whole.value.vertices
 
 
 def test_device_merge_rows_matches_numpy():

@@ -1,7 +1,8 @@
-"""Host logic of the multi-GPU path on CPU: slab planning, halo selection, and the
-gather + merge plumbing over torch.distributed (gloo, world_size 2).  Per-slab
-results come from the CPU oracle's single-chunk pass (test infrastructure), so what
-is under test is the sharding algebra: union over slabs == whole-input result."""
+"""Host logic of the multi-GPU path on CPU: slab planning, halo selection, the agreement on one
+status, and the gather + merge plumbing over torch.distributed (gloo, world_size 2 and 3).  Per-slab
+rows are cut out of the CPU oracle's complex by generator rank (test infrastructure: exactly what a
+slab must emit), so what is under test is the sharding algebra and the transport; the CUDA slabs
+themselves are checked against the same cut in tests/test_gpu_parity.py and tests/test_gpu_sharded.py."""
 import os
 import socket
 
@@ -10,6 +11,9 @@ import pytest
 
 import oracle
 from paper_1908_05944_b200 import sharding, synth
+from paper_1908_05944_b200.errors import DegenerateSimplex, DuplicateCenter, NonFiniteCoordinate
+
+from helpers import rows_generated_in
 
 
 def arrays(res):
@@ -60,6 +64,9 @@ def test_halo_selection():
 
 
 def test_union_of_slab_chunks_is_the_complex():
+    """The reference's own chunk semantics (a chunk also emits inherited faces, pipeline.py:501-513) over slab
+    rank ranges: the union is the complex but the parts OVERLAP -- which is why the CUDA slabs settle inherited
+    faces themselves and emit by generator, so that their lists are disjoint (next test)."""
     c, r = synth.jittered_lattice(4000, 7)
     for alpha in (0.0, 1.4):
         full = oracle.compute(c, r, alpha)
@@ -68,8 +75,62 @@ def test_union_of_slab_chunks_is_the_complex():
         for d in range(4):
             merged = sharding.numpy_merge([arrays(p)[d] for p in parts], d + 1)
             assert np.array_equal(merged, arrays(full)[d])
-        # inherited faces really do cross slabs: the parts overlap
         assert sum(len(p.triangles) for p in parts) > len(full.triangles)
+
+
+def test_generator_cut_partitions_the_complex():
+    c, r = synth.adversarial_density(4000, 3, shuffle=True)
+    full = oracle.compute(c, r, 0.5, eps_singular=1e-300)
+    st, g = oracle.grid_build(c, r, 0.5)
+    plan = sharding.plan_slabs(c, r, 0.5, 5)
+    parts = [rows_generated_in(arrays(full), g.rank, lo, hi) for lo, hi in plan.rank_ranges]
+    for d in range(4):
+        assert sum(p[d].shape[0] for p in parts) == arrays(full)[d].shape[0]
+        assert np.array_equal(sharding.numpy_merge([p[d] for p in parts], d + 1), arrays(full)[d])
+        # every simplex of a slab's cut touches only loaded layers (owned + 2 halo layers each side)
+        for rank, p in enumerate(parts):
+            if p[d].size:
+                lay = plan.layer[p[d].reshape(-1)]
+                z0, z1 = plan.owned[rank]
+                assert lay.min() >= z0 and lay.max() < z1 + sharding.HALO_LAYERS
+    assert plan.layer_start[0] == 0 and plan.layer_start[-1] == len(r)
+    s = sharding.slab_input(plan, c, r, 2)
+    assert s.first_rank == plan.layer_start[s.z_lo]
+
+
+def test_plan_validates_like_the_reference():
+    c, r = synth.jittered_lattice(500, 1)
+    bad = c.copy()
+    bad[17, 1] = np.nan
+    with pytest.raises(NonFiniteCoordinate, match="ball 17 is not finite"):
+        sharding.plan_slabs(bad, r, 0.0, 2)
+    rr = r.copy()
+    rr[3] = np.inf
+    with pytest.raises(NonFiniteCoordinate, match="ball 3 is not finite"):
+        sharding.plan_slabs(c, rr, 0.0, 2)
+    with pytest.raises(ValueError, match="non-positive squared cell side"):
+        sharding.plan_slabs(c, r, -100.0, 2)
+    with pytest.raises(ValueError):
+        sharding.plan_slabs(c, r[:-1], 0.0, 2)
+
+
+def test_pick_error_is_the_reference_order():
+    E = sharding.SlabError
+    dup_a = E(status=6, vertices=(5, 9), xyz=(1.0, 2.0, 3.0))
+    dup_b = E(status=6, vertices=(2, 3), xyz=(1.0, 2.0, 2.5))
+    deg_a = E(status=7, key=(1 << 60) | (700 << 24) | 3, vertices=(1, 2))
+    deg_b = E(status=7, key=(1 << 60) | (650 << 24) | 9, vertices=(4, 8))
+    deg_tri = E(status=7, key=(3 << 60) | (10 << 24), vertices=(0, 1, 2))
+    limit = E(status=10, message="too dense")
+    assert sharding.pick_error([None, None]) is None
+    assert sharding.pick_error([None, E(0)]) is None
+    assert sharding.pick_error([deg_a, dup_a, None, dup_b])[1] is dup_b          # validation comes before any solve
+    assert sharding.pick_error([deg_a, deg_tri, deg_b]) == (2, deg_b)          # smallest (stage, rank, ordinal)
+    assert sharding.pick_error([limit, None, deg_tri])[1] is deg_tri
+    assert sharding.pick_error([None, limit])[0] == 1
+    for rec in (dup_a, deg_a, limit):
+        back = E.unpack(rec.pack())
+        assert (back.status, back.key, back.vertices, back.xyz) == (rec.status, rec.key, rec.vertices, rec.xyz)
 
 
 def _free_port():
@@ -89,9 +150,17 @@ def _worker(rank, world, port, out_dir):
         c, r = synth.jittered_lattice(3000, 9)
         alpha = 0.6
         plan = sharding.plan_slabs(c, r, alpha, world)
-        res = oracle.compute(c, r, alpha, rank_range=plan.rank_ranges[rank])
-        local = [torch.as_tensor(a) for a in arrays(res)]
-        gathered = sharding.gather_rows(local, dist, device="cpu")
+        st, g = oracle.grid_build(c, r, alpha)
+        local = [torch.as_tensor(a) for a in rows_generated_in(arrays(oracle.compute(c, r, alpha)), g.rank,
+                                                                 *plan.rank_ranges[rank])]
+        # one status for all ranks: nobody failed -> None everywhere; one rank failed -> everyone learns which error
+        assert sharding.agree_on_error(None, dist) is None
+        mine = sharding.SlabError(status=7, key=(1 << 60) | ((100 - rank) << 24), vertices=(rank, rank + 5)) if rank else None
+        hit = sharding.agree_on_error(mine, dist)
+        assert hit[0] == world - 1 and hit[1].vertices == (world - 1, world + 4)
+        stats = {}
+        gathered = sharding.gather_rows(local, dist, device="cpu", stats=stats)
+        assert stats["rows"].shape == (world, 4) and int(stats["rows"][rank, 1]) == local[1].shape[0]
         if rank == 0:
             merged = [sharding.numpy_merge([gathered[d].numpy()], d + 1) for d in range(4)]
             np.savez(os.path.join(out_dir, "merged.npz"), *merged)
