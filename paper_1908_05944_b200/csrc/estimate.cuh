@@ -60,21 +60,28 @@ __device__ __forceinline__ void sort_small(int *v, int k) {
     }
 }
 
-__device__ __noinline__ void record_singular(const EstParams &P, unsigned long long key, int v0, int v1, int v2, int v3,
-                                             int nv) {
-    atomicMin(&P.ctr->err_key, key);
+// (takes what it needs BY VALUE: a reference to the kernel's parameter block would force a copy of the whole
+// block into a local-memory stack frame)
+__device__ __noinline__ void record_singular_impl(Counters *ctr, ErrRecord *errs, unsigned long long report_key,
+                                                  unsigned long long key, int v0, int v1, int v2, int v3, int nv) {
+    atomicMin(&ctr->err_key, key);
     ErrRecord r;
     r.key = key;
     r.verts[0] = v0; r.verts[1] = v1; r.verts[2] = v2; r.verts[3] = v3;
     sort_small(r.verts, nv);
     r.nverts = nv;
     r.pad = 0;
-    if (P.report_key) {
-        if (key == P.report_key) P.errs[0] = r;
+    if (report_key) {
+        if (key == report_key) errs[0] = r;
     } else {
-        unsigned slot = atomicAdd(&P.ctr->err_count, 1u);
-        if (slot < ERR_CAP) P.errs[slot] = r;
+        unsigned slot = atomicAdd(&ctr->err_count, 1u);
+        if (slot < ERR_CAP) errs[slot] = r;
     }
+}
+
+__device__ __forceinline__ void record_singular(const EstParams &P, unsigned long long key, int v0, int v1, int v2, int v3,
+                                                int nv) {
+    record_singular_impl(P.ctr, P.errs, P.report_key, key, v0, v1, v2, v3, nv);
 }
 
 // ---------------------------------------------------------------- k_edges

@@ -187,6 +187,55 @@ def test_config3_1m_against_oracle_and_reference_golden(gold_large):
     assert (np.diff(k.vertices) > 0).all()
 
 
+def test_config3_1m_alpha14_against_oracle_and_survey_counts():
+    """SURVEY.md 8(d) config 3 at alpha = 1.4 with the H1 pivot threshold (1e-300): the counts the survey measured
+    with the real reference, and every row against the CPU oracle."""
+    c, r = synth.jittered_lattice(1_000_000, 0)
+    tol = ax.TolerancePolicy(1e-9, 1e-300)
+    k = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=1.4, tolerance=tol))
+    assert k.counts() == (1000000, 7245190, 11673237, 5174354)
+    ref = oracle.compute(c, r, 1.4, eps_singular=1e-300, threads=os.cpu_count(), chunk=4000)
+    assert ref.status == oracle.OK
+    assert_same_complex(k, ref, "1M a1.4")
+    # with the default threshold both sides raise on the tet the survey names
+    with pytest.raises(ax.DegenerateSimplex) as err:
+        ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=1.4))
+    assert tuple(err.value.vertices) == (236991, 237091, 246991, 247091)
+
+
+def test_config5_adversarial_1m_against_oracle():
+    """BASELINE config 5 at full size: 1M atoms, 20 % of the volume carved into voids, 20 % of the atoms in 3x-dense
+    cores, alpha 0, H1 tolerance -- no golden exists, the oracle is computed in the same run."""
+    c, r = synth.adversarial_density(1_000_000, 0)
+    tol = ax.TolerancePolicy(1e-9, 1e-300)
+    k = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=0.0, tolerance=tol))
+    ref = oracle.compute(c, r, 0.0, eps_singular=1e-300, threads=os.cpu_count(), chunk=4000)
+    assert ref.status == oracle.OK
+    assert_same_complex(k, ref, "adversarial 1M")
+    assert ax.closure_ok(k)
+
+
+def test_config4_10m_on_one_gpu_counts_and_oracle():
+    """BASELINE config 4's input (10M atoms, alpha 0, H1 tolerance) in ONE pass on one GPU: the counts the builder
+    logged against the oracle in round 1, every row against the oracle again, and the size-independent properties."""
+    c, r = synth.jittered_lattice(10_000_000, 0)
+    tol = ax.TolerancePolicy(1e-9, 1e-300)
+    k = ax.compute_alpha_complex_arrays(c, r, ax.PipelineConfig(alpha=0.0, tolerance=tol))
+    assert k.counts() == (10000000, 46142433, 34798584, 5092246)
+    for rows in (k.edges, k.triangles, k.tets):
+        assert (np.diff(rows, axis=1) > 0).all()
+        a, b = rows[:-1], rows[1:]
+        less = np.zeros(a.shape[0], dtype=bool)
+        equal = np.ones(a.shape[0], dtype=bool)
+        for col in range(rows.shape[1]):
+            less |= equal & (a[:, col] < b[:, col])
+            equal &= a[:, col] == b[:, col]
+        assert less.all()
+    ref = oracle.compute(c, r, 0.0, eps_singular=1e-300, threads=os.cpu_count(), chunk=8000)
+    assert ref.status == oracle.OK
+    assert_same_complex(k, ref, "10M")
+
+
 def test_alpha14_200k_tiny_eps_against_oracle():
     c, r = synth.jittered_lattice(200_000, 0)
     tol = ax.TolerancePolicy(1e-9, 1e-300)
