@@ -136,6 +136,28 @@ int axb_potential_counts(const axb_ctx *ctx, int64_t counts[3]);
  * with cached centres (m,3) / sizes (m,) (either may be NULL).  DEVICE buffers. */
 int axb_potential_export(axb_ctx *ctx, int what, int64_t *d_rows, double *d_centers, double *d_sizes);
 
+/* ---- the standalone stage operations (pipeline.py:640-731) on resident or caller-supplied levels ---------- */
+/* potential_edges (pipeline.py:640-646): stage one alone; the edge level stays resident */
+int axb_potential_edges(axb_ctx *ctx, int64_t rank_lo, int64_t rank_hi);
+/* potential triangles + tets (_chunk_potential_triangles / _tets, pipeline.py:373-479) from the RESIDENT edge level,
+ * whichever way it got there (axb_potential_edges or axb_potential_import_edges) */
+int axb_potential_simplices(axb_ctx *ctx);
+/* potential_triangles(edges, ...) / prune(potentials, ...) consume the ROWS the caller passes (pipeline.py:658-667,
+ * 712-731): replace the resident edge level by d_rows (m, 2) int64 ball indices, any row order (needs the grid);
+ * replace the resident triangle and tet lists by rows (m_t, 3) / (m_q, 4) (needs the edge level; every edge of every
+ * row must be in it).  DEVICE buffers.  AXB_ERR_BAD_ARG for rows that are not simplices of the input. */
+int axb_potential_import_edges(axb_ctx *ctx, const int64_t *d_rows, int64_t m);
+int axb_potential_import_simplices(axb_ctx *ctx, const int64_t *d_tri_rows, int64_t m_t, const int64_t *d_tet_rows, int64_t m_q);
+/* potential_tets(triangles, ...) as the reference's standalone form (pipeline.py:670-709): every given triangle
+ * (d_tri_rows: (m_t, 3) ascending ball indices, rows in lexicographic order) is extended by the larger ball indices
+ * of the 5x5x5 cell block around its first ball whose three new faces are all in the list; kept when the
+ * ortho-size is at most alpha + slack.  The given triangles and the resulting tets become the resident lists. */
+int axb_potential_tets_from_triangles(axb_ctx *ctx, const int64_t *d_tri_rows, int64_t m_t);
+/* _ac2_mask (pipeline.py:286-313) of one resident potential level (what = AXB_PE / AXB_PT / AXB_PQ), in the row
+ * order of axb_potential_export: d_mask[e] = 1 iff no non-incident ball of the 27 cells around the ortho-centre
+ * has power distance < size - eps_abs.  DEVICE buffer of uint8. */
+int axb_ac2_mask(axb_ctx *ctx, int what, uint8_t *d_mask);
+
 /* _prune_levels (pipeline.py:482-527): AC2 at every ortho-centre, inheritance of faces */
 int axb_prune(axb_ctx *ctx);
 /* canonical sort + dedup (pipeline.py:611-614, _arrays.py:12-16); counts[d] = simplices of dimension d */

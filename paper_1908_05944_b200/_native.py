@@ -26,7 +26,9 @@ SYMBOLS = (
     "axb_ctx_set_arena", "axb_arena_needed", "axb_arena_used", "axb_arena_hint", "axb_last_message",
     "axb_last_error", "axb_last_error_detail", "axb_grid_build", "axb_grid_build_slab", "axb_slab_rank_range", "axb_merge_rows", "axb_compute_slab",
     "axb_grid_get_info", "axb_grid_export", "axb_potential",
-    "axb_potential_counts", "axb_potential_export", "axb_prune", "axb_canonicalize", "axb_export",
+    "axb_potential_counts", "axb_potential_export", "axb_potential_edges", "axb_potential_simplices",
+    "axb_potential_import_edges", "axb_potential_import_simplices", "axb_potential_tets_from_triangles", "axb_ac2_mask",
+    "axb_prune", "axb_canonicalize", "axb_export",
     "axb_sync_check", "axb_compute", "axb_compute_host", "axb_export_host", "axb_compute_host_begin",
     "axb_compute_host_finish", "axb_last_d2h_bytes", "axb_stage_ms",
     "axb_kernel_launches", "axb_ortho_batch", "axb_format_complex",
@@ -86,6 +88,12 @@ def load() -> C.CDLL:
         "axb_potential": (C.c_int, [vp, i64, i64]),
         "axb_potential_counts": (C.c_int, [vp, pi64]),
         "axb_potential_export": (C.c_int, [vp, C.c_int, vp, vp, vp]),
+        "axb_potential_edges": (C.c_int, [vp, i64, i64]),
+        "axb_potential_simplices": (C.c_int, [vp]),
+        "axb_potential_import_edges": (C.c_int, [vp, vp, i64]),
+        "axb_potential_import_simplices": (C.c_int, [vp, vp, i64, vp, i64]),
+        "axb_potential_tets_from_triangles": (C.c_int, [vp, vp, i64]),
+        "axb_ac2_mask": (C.c_int, [vp, C.c_int, vp]),
         "axb_prune": (C.c_int, [vp]),
         "axb_canonicalize": (C.c_int, [vp, pi64]),
         "axb_export": (C.c_int, [vp, vp, vp, vp, vp]),

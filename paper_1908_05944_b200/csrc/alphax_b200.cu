@@ -13,6 +13,7 @@
 #include "prune.cuh"
 #include "scan.cuh"
 #include "sparse.cuh"
+#include "stages.cuh"
 #include "widen_pool.h"
 
 #include <math.h>
@@ -43,7 +44,7 @@ struct HostBlock {            // pinned; filled by async copies
     int2 dups[DUP_CAP];
 };
 
-enum State { S_NONE = 0, S_GRID = 1, S_POTENTIAL = 2, S_PRUNED = 3, S_CANON = 4 };
+enum State { S_NONE = 0, S_GRID = 1, S_EDGES = 2, S_POTENTIAL = 3, S_PRUNED = 4, S_CANON = 5 };
 
 }  // namespace
 
@@ -869,6 +870,7 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
     c->n_pe = c->h->ctr.n_pe;
     c->W = c->h->ctr.max_deg <= 64 ? 1 : 4;
     c->mark_after_edges = c->arena_used;
+    c->state = S_EDGES;
     return AXB_OK;
 }
 
@@ -1040,8 +1042,10 @@ extern "C" int axb_potential(axb_ctx *c, int64_t lo, int64_t hi) {
 
 extern "C" int axb_potential_counts(const axb_ctx *c, int64_t counts[3]) {
     if (!c || !counts) return AXB_ERR_BAD_ARG;
-    if (c->state < S_POTENTIAL) return AXB_ERR_STATE;
-    counts[0] = c->n_pe; counts[1] = c->n_pt; counts[2] = c->n_pq;
+    if (c->state < S_EDGES) return AXB_ERR_STATE;
+    counts[0] = c->n_pe;
+    counts[1] = c->state >= S_POTENTIAL ? c->n_pt : 0;
+    counts[2] = c->state >= S_POTENTIAL ? c->n_pq : 0;
     return AXB_OK;
 }
 
@@ -1077,14 +1081,203 @@ __global__ void k_export_potential(int what, unsigned m, const Atom *__restrict_
 
 extern "C" int axb_potential_export(axb_ctx *c, int what, int64_t *d_rows, double *d_centers, double *d_sizes) {
     if (!c) return AXB_ERR_BAD_ARG;
-    if (c->state < S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_potential_export before axb_potential");
     if (what < AXB_PE || what > AXB_PQ) return fail(c, AXB_ERR_BAD_ARG, "what must be AXB_PE, AXB_PT or AXB_PQ");
+    if (c->state < (what == AXB_PE ? S_EDGES : S_POTENTIAL)) return fail(c, AXB_ERR_STATE, "axb_potential_export: that level is not resident");
     if (what == AXB_PQ && c->pq_r == nullptr)
         return fail(c, AXB_ERR_STATE, "the potential-tet list is not materialised by axb_compute (fused path); use axb_potential");
     unsigned m = what == AXB_PE ? c->n_pe : (what == AXB_PT ? c->n_pt : c->n_pq);
     if (m) {
         k_export_potential<<<blocks_for(m, 128), 128, 0, c->stream>>>(what, m, c->atoms, c->orig, c->pe_u, c->pe_v, c->pt,
                                                                       c->pq_r, c->tol.eps_sing, d_rows, d_centers, d_sizes);
+        LAUNCH_CHECK(c);
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return AXB_OK;
+}
+
+// ---- stage operations on resident or caller-supplied levels (stages.cuh) ----
+
+extern "C" int axb_potential_edges(axb_ctx *c, int64_t lo, int64_t hi) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    c->cull = false;
+    return run_edges(c, lo, hi);
+}
+
+namespace {
+// the triangle / tet counters back to their state after the edge stage (a stage may be run again)
+int reset_simplex_counters(axb_ctx *c) {
+    c->h->ctr.n_pt = 0; c->h->ctr.n_pq = 0; c->h->ctr.overflow = 0; c->h->ctr.tile_next = 0;
+    c->h->ctr.err_key = ~0ull; c->h->ctr.err_count = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
+    return AXB_OK;
+}
+}  // namespace
+
+extern "C" int axb_potential_simplices(axb_ctx *c) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (c->state < S_EDGES) return fail(c, AXB_ERR_STATE, "axb_potential_simplices needs the potential edges first");
+    c->cull = false;
+    c->state = S_EDGES;
+    int st = reset_simplex_counters(c);
+    if (st != AXB_OK) return st;
+    if ((st = mark_event(c, AXB_ST_POT_TRIANGLES)) != AXB_OK) return st;
+    return run_tri_tet_lists(c);
+}
+
+extern "C" int axb_potential_import_edges(axb_ctx *c, const int64_t *d_rows, int64_t m) {
+    if (!c || m < 0 || (m > 0 && !d_rows)) return AXB_ERR_BAD_ARG;
+    if (c->state < S_GRID) return fail(c, AXB_ERR_STATE, "axb_potential_import_edges before axb_grid_build");
+    if (c->slab_mode) return fail(c, AXB_ERR_STATE, "levels cannot be imported into a slab");
+    if (m > 0xfffffff0ll) return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential edges");
+    const int n = (int)c->n;
+    c->state = S_GRID;
+    c->arena_used = c->mark_after_grid;
+    c->rank_lo = 0; c->rank_hi = n; c->gen_lo = 0;
+    c->dup_pending = false;
+    memset(&c->h->ctr, 0, sizeof(Counters));
+    c->h->ctr.err_key = ~0ull;
+    c->h->ctr.first_bad = 0xffffffffu;
+    c->h->ctr.n_pe = (unsigned)m;
+    CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
+    int st;
+    if ((st = mark_event(c, AXB_ST_POT_EDGES)) != AXB_OK) return st;
+    ARENA(c, c->adj_off, uint32_t, (size_t)n + 2);
+    ARENA(c, c->deg, int, (size_t)n + 2);
+    c->pe_cap = (uint32_t)std::max<int64_t>(m, 1);
+    ARENA(c, c->pe_v, int, c->pe_cap);
+    ARENA(c, c->pe_u, int, c->pe_cap);
+    const size_t mark = c->arena_used;
+    int *cursor;
+    ARENA(c, cursor, int, (size_t)n + 2);
+    CUDA_TRY(c, cudaMemsetAsync(c->deg, 0, sizeof(int) * ((size_t)n + 2), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(cursor, 0, sizeof(int) * ((size_t)n + 2), c->stream));
+    if (m) {
+        k_import_edge_count<<<blocks_for((size_t)m, 256), 256, 0, c->stream>>>(d_rows, (unsigned)m, n, c->rank, c->deg, c->ctr);
+        LAUNCH_CHECK(c);
+    }
+    if ((st = device_scan(c, reinterpret_cast<const uint32_t *>(c->deg), (size_t)n, c->adj_off)) != AXB_OK) return st;
+    if (m) {
+        k_import_edge_scatter<<<blocks_for((size_t)m, 256), 256, 0, c->stream>>>(d_rows, (unsigned)m, n, c->rank, c->adj_off, cursor, c->pe_u, c->pe_v);
+        LAUNCH_CHECK(c);
+    }
+    k_import_edge_order<<<blocks_for((size_t)n, 256), 256, 0, c->stream>>>(n, c->adj_off, c->deg, c->pe_v, c->ctr);
+    LAUNCH_CHECK(c);
+    if ((st = fetch_counters(c)) != AXB_OK) return st;
+    c->arena_used = mark;
+    if ((st = mark_event(c, AXB_ST_POT_EDGES + 1)) != AXB_OK) return st;
+    if (c->h->ctr.overflow & (1u << 6)) return fail(c, AXB_ERR_BAD_ARG, "edge rows must hold two different ball indices in [0, n)");
+    if (c->h->ctr.overflow & (1u << 7)) return fail(c, AXB_ERR_BAD_ARG, "edge rows hold the same edge twice");
+    if (c->h->ctr.max_deg > (unsigned)AXB_MAX_PARTNERS)
+        return fail(c, AXB_ERR_DENSITY, "a ball has more than %d potential-edge partners", AXB_MAX_PARTNERS);
+    c->n_pe = (uint32_t)m;
+    c->W = c->h->ctr.max_deg <= 64 ? 1 : 4;
+    c->mark_after_edges = c->arena_used;
+    c->state = S_EDGES;
+    return AXB_OK;
+}
+
+namespace {
+// allocate the triangle / tet lists after the edges and translate triangle rows into them
+int import_triangles(axb_ctx *c, const int64_t *d_tri, int64_t m_t, uint32_t pq_cap) {
+    c->arena_used = c->mark_after_edges;
+    c->pt_cap = (uint32_t)std::max<int64_t>(m_t, 1);
+    c->pq_cap = std::max<uint32_t>(pq_cap, 1);
+    ARENA(c, c->pt, int4, c->pt_cap);
+    ARENA(c, c->pq_r, int4, c->pq_cap);
+    ARENA(c, c->pq_l, int, c->pq_cap);
+    if (m_t) {
+        k_import_simplices<<<blocks_for((size_t)m_t, 256), 256, 0, c->stream>>>(3, d_tri, (unsigned)m_t, (int)c->n, c->rank, c->adj_off,
+                                                                             c->deg, c->pe_v, c->pt, c->pq_r, c->pq_l, c->ctr);
+        LAUNCH_CHECK(c);
+    }
+    return AXB_OK;
+}
+
+int finish_import(axb_ctx *c) {
+    int st = fetch_counters(c);
+    if (st != AXB_OK) return st;
+    if (c->h->ctr.overflow & (1u << 6))
+        return fail(c, AXB_ERR_BAD_ARG, "a row names a ball outside [0, n), repeats one, or has an edge that is not in the edge level");
+    if (c->h->ctr.err_key != ~0ull) return report_degenerate(c);
+    c->n_pt = c->h->ctr.n_pt;
+    c->n_pq = c->h->ctr.n_pq;
+    c->k3_cap = c->pq_cap;
+    c->many_tets = false;
+    c->state = S_POTENTIAL;
+    return AXB_OK;
+}
+}  // namespace
+
+extern "C" int axb_potential_import_simplices(axb_ctx *c, const int64_t *d_tri, int64_t m_t, const int64_t *d_tet, int64_t m_q) {
+    if (!c || m_t < 0 || m_q < 0 || (m_t > 0 && !d_tri) || (m_q > 0 && !d_tet)) return AXB_ERR_BAD_ARG;
+    if (c->state < S_EDGES) return fail(c, AXB_ERR_STATE, "axb_potential_import_simplices needs the potential edges first");
+    if (m_t > 0xfffffff0ll || m_q > 0xfffffff0ll) return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential triangles or tetrahedra");
+    c->state = S_EDGES;
+    c->h->ctr.n_pt = (unsigned)m_t; c->h->ctr.n_pq = (unsigned)m_q; c->h->ctr.overflow = 0;
+    c->h->ctr.err_key = ~0ull; c->h->ctr.err_count = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
+    int st = import_triangles(c, d_tri, m_t, (uint32_t)m_q);
+    if (st != AXB_OK) return st;
+    if (m_q) {
+        k_import_simplices<<<blocks_for((size_t)m_q, 256), 256, 0, c->stream>>>(4, d_tet, (unsigned)m_q, (int)c->n, c->rank, c->adj_off,
+                                                                             c->deg, c->pe_v, c->pt, c->pq_r, c->pq_l, c->ctr);
+        LAUNCH_CHECK(c);
+    }
+    return finish_import(c);
+}
+
+extern "C" int axb_potential_tets_from_triangles(axb_ctx *c, const int64_t *d_tri, int64_t m_t) {
+    if (!c || m_t < 0 || (m_t > 0 && !d_tri)) return AXB_ERR_BAD_ARG;
+    if (c->state < S_EDGES) return fail(c, AXB_ERR_STATE, "axb_potential_tets_from_triangles needs the potential edges first");
+    if (m_t > 0xfffffff0ll) return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential triangles");
+    c->state = S_EDGES;
+    uint64_t want = (uint64_t)m_t + 4096;
+    for (int attempt = 0;; ++attempt) {
+        if (want > 0xfffffff0ull) return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential tetrahedra");
+        c->h->ctr.n_pt = (unsigned)m_t; c->h->ctr.n_pq = 0; c->h->ctr.overflow = 0;
+        c->h->ctr.err_key = ~0ull; c->h->ctr.err_count = 0;
+        CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
+        int st = import_triangles(c, d_tri, m_t, (uint32_t)want);
+        if (st != AXB_OK) return st;
+        if (m_t) {
+            TetsFromTris P;
+            P.g = c->g; P.atoms = c->atoms; P.orig = c->orig; P.rank = c->rank; P.cell_of_rank = c->cell_of_rank;
+            P.adj_off = c->adj_off; P.deg = c->deg; P.pe_v = c->pe_v; P.rows = d_tri; P.m = (unsigned)m_t;
+            P.lim_a = c->tol.lim_a; P.eps_sing = c->tol.eps_sing;
+            P.pq_r = c->pq_r; P.pq_l = c->pq_l; P.pq_cap = c->pq_cap; P.ctr = c->ctr; P.errs = c->errs; P.report_key = 0;
+            k_tets_from_triangles<<<blocks_for((size_t)m_t, 128), 128, 0, c->stream>>>(P);
+            LAUNCH_CHECK(c);
+        }
+        if ((st = fetch_counters(c)) != AXB_OK) return st;
+        if (c->h->ctr.err_key != ~0ull && c->h->ctr.err_count > (unsigned)ERR_CAP) {
+            // more singular solves than record slots: once more with only the first one (smallest key) reporting
+            TetsFromTris P;
+            P.g = c->g; P.atoms = c->atoms; P.orig = c->orig; P.rank = c->rank; P.cell_of_rank = c->cell_of_rank;
+            P.adj_off = c->adj_off; P.deg = c->deg; P.pe_v = c->pe_v; P.rows = d_tri; P.m = (unsigned)m_t;
+            P.lim_a = c->tol.lim_a; P.eps_sing = c->tol.eps_sing;
+            P.pq_r = c->pq_r; P.pq_l = c->pq_l; P.pq_cap = 0; P.ctr = c->ctr; P.errs = c->errs; P.report_key = c->h->ctr.err_key;
+            k_tets_from_triangles<<<blocks_for((size_t)m_t, 128), 128, 0, c->stream>>>(P);
+            LAUNCH_CHECK(c);
+            CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+            c->h->ctr.err_count = 1;
+            return report_degenerate(c);
+        }
+        if (c->h->ctr.n_pq <= c->pq_cap) break;
+        if (attempt >= 2) return fail(c, AXB_ERR_INTERNAL, "potential-tet buffer still too small after resize");
+        want = (uint64_t)c->h->ctr.n_pq + 1024;
+    }
+    return finish_import(c);
+}
+
+extern "C" int axb_ac2_mask(axb_ctx *c, int what, uint8_t *d_mask) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (what < AXB_PE || what > AXB_PQ) return fail(c, AXB_ERR_BAD_ARG, "what must be AXB_PE, AXB_PT or AXB_PQ");
+    if (c->state < (what == AXB_PE ? S_EDGES : S_POTENTIAL)) return fail(c, AXB_ERR_STATE, "axb_ac2_mask: that level is not resident");
+    const unsigned m = what == AXB_PE ? c->n_pe : (what == AXB_PT ? c->n_pt : c->n_pq);
+    if (m) {
+        if (!d_mask) return AXB_ERR_BAD_ARG;
+        k_ac2_mask<<<blocks_for(m, 128), 128, 0, c->stream>>>(what - AXB_PE, m, c->g, c->tol, c->atoms, c->orig, c->pe_u, c->pe_v, c->pt,
+                                                              c->pq_r, d_mask);
         LAUNCH_CHECK(c);
     }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1403,12 +1596,20 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
         c->h_stage_elems = want;
     }
     if ((st = ensure_pool(c)) != AXB_OK) return st;
-    const size_t max_chunks = stage_elems / D2H_CHUNK + 8;
-    while (c->chunk_ev.size() < max_chunks) {
-        cudaEvent_t e;
-        CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        c->chunk_ev.push_back(e);
-    }
+    // one event per D2H chunk: a chunk holds rows_per_chunk_of[d] whole rows, which can be fewer values than D2H_CHUNK
+    // (24-bit planes round the rows down to a power of two), so count chunks per dimension
+    size_t max_chunks = 8;
+    for (int d = 0; d < 4; ++d)
+        max_chunks += ((size_t)std::max<int64_t>(c->host_cap[d], 1) + rows_per_chunk_of[d] - 1) / rows_per_chunk_of[d] + 1;
+    auto grow_events = [&](size_t want) -> int {
+        while (c->chunk_ev.size() < want) {
+            cudaEvent_t e;
+            CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->chunk_ev.push_back(e);
+        }
+        return AXB_OK;
+    };
+    if ((st = grow_events(max_chunks)) != AXB_OK) return st;
     PruneParams P = prune_params(c);
     CanonParams Q;
     Q.n = (int)n; Q.orig = c->orig; Q.adj_off = c->adj_off; Q.pe_u = c->pe_u; Q.pe_v = c->pe_v; Q.pe_cap = c->pe_cap;
@@ -1443,8 +1644,8 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(3, c->off3 + n)) != AXB_OK) return st;
     k_scatter_tets<<<grid, 256, 0, c->stream>>>(Q);
     LAUNCH_CHECK(c);
-    if (p24) k_emit_tets<Packed24Out><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, 0u, c->off3 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[3]), rows_shift[3]}, c->ctr);
-    else k_emit_tets<PlainOut<int32_t>><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, 0u, c->off3 + n, nullptr, PlainOut<int32_t>{d_out[3]}, c->ctr);
+    if (p24) k_emit_tets<Packed24Out><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->host_cap[3], c->off3 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[3]), rows_shift[3]}, c->ctr);
+    else k_emit_tets<PlainOut<int32_t>><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->host_cap[3], c->off3 + n, nullptr, PlainOut<int32_t>{d_out[3]}, c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(3)) != AXB_OK) return st;
     // triangles
@@ -1455,9 +1656,9 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(2, c->off2 + n)) != AXB_OK) return st;
     k_scatter_tris<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[2]);
     LAUNCH_CHECK(c);
-    if (p24) k_emit_tris<Packed24Out, false><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[2]), rows_shift[2]}, c->ctr);
-    else if (compact2) k_emit_tris<PlainOut<int32_t>, true><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, PlainOut<int32_t>{d_out[2]}, c->ctr);
-    else k_emit_tris<PlainOut<int32_t>, false><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, 0u, c->off2 + n, nullptr, PlainOut<int32_t>{d_out[2]}, c->ctr);
+    if (p24) k_emit_tris<Packed24Out, false><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->host_cap[2], c->off2 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[2]), rows_shift[2]}, c->ctr);
+    else if (compact2) k_emit_tris<PlainOut<int32_t>, true><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->host_cap[2], c->off2 + n, nullptr, PlainOut<int32_t>{d_out[2]}, c->ctr);
+    else k_emit_tris<PlainOut<int32_t>, false><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, (unsigned)c->host_cap[2], c->off2 + n, nullptr, PlainOut<int32_t>{d_out[2]}, c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(2)) != AXB_OK) return st;
     // edges
@@ -1468,9 +1669,9 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_total(1, c->off1 + n)) != AXB_OK) return st;
     k_scatter_edges<<<grid, 256, 0, c->stream>>>(Q, (unsigned)c->host_cap[1]);
     LAUNCH_CHECK(c);
-    if (p24) k_emit_edges<Packed24Out, false><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[1]), rows_shift[1]}, c->ctr);
-    else if (compact1) k_emit_edges<PlainOut<int32_t>, true><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, PlainOut<int32_t>{d_out[1]}, c->ctr);
-    else k_emit_edges<PlainOut<int32_t>, false><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, 0u, c->off1 + n, nullptr, PlainOut<int32_t>{d_out[1]}, c->ctr);
+    if (p24) k_emit_edges<Packed24Out, false><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->host_cap[1], c->off1 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[1]), rows_shift[1]}, c->ctr);
+    else if (compact1) k_emit_edges<PlainOut<int32_t>, true><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->host_cap[1], c->off1 + n, nullptr, PlainOut<int32_t>{d_out[1]}, c->ctr);
+    else k_emit_edges<PlainOut<int32_t>, false><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, (unsigned)c->host_cap[1], c->off1 + n, nullptr, PlainOut<int32_t>{d_out[1]}, c->ctr);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(1)) != AXB_OK) return st;
     // vertices
@@ -1546,7 +1747,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
                 char *hst = reinterpret_cast<char *>(stage);
                 for (size_t lo = 0; lo < rows; lo += rows_per_chunk) {
                     const size_t m = std::min(rows_per_chunk, rows - lo);
-                    if (chunks.size() >= c->chunk_ev.size()) return fail(c, AXB_ERR_INTERNAL, "chunk event pool exhausted");
+                    if ((st = grow_events(chunks.size() + 1)) != AXB_OK) return st;
                     cudaEvent_t ev = c->chunk_ev[chunks.size()];
                     CUDA_TRY(c, cudaMemcpyAsync(hst + lo * w * 3, dev + lo * w * 3, m * w * 3, cudaMemcpyDeviceToHost, c->copy_stream));
                     CUDA_TRY(c, cudaEventRecord(ev, c->copy_stream));
@@ -1565,7 +1766,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
             CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->dim_ready[d], 0));
             for (size_t lo = 0; lo < rows; lo += rows_per_chunk) {
                 const size_t m = std::min(rows_per_chunk, rows - lo);
-                if (chunks.size() >= c->chunk_ev.size()) return fail(c, AXB_ERR_INTERNAL, "chunk event pool exhausted");
+                if ((st = grow_events(chunks.size() + 1)) != AXB_OK) return st;
                 cudaEvent_t ev = c->chunk_ev[chunks.size()];
                 CUDA_TRY(c, cudaMemcpyAsync(stage + lo * w, d_out[d] + lo * w, m * w * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                             c->copy_stream));

@@ -158,13 +158,17 @@ struct Packed24Out {
 };
 
 // `total_dev` (optional) = device-side row count (the last entry of the offset array): lets the caller
-// launch without knowing the count on the host.
+// launch without knowing the count on the host; `total` then carries the capacity the buffers were sized for.
 // SKIP0: write only the columns after the owner (the host rebuilds column 0 from the offsets)
 template <class Out, bool SKIP0 = false>
 __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                     unsigned total, const uint32_t *__restrict__ total_dev,
                                                     const int64_t *__restrict__ map, Out out, Counters *ctr) {
-    if (total_dev) total = *total_dev;
+    if (total_dev) {                        // device-side row count; `total` then is the CAPACITY of tmp / out: when the
+        const unsigned cap = total;         // count exceeds it the host falls back (AXB_ERR_STATE) and nothing is read
+        total = *total_dev;
+        if (total > cap) return;
+    }
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int2 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];
@@ -188,7 +192,11 @@ template <class Out, bool SKIP0 = false>
 __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                    unsigned total, const uint32_t *__restrict__ total_dev,
                                                    const int64_t *__restrict__ map, Out out, Counters *ctr) {
-    if (total_dev) total = *total_dev;
+    if (total_dev) {                        // device-side row count; `total` then is the CAPACITY of tmp / out: when the
+        const unsigned cap = total;         // count exceeds it the host falls back (AXB_ERR_STATE) and nothing is read
+        total = *total_dev;
+        if (total > cap) return;
+    }
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int4 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];
@@ -215,7 +223,11 @@ template <class Out>
 __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                    unsigned total, const uint32_t *__restrict__ total_dev,
                                                    const int64_t *__restrict__ map, Out out, Counters *ctr) {
-    if (total_dev) total = *total_dev;
+    if (total_dev) {                        // device-side row count; `total` then is the CAPACITY of tmp / out: when the
+        const unsigned cap = total;         // count exceeds it the host falls back (AXB_ERR_STATE) and nothing is read
+        total = *total_dev;
+        if (total > cap) return;
+    }
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
     const int4 me = tmp[s];
     const unsigned lo = off[me.x], hi = off[me.x + 1];

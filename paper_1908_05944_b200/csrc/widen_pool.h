@@ -290,10 +290,15 @@ public:
             return;
         }
         size_t p = published_.load(std::memory_order_relaxed);
-        for (size_t lo = 0; lo < n && p < tasks_.size(); lo += piece) {
-            tasks_[p++] = WidenTask{src ? src + lo * src_width : nullptr, dst + lo * dst_width, n - lo < piece ? n - lo : piece,
-                                    kind, off, n_index, row0 + lo};
-            published_.store(p, std::memory_order_release);
+        for (size_t lo = 0; lo < n; lo += piece) {
+            const WidenTask t{src ? src + lo * src_width : nullptr, dst + lo * dst_width, n - lo < piece ? n - lo : piece,
+                              kind, off, n_index, row0 + lo};
+            if (p < tasks_.size()) {
+                tasks_[p++] = t;
+                published_.store(p, std::memory_order_release);
+            } else {
+                run_task(t);      // the task array is full (it cannot grow under the workers): never drop, do it here
+            }
         }
     }
     // parallel memcpy of `bytes` (a multiple of 8) from src to dst in pieces of piece_bytes
@@ -304,12 +309,17 @@ public:
             return;
         }
         size_t p = published_.load(std::memory_order_relaxed);
-        for (size_t lo = 0; lo < bytes && p < tasks_.size(); lo += piece_bytes) {
+        for (size_t lo = 0; lo < bytes; lo += piece_bytes) {
             const size_t m = bytes - lo < piece_bytes ? bytes - lo : piece_bytes;
-            tasks_[p++] = WidenTask{reinterpret_cast<const int32_t *>(static_cast<const char *>(src) + lo),
-                                    reinterpret_cast<int64_t *>(static_cast<char *>(dst) + lo), m / sizeof(int32_t), WK_COPY,
-                                    nullptr, 0, 0};
-            published_.store(p, std::memory_order_release);
+            const WidenTask t{reinterpret_cast<const int32_t *>(static_cast<const char *>(src) + lo),
+                              reinterpret_cast<int64_t *>(static_cast<char *>(dst) + lo), m / sizeof(int32_t), WK_COPY,
+                              nullptr, 0, 0};
+            if (p < tasks_.size()) {
+                tasks_[p++] = t;
+                published_.store(p, std::memory_order_release);
+            } else {
+                run_task(t);
+            }
         }
     }
     // no more tasks: help with what is left and wait until every task has run

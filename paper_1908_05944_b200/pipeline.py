@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _native as N
 from .errors import (AlphaxError, DegenerateSimplex, DuplicateCenter, EmptyInput, NativeLibraryMissing,
-                     NonFiniteCoordinate)
+                     NonFiniteCoordinate, UnsupportedMode)
 from .types import Ball, SimplexKey, TolerancePolicy
 
 STAGE_NAMES = ("grid", "potential_edges", "potential_triangles", "potential_tets",
@@ -185,6 +185,12 @@ class Engine:
             raise AlphaxError(f"axb_ctx_create failed: {self.lib.axb_status_name(st).decode()}")
         self.arena = None
         self.last_stage_ms: dict = {}
+        # identity of what is resident on the device, for the stage API's handles (stages.py): a new token for every
+        # run that rebuilds the grid, a new id for every edge level / simplex level computed or imported
+        self.token = 0
+        self.edge_id = 0
+        self.simplex_id = 0
+        self.stage_key = None
         if arena_bytes:
             self._set_arena(arena_bytes)
 
@@ -210,7 +216,11 @@ class Engine:
         if st != N.OK:
             raise AlphaxError(self._message())
 
-    def _bind_stream(self):
+    def _bind_stream(self, fresh: bool = True):
+        """fresh: the call rebuilds the device state from the inputs, so handles of the stage API go stale."""
+        if fresh:
+            self.token += 1
+            self.stage_key = None
         stream = self.torch.cuda.current_stream(self.device)
         self.lib.axb_ctx_set_stream(self.handle, C.c_void_p(stream.cuda_stream))
 
@@ -384,8 +394,9 @@ class Engine:
         if st != N.OK:
             self._raise(st, cfg, centers, radii)
 
-    def stage_grid(self, centers, radii, cfg: PipelineConfig, arena_factor: float = 4.0):
-        """validate_input + build_grid_arrays on CUDA tensors; returns the grid geometry."""
+    def stage_grid(self, centers, radii, cfg: PipelineConfig, arena_factor: float = 4.0, key=None):
+        """validate_input + build_grid_arrays on CUDA tensors; returns the grid geometry.
+        key: what the caller wants to recognise this device state by later (stages.py)."""
         torch = self.torch
         self._stage_inputs = (centers.to(dtype=torch.float64).contiguous().reshape(-1, 3),
                               radii.to(dtype=torch.float64).contiguous().reshape(-1))
@@ -400,6 +411,7 @@ class Engine:
             st = self.lib.axb_grid_build(self.handle, n, self._stage_inputs[0].data_ptr(),
                                          self._stage_inputs[1].data_ptr(), C.byref(prm))
         self._check(st, cfg, *self._stage_inputs)
+        self.stage_key = key
         info = N.GridInfo()
         self.lib.axb_grid_get_info(self.handle, C.byref(info))
         return dict(origin=np.array(list(info.origin)), cell_side=float(info.cell_side),
@@ -412,35 +424,89 @@ class Engine:
         self._check(self.lib.axb_grid_export(self.handle, *(o.data_ptr() for o in out)), self._stage_cfg)
         return out      # order, rank, ball_cells
 
-    def stage_potential(self, lo: int = 0, hi: int | None = None):
-        n = self._stage_inputs[0].shape[0]
-        st = self.lib.axb_potential(self.handle, int(lo), int(n if hi is None else hi))
+    def _stage_call(self, fn, *args):
+        with self.torch.cuda.device(self.device):
+            self._bind_stream(fresh=False)
+            st = fn(self.handle, *args)
         self._check(st, self._stage_cfg, *self._stage_inputs)
+
+    def _rows_arg(self, rows, k: int):
+        torch = self.torch
+        t = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.int64).reshape(-1, k) if isinstance(rows, np.ndarray) else rows,
+                            device=f"cuda:{self.device}").to(dtype=torch.int64).contiguous().reshape(-1, k)
+        return t, (t.data_ptr() if t.shape[0] else None), int(t.shape[0])
+
+    def stage_potential(self, lo: int = 0, hi: int | None = None):
+        """All three potential levels for the generators at grid ranks [lo, hi) (one reference chunk)."""
+        n = self._stage_inputs[0].shape[0]
+        self._stage_call(self.lib.axb_potential, int(lo), int(n if hi is None else hi))
+        self.edge_id += 1
+        self.simplex_id += 1
+        return self.stage_potential_counts()
+
+    def stage_potential_counts(self):
         counts = (C.c_int64 * 3)()
         self.lib.axb_potential_counts(self.handle, counts)
         return tuple(int(v) for v in counts)
 
+    def stage_edges(self, lo: int = 0, hi: int | None = None):
+        """Stage one alone (potential_edges, pipeline.py:640-646); the level stays resident."""
+        n = self._stage_inputs[0].shape[0]
+        self._stage_call(self.lib.axb_potential_edges, int(lo), int(n if hi is None else hi))
+        self.edge_id += 1
+        return self.stage_potential_counts()[0]
+
+    def stage_import_edges(self, rows):
+        """Replace the resident edge level by caller rows (m, 2) of ball indices."""
+        keep, ptr, m = self._rows_arg(rows, 2)
+        self._stage_call(self.lib.axb_potential_import_edges, ptr, m)
+        self.edge_id += 1
+
+    def stage_simplices(self):
+        """Potential triangles + tets from the resident edge level."""
+        self._stage_call(self.lib.axb_potential_simplices)
+        self.simplex_id += 1
+        return self.stage_potential_counts()
+
+    def stage_import_simplices(self, tri_rows, tet_rows):
+        kt, pt, mt = self._rows_arg(tri_rows, 3)
+        kq, pq, mq = self._rows_arg(tet_rows, 4)
+        self._stage_call(self.lib.axb_potential_import_simplices, pt, mt, pq, mq)
+        self.simplex_id += 1
+
+    def stage_tets_from_triangles(self, tri_rows):
+        """The reference's standalone potential_tets (pipeline.py:670-709) on caller triangle rows."""
+        kt, pt, mt = self._rows_arg(tri_rows, 3)
+        self._stage_call(self.lib.axb_potential_tets_from_triangles, pt, mt)
+        self.simplex_id += 1
+        return self.stage_potential_counts()
+
+    def stage_ac2_mask(self, dim: int):
+        """_ac2_mask (pipeline.py:286-313) of the resident potential level `dim`, in stage_potential_export's row order."""
+        torch = self.torch
+        m = self.stage_potential_counts()[dim - 1]
+        mask = torch.empty(m, dtype=torch.uint8, device=f"cuda:{self.device}")
+        self._stage_call(self.lib.axb_ac2_mask, N.PE + dim - 1, mask.data_ptr() if m else None)
+        return mask.to(torch.bool)
+
     def stage_potential_export(self, dim: int):
         """(rows, centres, sizes) of one potential level as CUDA tensors, in generation order."""
         torch = self.torch
-        counts = (C.c_int64 * 3)()
-        self.lib.axb_potential_counts(self.handle, counts)
-        m = int(counts[dim - 1])
+        m = self.stage_potential_counts()[dim - 1]
         dev = f"cuda:{self.device}"
         rows = torch.empty((m, dim + 1), dtype=torch.int64, device=dev)
         cen = torch.empty((m, 3), dtype=torch.float64, device=dev)
         siz = torch.empty(m, dtype=torch.float64, device=dev)
-        st = self.lib.axb_potential_export(self.handle, N.PE + dim - 1, rows.data_ptr() if m else None,
-                                           cen.data_ptr() if m else None, siz.data_ptr() if m else None)
-        self._check(st, self._stage_cfg)
+        self._stage_call(self.lib.axb_potential_export, N.PE + dim - 1, rows.data_ptr() if m else None,
+                         cen.data_ptr() if m else None, siz.data_ptr() if m else None)
         return rows, cen, siz
 
     def stage_prune(self):
-        self._check(self.lib.axb_prune(self.handle), self._stage_cfg, *self._stage_inputs)
+        self._stage_call(self.lib.axb_prune)
 
     def stage_canonicalize(self):
         counts = (C.c_int64 * 4)()
-        self._check(self.lib.axb_canonicalize(self.handle, counts), self._stage_cfg, *self._stage_inputs)
+        self._stage_call(self.lib.axb_canonicalize, counts)
         return tuple(int(v) for v in counts)
 
     def stage_export(self, counts):
@@ -448,10 +514,8 @@ class Engine:
         dev = f"cuda:{self.device}"
         outs = [torch.empty((int(counts[d]),) if d == 0 else (int(counts[d]), d + 1), dtype=torch.int64, device=dev)
                 for d in range(4)]
-        st = self.lib.axb_export(self.handle, *(o.data_ptr() if o.numel() else None for o in outs))
-        if st == N.OK:
-            st = self.lib.axb_sync_check(self.handle)
-        self._check(st, self._stage_cfg, *self._stage_inputs)
+        self._stage_call(self.lib.axb_export, *(o.data_ptr() if o.numel() else None for o in outs))
+        self._stage_call(self.lib.axb_sync_check)
         self._collect_stage_ms()
         return outs
 
@@ -531,7 +595,7 @@ class Engine:
         siz = torch.empty(m, dtype=torch.float64, device=dev)
         sg = torch.zeros(m, dtype=torch.uint8, device=dev)
         with torch.cuda.device(self.device):
-            self._bind_stream()
+            self._bind_stream(fresh=False)
             st = self.lib.axb_ortho_batch(self.handle, m, k, p.data_ptr(), q.data_ptr(), float(eps_singular),
                                           cen.data_ptr(), siz.data_ptr(), sg.data_ptr())
         if st != N.OK:
@@ -570,11 +634,19 @@ def as_ball_arrays(balls: Sequence[Ball]):
     return centers, radii
 
 
+# the keys the reference's compute_alpha_complex writes into stage_times (pipeline.py:498-549, 595)
+_REFERENCE_STAGE_KEYS = ("grid", "potential_edges", "potential_triangles", "potential_tets", "prune_tets",
+                         "prune_triangles", "prune_edges", "prune_vertices")
+
+
 def _accumulate_stage_times(stage_times, stage_ms: dict):
+    """CUDA-event seconds per stage into the caller's dict -- the reference's keys only (its merge + unique,
+    pipeline.py:611-614, is not timed either); the canonicalisation and export times stay in Engine.last_stage_ms."""
     if stage_times is None:
         return
-    for key, ms in stage_ms.items():
-        stage_times[key] = stage_times.get(key, 0.0) + ms * 1e-3
+    for key in _REFERENCE_STAGE_KEYS:
+        if key in stage_ms:
+            stage_times[key] = stage_times.get(key, 0.0) + stage_ms[key] * 1e-3
 
 
 def compute_alpha_complex_arrays(centers, radii, cfg: PipelineConfig, stage_times: dict | None = None,
@@ -583,7 +655,8 @@ def compute_alpha_complex_arrays(centers, radii, cfg: PipelineConfig, stage_time
     ``radii`` (n,) as numpy arrays (ball i = row i).  Same result, no ``Ball``
     objects (building 10^6 of them costs seconds of Python)."""
     if cfg.mode == "naive":
-        raise NotImplementedError("mode='naive' (the exhaustive reference oracle) is not part of the B200 build")
+        raise UnsupportedMode("mode='naive' (the reference's exhaustive O(n^4) test oracle, oracle.py) is not part of "
+                              "the B200 build; use mode='grid'")
     eng = default_engine(device)
     n = int(np.asarray(radii).shape[0])
     v, e, t, q = eng.compute_host(centers, radii, cfg)
