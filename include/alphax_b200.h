@@ -158,6 +158,16 @@ int axb_potential_tets_from_triangles(axb_ctx *ctx, const int64_t *d_tri_rows, i
  * has power distance < size - eps_abs.  DEVICE buffer of uint8. */
 int axb_ac2_mask(axb_ctx *ctx, int what, uint8_t *d_mask);
 
+/* ---- alpha sweep with re-use ----------------------------------------------
+ * Ortho-sizes and AC2 outcomes do not depend on alpha, and the potential levels at alpha are subsets of those at
+ * a larger alpha.  axb_sweep_prepare: after axb_grid_build + axb_potential(0, n) at the LARGEST alpha of a sweep,
+ * evaluate size and AC2 once for every listed simplex.  axb_sweep_prune(alpha), alpha <= that largest value: the
+ * pruning stage for `alpha` from those arrays (the reference's own comparisons re-evaluated with alpha's reach and
+ * limit, pipeline.py:322-324, 341-344, 358, 415, 420, 478), followed by axb_canonicalize / axb_export as usual;
+ * may be called for any number of alphas.  Results are bit-identical to independent runs at each alpha. */
+int axb_sweep_prepare(axb_ctx *ctx);
+int axb_sweep_prune(axb_ctx *ctx, double alpha);
+
 /* _prune_levels (pipeline.py:482-527): AC2 at every ortho-centre, inheritance of faces */
 int axb_prune(axb_ctx *ctx);
 /* canonical sort + dedup (pipeline.py:611-614, _arrays.py:12-16); counts[d] = simplices of dimension d */

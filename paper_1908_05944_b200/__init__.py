@@ -36,12 +36,14 @@ from .pipeline import (
     complex_stats,
     compute_alpha_complex,
     compute_alpha_complex_arrays,
+    compute_alpha_sweep,
     default_engine,
 )
 from .io import (format_xyzr, format_xyzr_arrays, parse_xyzr, parse_xyzr_arrays, read_complex, stats_csv,
                  write_complex)
 from .stages import (CellKey, Grid, PotentialLevel, PotentialSets, ac2_mask, build_grid, cell_of, neighborhood,
                      potential_edges, potential_tets, potential_triangles, prune)
+from .validate import ValidationReport, validate_complex
 from . import synth
 
 __all__ = [
@@ -52,5 +54,5 @@ __all__ = [
     "compute_alpha_complex", "compute_alpha_complex_arrays", "default_engine", "simplex_compare", "synth",
     "CellKey", "Grid", "PotentialLevel", "PotentialSets", "build_grid", "potential_edges", "potential_triangles",
     "potential_tets", "prune", "read_complex", "stats_csv", "write_complex", "parse_xyzr", "parse_xyzr_arrays",
-    "format_xyzr", "format_xyzr_arrays", "UnsupportedMode", "ac2_mask", "cell_of", "neighborhood",
+    "format_xyzr", "format_xyzr_arrays", "UnsupportedMode", "ac2_mask", "cell_of", "neighborhood", "compute_alpha_sweep", "validate_complex", "ValidationReport",
 ]

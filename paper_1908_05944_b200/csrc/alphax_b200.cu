@@ -14,6 +14,7 @@
 #include "scan.cuh"
 #include "sparse.cuh"
 #include "stages.cuh"
+#include "sweep.cuh"
 #include "widen_pool.h"
 
 #include <math.h>
@@ -124,6 +125,11 @@ struct axb_ctx {
     bool defer_dup = false;               // one-call paths: the duplicate-centre check rides on the edge stage's host sync
     bool dup_pending = false;
     const int64_t *gidx = nullptr;        // slab mode: global ball index per local ball (ascending)
+    // alpha sweep (sweep.cuh)
+    bool sweep_ready = false, sweep_on = false;
+    bool lists_complete = false;          // the resident potential lists were built without cull mode
+    SweepArrays sw = {};
+    size_t mark_after_sweep = 0;
 };
 
 namespace {
@@ -433,6 +439,9 @@ PruneParams prune_params(axb_ctx *c) {
     P.ctr = c->ctr; P.biomolecule = c->prm.biomolecule;
     P.rank_lo = c->rank_lo; P.rank_hi = c->rank_hi;
     P.own_only = c->slab_mode ? 1 : 0;
+    P.sweep = c->sweep_on ? 1 : 0;
+    P.sw_pf = c->sw.pf; P.sw_tsize = c->sw.tsize; P.sw_tvw = c->sw.tvw; P.sw_qsize = c->sw.qsize; P.sw_qtsize = c->sw.qtsize;
+    P.sw_qe = c->sw.qe; P.sw_ac2e = c->sw.ac2e; P.sw_ac2t = c->sw.ac2t; P.sw_ac2q = c->sw.ac2q;
     P.k3_cap = c->k3_cap;
     // n_pt may still be the optimistic capacity (axb_compute); the potential triangles are ~0.8 per potential edge
     const unsigned warps = (unsigned)c->sm_count * (unsigned)PRUNE_GRID * (unsigned)PRUNE_WARPS;
@@ -675,6 +684,8 @@ int grid_build_common(axb_ctx *c, int64_t n, const double *d_xyz, const double *
     c->arena_needed = 0;
     c->slab_mode = slab != nullptr;
     c->gidx = d_gidx;
+    c->sweep_ready = false;
+    c->sweep_on = false;
     if (n <= 0) return fail(c, AXB_ERR_EMPTY, "at least one ball is required");
     if (n >= ((int64_t)1 << 31) - 1) return fail(c, AXB_ERR_BAD_ARG, "more than 2^31 - 2 balls are not supported");
     if (!d_xyz || !d_radii) return fail(c, AXB_ERR_BAD_ARG, "null input pointer");
@@ -880,6 +891,7 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
 // which the caller redoes the stage with optimistic = false (exact sizes, one sync)
 int run_tri_tet_lists(axb_ctx *c, bool optimistic = false, bool redo = false) {
     int st;
+    c->lists_complete = !c->cull;
     uint64_t pt_want = c->h->ctr.pair_bound + 32;           // every potential triangle is a partner pair
     uint64_t pq_want = c->h->ctr.pair_bound + 4096;         // first guess; re-run on overflow
     if (!redo && getenv("AXB_TEST_SMALL_PQ")) pq_want = 64;   // test hook: make the first guess fail
@@ -1203,6 +1215,7 @@ int finish_import(axb_ctx *c) {
     c->n_pq = c->h->ctr.n_pq;
     c->k3_cap = c->pq_cap;
     c->many_tets = false;
+    c->lists_complete = true;
     c->state = S_POTENTIAL;
     return AXB_OK;
 }
@@ -1282,6 +1295,62 @@ extern "C" int axb_ac2_mask(axb_ctx *c, int what, uint8_t *d_mask) {
     }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return AXB_OK;
+}
+
+// ---- alpha sweep with re-use (sweep.cuh) ----
+
+extern "C" int axb_sweep_prepare(axb_ctx *c) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (c->state < S_POTENTIAL || !c->lists_complete || c->slab_mode || c->rank_lo != 0 || c->rank_hi != (int)c->n)
+        return fail(c, AXB_ERR_STATE, "axb_sweep_prepare needs the complete potential levels of the whole input (axb_potential(0, n))");
+    c->state = S_POTENTIAL;
+    c->sweep_on = false;
+    c->sweep_ready = false;
+    const unsigned E = c->n_pe, T = c->n_pt, Q = c->n_pq;
+    // the lists end at pt_cap / pq_cap; everything the sweep keeps across alphas sits behind them
+    ARENA(c, c->sw.esize, double, std::max(E, 1u));
+    ARENA(c, c->sw.pf, unsigned char, std::max(E, 1u));
+    ARENA(c, c->sw.ac2e, unsigned char, std::max(E, 1u));
+    ARENA(c, c->sw.tsize, double, std::max(T, 1u));
+    ARENA(c, c->sw.tvw, int, std::max(T, 1u));
+    ARENA(c, c->sw.ac2t, unsigned char, std::max(T, 1u));
+    ARENA(c, c->sw.qsize, double, std::max(Q, 1u));
+    ARENA(c, c->sw.qtsize, double, std::max(Q, 1u));
+    ARENA(c, c->sw.qe, int4, std::max(Q, 1u));
+    ARENA(c, c->sw.ac2q, unsigned char, std::max(Q, 1u));
+    c->mark_after_sweep = c->arena_used;
+    CUDA_TRY(c, cudaMemsetAsync(&c->ctr->n_k3, 0, sizeof(unsigned int) * PRUNE_COUNTER_WORDS, c->stream));
+    PruneParams P = prune_params(c);
+    if (E) { k_sweep_prepare_edges<<<blocks_for(E, SWEEP_THREADS), SWEEP_THREADS, 0, c->stream>>>(P, E, c->sw); LAUNCH_CHECK(c); }
+    if (T) { k_sweep_prepare_tris<<<blocks_for(T, SWEEP_THREADS), SWEEP_THREADS, 0, c->stream>>>(P, T, c->sw); LAUNCH_CHECK(c); }
+    if (Q) { k_sweep_prepare_tets<<<blocks_for(Q, SWEEP_THREADS), SWEEP_THREADS, 0, c->stream>>>(P, Q, c->sw); LAUNCH_CHECK(c); }
+    int st = fetch_counters(c);
+    if (st != AXB_OK) return st;
+    if ((st = check_run_flags(c)) != AXB_OK) return st;
+    c->sweep_ready = true;
+    return AXB_OK;
+}
+
+extern "C" int axb_sweep_prune(axb_ctx *c, double alpha) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (!c->sweep_ready || c->state < S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_sweep_prune before axb_sweep_prepare");
+    if (!(alpha <= c->prm.alpha)) return fail(c, AXB_ERR_BAD_ARG, "the sweep was prepared for alpha <= %.17g", c->prm.alpha);
+    if (c->prm.biomolecule && alpha < 0.0) return fail(c, AXB_ERR_BAD_ARG, "biomolecule mode requires alpha >= 0");
+    c->state = S_POTENTIAL;
+    c->arena_used = c->mark_after_sweep;
+    c->tol.lim_a = alpha + c->prm.eps_abs;
+    for (int i = AXB_ST_PRUNE_TETS; i < AXB_ST_COUNT + 2; ++i) c->ev_set[i] = false;
+    int st = mark_event(c, AXB_ST_PRUNE_TETS);
+    if (st != AXB_OK) return st;
+    if (c->n_pe) {
+        k_sweep_edge_flags<<<blocks_for(c->n_pe, 256), 256, 0, c->stream>>>(c->n_pe, c->atoms, c->pe_u, c->pe_v, c->sw.esize, alpha,
+                                                                            c->prm.eps_abs, c->sw.pf);
+        LAUNCH_CHECK(c);
+    }
+    c->sweep_on = true;
+    st = run_prune(c);
+    c->sweep_on = false;
+    return st;
 }
 
 extern "C" int axb_prune(axb_ctx *c) {

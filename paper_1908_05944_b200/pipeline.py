@@ -519,6 +519,27 @@ class Engine:
         self._collect_stage_ms()
         return outs
 
+    # -- alpha sweep with re-use (csrc/sweep.cuh)
+    def sweep_device(self, centers, radii, alphas, cfg: PipelineConfig):
+        """The complexes of ONE ball set at several alphas: grid, potential levels, ortho solves and every AC2 walk
+        are done once at max(alphas); each alpha then costs one flag pass over the listed edges, the inheritance marks
+        and the canonical lists.  CUDA tensors in, a list (one entry per alpha, in the given order) of four CUDA int64
+        tensors out -- bit-identical to independent runs.  ``cfg.alpha`` is ignored."""
+        from dataclasses import replace
+
+        alphas = [float(a) for a in alphas]
+        if not alphas:
+            return []
+        top = replace(cfg, alpha=max(alphas))
+        self.stage_grid(centers, radii, top)
+        self.stage_potential()
+        self._stage_call(self.lib.axb_sweep_prepare)
+        out = []
+        for a in alphas:
+            self._stage_call(self.lib.axb_sweep_prune, C.c_double(a))
+            out.append(self.stage_export(self.stage_canonicalize()))
+        return out
+
     # -- multi-GPU building blocks (sharding.py)
     def compute_slab_device(self, centers, radii, global_index, cfg: PipelineConfig, plan, slab, raise_errors: bool = True):
         """One z-slab of a global grid: CUDA tensors of the loaded balls (ascending global index) in,
@@ -662,6 +683,40 @@ def compute_alpha_complex_arrays(centers, radii, cfg: PipelineConfig, stage_time
     v, e, t, q = eng.compute_host(centers, radii, cfg)
     _accumulate_stage_times(stage_times, eng.last_stage_ms)
     return AlphaComplex(vertices=v, edges=e, triangles=t, tets=q, alpha=cfg.alpha, ball_count=n)
+
+
+def compute_alpha_sweep(centers, radii, alphas, cfg: PipelineConfig, device: int | None = None) -> list:
+    """``[compute_alpha_complex_arrays(centers, radii, replace(cfg, alpha=a)) for a in alphas]`` with re-use: one
+    upload, one grid, one potential stage, one evaluation of every ortho-size and AC2 outcome at max(alphas) (they do
+    not depend on alpha), then per alpha only the flags, the inheritance marks and the canonical lists
+    (``Engine.sweep_device``).  The complexes are bit-identical to independent runs; if the largest alpha meets a
+    singular solve (which a smaller alpha may never evaluate) the sweep falls back to independent runs, so the
+    exceptions are the reference's as well."""
+    from dataclasses import replace
+
+    import torch
+
+    if cfg.mode == "naive":
+        raise UnsupportedMode("mode='naive' is not part of the B200 build; use mode='grid'")
+    alphas = [float(a) for a in alphas]
+    for a in alphas:
+        replace(cfg, alpha=a)                        # the reference's own argument checks, per alpha
+    eng = default_engine(device)
+    centers = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 3)
+    radii = np.ascontiguousarray(radii, dtype=np.float64).reshape(-1)
+    n = int(radii.shape[0])
+    if n == 0:
+        raise EmptyInput("at least one ball is required")
+    dev = f"cuda:{eng.device}"
+    try:
+        levels = eng.sweep_device(torch.as_tensor(centers, device=dev), torch.as_tensor(radii, device=dev), alphas, cfg)
+    except DegenerateSimplex:
+        return [compute_alpha_complex_arrays(centers, radii, replace(cfg, alpha=a), device=device) for a in alphas]
+    out = []
+    for a, (v, e, t, q) in zip(alphas, levels):
+        out.append(AlphaComplex(vertices=v.cpu().numpy(), edges=e.cpu().numpy(), triangles=t.cpu().numpy(),
+                                tets=q.cpu().numpy(), alpha=a, ball_count=n))
+    return out
 
 
 def compute_alpha_complex(balls: Sequence[Ball], cfg: PipelineConfig, stage_times: dict | None = None) -> AlphaComplex:

@@ -174,3 +174,47 @@ def test_chunk_ownership_partitions_potentials():
         stacked = np.concatenate(parts[d], axis=0)
         assert stacked.shape[0] == len(level)                     # disjoint: no duplicates lost
         assert np.array_equal(np.unique(stacked, axis=0), level.simplices)
+
+
+def test_alpha_sweep_with_reuse_equals_independent_runs():
+    """one grid / potential stage / AC2 evaluation at the largest alpha serves every alpha of the
+    sweep; each complex must be bit-identical to an independent run (and to the oracle)."""
+    cases = [(synth.jittered_lattice(30_000, 21), [0.0, 1.4, 0.3, 0.7, -0.4], False),
+             (synth.adversarial_density(20_000, 4, shuffle=True), [0.9, 0.0, 0.45], False),
+             (synth.random_globule(2500, 8, 0.5, (0.2, 2.4), 0.12), [1.0, -1.5, 0.0, 0.2, -0.05], False),
+             (synth.jittered_lattice(8_000, 22), [0.0, 1.1], True)]
+    for (c, r), alphas, bio in cases:
+        cfg = ax.PipelineConfig(alpha=0.0, biomolecule_mode=bio, tolerance=ax.TolerancePolicy(1e-9, 1e-300))
+        sweep = ax.compute_alpha_sweep(c, r, alphas, cfg)
+        assert [k.alpha for k in sweep] == alphas
+        for a, k in zip(alphas, sweep):
+            from dataclasses import replace
+
+            alone = ax.compute_alpha_complex_arrays(c, r, replace(cfg, alpha=a))
+            assert k == alone, (a, k.counts(), alone.counts())
+            ref = oracle.compute(c, r, a, eps_singular=1e-300, biomolecule=bio, threads=os.cpu_count(), chunk=2000)
+            assert ref.status == oracle.OK
+            for got, want in zip((k.vertices, k.edges, k.triangles, k.tets), (ref.vertices, ref.edges, ref.triangles, ref.tets)):
+                assert np.array_equal(got, want), a
+        for lo, hi in zip(sorted(alphas), sorted(alphas)[1:]):
+            assert sweep[alphas.index(lo)].is_subcomplex_of(sweep[alphas.index(hi)])
+    # a singular solve at the largest alpha: the sweep falls back to independent runs, i.e. the reference's behaviour
+    g = np.stack(np.meshgrid(np.arange(6.0), np.arange(6.0), np.arange(6.0), indexing="ij"), -1).reshape(-1, 3) * 1.5
+    with pytest.raises(ax.DegenerateSimplex):
+        ax.compute_alpha_sweep(g, np.full(len(g), 1.2), [0.0, 1.0], ax.PipelineConfig(alpha=0.0))
+
+
+def test_validate_on_the_gpu_path(stage_cases):
+    """reference cli.py:134-180: symmetric difference against a partner complex, closure, monotonicity alpha -> alpha+1."""
+    meta, a = stage_cases["globule_a1"]
+    cfg = ax.PipelineConfig(alpha=meta["alpha"], tolerance=ax.TolerancePolicy(1e-9, meta["eps_singular"]))
+    want = ax.AlphaComplex(vertices=a["k_full_0"].reshape(-1), edges=a["k_full_1"], triangles=a["k_full_2"], tets=a["k_full_3"],
+                           alpha=meta["alpha"], ball_count=meta["n"])
+    rep = ax.validate_complex(a["centers"], a["radii"], cfg, expected=want)
+    assert rep.ok and rep.mismatches == (0, 0, 0, 0) and list(rep.counts) == meta["counts_full"]
+    assert "closure: ok" in rep.lines()[2] and "monotonicity (alpha -> alpha+1): ok" in rep.lines()[2]
+    broken = ax.AlphaComplex(vertices=want.vertices, edges=want.edges[:-3], triangles=want.triangles, tets=want.tets,
+                             alpha=want.alpha, ball_count=want.ball_count)
+    rep = ax.validate_complex(a["centers"], a["radii"], cfg, expected=broken)
+    assert not rep.ok and rep.mismatches[1] == 3 and not rep.closed
+    assert ax.validate_complex(a["centers"], a["radii"], ax.PipelineConfig(alpha=0.4)).ok
