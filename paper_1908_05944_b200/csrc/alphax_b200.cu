@@ -6,6 +6,7 @@
 
 #include "canon.cuh"
 #include "common.cuh"
+#include "edges.cuh"
 #include "estimate.cuh"
 #include "estimate3.cuh"
 #include "grid.cuh"
@@ -451,10 +452,13 @@ PruneParams prune_params(axb_ctx *c) {
 }
 
 int launch_edges(axb_ctx *c, const EstParams &P, int lo, int hi) {
-    const unsigned nblocks = (unsigned)std::max(1, (hi - lo + E2_GB * EST_WARPS - 1) / (E2_GB * EST_WARPS));
-    const size_t smem = sizeof(E2Warp) * EST_WARPS;
+    const unsigned nblocks = (unsigned)std::max(1, (hi - lo + 32 * EL_WARPS - 1) / (32 * EL_WARPS));
+    const size_t smem = sizeof(ELWarp) * EL_WARPS;
     CUDA_TRY(c, cudaFuncSetAttribute(k_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_edges<<<std::min(nblocks, (unsigned)c->sm_count * (unsigned)E2_MINB), EST_WARPS * 32, smem, c->stream>>>(P, lo, hi);
+    const unsigned resident = (unsigned)c->sm_count * (unsigned)EL_MINB;
+    const int dyn = nblocks > resident ? 1 : 0;
+    if (dyn) CUDA_TRY(c, cudaMemsetAsync(&c->ctr->work_next[0], 0, sizeof(unsigned int), c->stream));     // tile claims
+    k_edges<<<std::min(nblocks, resident), EL_WARPS * 32, smem, c->stream>>>(P, lo, hi, dyn);
     LAUNCH_CHECK(c);
     return AXB_OK;
 }

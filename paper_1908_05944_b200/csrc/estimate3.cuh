@@ -53,15 +53,34 @@ constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved 
 #define T3H_MINB 6
 #endif
 
+// light tile shape
+#ifndef T3L_SCAP
+#define T3L_SCAP 128
+#endif
+#ifndef T3L_TCAP
+#define T3L_TCAP 224
+#endif
+#ifndef T3L_MINB
+#define T3L_MINB 4
+#endif
+#ifndef T3L_PTAB
+#define T3L_PTAB 1024
+#endif
+// cull mode bit 1 (triangles flagged as dominated by a partner, AXB_CULL=2|3) needs a third bit matrix per warp; it
+// never paid, so it is compiled out unless asked for
+#ifndef T3_CULL_TRIS
+#define T3_CULL_TRIS 0
+#endif
+
 template <int W, int SHAPE>
 struct T3Cfg {
     static constexpr int GENS = (W == 1 && SHAPE == T3_HEAVY) ? T3H_GENS : 16;                      // generators per warp tile (<= 16)
-    static constexpr int SCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_SCAP : 128) : 256;   // partner slots per sub-pass (>= 64 * W)
-    static constexpr int TCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_TCAP : 224) : 512;  // triangles per round
-    static constexpr int MINB = W == 1 ? (SHAPE == T3_HEAVY ? T3H_MINB : 4) : 1;        // resident blocks per SM the registers must allow
+    static constexpr int SCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_SCAP : T3L_SCAP) : 256;   // partner slots per sub-pass (>= 64 * W)
+    static constexpr int TCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_TCAP : T3L_TCAP) : 512;  // triangles per round
+    static constexpr int MINB = W == 1 ? (SHAPE == T3_HEAVY ? T3H_MINB : T3L_MINB) : 1;        // resident blocks per SM the registers must allow
     static constexpr int NA = SCAP + GENS;              // atom index space: partner slots, then the tile's generators
     static constexpr bool FLAT = W == 1 && SHAPE == T3_LIGHT;   // flattened pair enumeration (pays while degrees are small)
-    static constexpr int PTAB = FLAT ? 8 * SCAP : 32;   // partner pairs of a sub-pass covered by the stamped pair table
+    static constexpr int PTAB = FLAT ? T3L_PTAB : 32;   // partner pairs of a sub-pass covered by the stamped pair table
 };
 
 template <int W, int SHAPE>
@@ -71,7 +90,9 @@ struct T3Warp {
     double sreach[C::SCAP];
     unsigned long long M[C::SCAP * W];
     unsigned long long T[C::SCAP * W];
-    unsigned long long D[C::SCAP * W];         // potential triangles already known to be dominated (cull mode)
+#if T3_CULL_TRIS
+    unsigned long long D[C::SCAP * W];         // potential triangles already known to be dominated (cull mode bit 1)
+#endif
     int aorig[C::NA];
     int srank[C::SCAP];
     int rowpre[C::SCAP + 1];
@@ -261,7 +282,12 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                     S.sgen[s] = (unsigned char)g;
                     S.sli[s] = (unsigned char)li;
 #pragma unroll
-                    for (int w = 0; w < W; ++w) { S.M[s * W + w] = 0ull; S.T[s * W + w] = 0ull; S.D[s * W + w] = 0ull; }
+                    for (int w = 0; w < W; ++w) {
+                        S.M[s * W + w] = 0ull; S.T[s * W + w] = 0ull;
+#if T3_CULL_TRIS
+                        S.D[s * W + w] = 0ull;
+#endif
+                    }
                 }
                 __syncwarp();
                 // ---- B: partner pairs.  Lane = partner slot i; round r pairs it with slot i + r of the same
@@ -290,11 +316,13 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                                         record_singular(P, make_err_key(ST_TRI, t, q), S.aorig[SCAP + g], S.aorig[si], S.aorig[sj], -1, 3);
                                     if (e3.size <= P.tol.lim_a) {                                        // pipeline.py:420
                                         set_bit(&S.T[si * W], j);
+#if T3_CULL_TRIS
                                         if (P.cull & 2) {
                                             const int sb = S.sp[g] - base;
                                             if (dominated_by_partner3(S, sb, sb + d, si, sj, -1, e3.cx, e3.cy, e3.cz, e3.size - P.tol.eps_abs))
                                                 set_bit(&S.D[si * W], j);
                                         }
+#endif
                                     }
                                 }
                             }
@@ -417,7 +445,11 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                                 }
                                 S.u.t.cpre[x] = cnt;
                                 const unsigned pos = pt_base + (unsigned)(tc0 + x);
+#if T3_CULL_TRIS
                                 const int dom = (int)((S.D[srow * W + (j >> 6)] >> (j & 63)) & 1ull);
+#else
+                                const int dom = 0;
+#endif
                                 if (pos < P.pt_cap)
                                     P.pt[pos] = make_int4(t0 + g, S.srank[srow], S.srank[sj],
                                                           (int)S.sli[srow] | (j << 16) | (dom << 31));

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Iterator, Sequence
 
@@ -682,7 +683,13 @@ def compute_alpha_complex_arrays(centers, radii, cfg: PipelineConfig, stage_time
     n = int(np.asarray(radii).shape[0])
     v, e, t, q = eng.compute_host(centers, radii, cfg)
     _accumulate_stage_times(stage_times, eng.last_stage_ms)
-    return AlphaComplex(vertices=v, edges=e, triangles=t, tets=q, alpha=cfg.alpha, ball_count=n)
+    k = AlphaComplex(vertices=v, edges=e, triangles=t, tets=q, alpha=cfg.alpha, ball_count=n)
+    # The reference re-checks closure on every result (pipeline.py:623-624).  Here closure holds by construction --
+    # a kept simplex marks all its faces on the device, and the emit kernels flag anything inconsistent -- so the
+    # host-side re-check (seconds of numpy per million balls) is a debug switch: AXB_CHECK_CLOSURE=1.
+    if os.environ.get("AXB_CHECK_CLOSURE") == "1" and not closure_ok(k):
+        raise AlphaxError("internal error: output violates closure")
+    return k
 
 
 def compute_alpha_sweep(centers, radii, alphas, cfg: PipelineConfig, device: int | None = None) -> list:
