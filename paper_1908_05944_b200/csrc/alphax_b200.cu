@@ -118,7 +118,7 @@ struct axb_ctx {
     uint32_t n_pe = 0, n_pt = 0, n_pq = 0;
     int64_t counts[4] = {0, 0, 0, 0};
     int64_t host_cap[4] = {0, 0, 0, 0};
-    size_t mark_after_grid = 0, mark_after_edges = 0;
+    size_t mark_after_grid = 0, mark_after_edges = 0, arena_after_prune = 0;
     int cull_mask = 1;                    // bit 0: tets, bit 1: triangles (A/B switch AXB_CULL=0..3)
     bool cull = false;                    // one-call path: k_tri_tet3 settles partner-dominated simplices itself
     bool slab_mode = false;               // grid geometry fixed by the caller (one z-slab of a global grid)
@@ -127,6 +127,8 @@ struct axb_ctx {
     bool dup_pending = false;
     const int64_t *gidx = nullptr;        // slab mode: global ball index per local ball (ascending)
     // alpha sweep (sweep.cuh)
+    cudaEvent_t side_go = nullptr, side_done = nullptr;     // hand-over to / from the second stream (early memset)
+    bool prune_prealloc = false, side_pending = false;
     bool sweep_ready = false, sweep_on = false;
     bool lists_complete = false;          // the resident potential lists were built without cull mode
     SweepArrays sw = {};
@@ -236,6 +238,16 @@ int device_scan4(axb_ctx *c, const uint32_t *const in[4], size_t n, uint32_t *co
     k_scan4_apply<<<dim3((unsigned)ntiles, 4), SCAN_THREADS, 0, c->stream>>>(a, n);
     LAUNCH_CHECK(c);
     return AXB_OK;
+}
+
+__global__ void k_publish_state(const uint32_t *__restrict__ t0, const uint32_t *__restrict__ t1, const uint32_t *__restrict__ t2,
+                                const uint32_t *__restrict__ t3, const Counters *__restrict__ ctr, uint32_t *h_totals,
+                                Counters *h_ctr) {
+    const unsigned *src = reinterpret_cast<const unsigned *>(ctr);
+    unsigned *dst = reinterpret_cast<unsigned *>(h_ctr);
+    for (unsigned w = threadIdx.x; w < sizeof(Counters) / sizeof(unsigned); w += blockDim.x) dst[w] = src[w];
+    if (threadIdx.x == 0) { h_totals[0] = *t0; h_totals[1] = *t1; h_totals[2] = *t2; h_totals[3] = *t3; }
+    __threadfence_system();
 }
 
 int fetch_counters(axb_ctx *c) {
@@ -579,6 +591,8 @@ extern "C" int axb_ctx_create(axb_ctx **out, int device) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
     for (int i = 0; e == cudaSuccess && i < 4; ++i) e = cudaEventCreateWithFlags(&c->dim_ready[i], cudaEventDisableTiming);
     for (int i = 0; e == cudaSuccess && i < 4; ++i) e = cudaEventCreateWithFlags(&c->dim_count[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->side_go, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->side_done, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         fprintf(stderr, "axb_ctx_create: %s\n", cudaGetErrorString(e));
         delete c;
@@ -597,6 +611,8 @@ extern "C" void axb_ctx_destroy(axb_ctx *c) {
         if (c->dim_ready[i]) cudaEventDestroy(c->dim_ready[i]);
         if (c->dim_count[i]) cudaEventDestroy(c->dim_count[i]);
     }
+    if (c->side_go) cudaEventDestroy(c->side_go);
+    if (c->side_done) cudaEventDestroy(c->side_done);
     delete c->pool;
     for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -690,6 +706,8 @@ int grid_build_common(axb_ctx *c, int64_t n, const double *d_xyz, const double *
     c->gidx = d_gidx;
     c->sweep_ready = false;
     c->sweep_on = false;
+    c->prune_prealloc = false;
+    c->side_pending = false;
     if (n <= 0) return fail(c, AXB_ERR_EMPTY, "at least one ball is required");
     if (n >= ((int64_t)1 << 31) - 1) return fail(c, AXB_ERR_BAD_ARG, "more than 2^31 - 2 balls are not supported");
     if (!d_xyz || !d_radii) return fail(c, AXB_ERR_BAD_ARG, "null input pointer");
@@ -712,7 +730,7 @@ int grid_build_common(axb_ctx *c, int64_t n, const double *d_xyz, const double *
     ARENA(c, c->ctr, Counters, 1);
     ARENA(c, c->errs, ErrRecord, ERR_CAP);
     ARENA(c, c->dups, int2, DUP_CAP);
-    const unsigned nb = std::max(1u, std::min(blocks_for((size_t)n, BOUNDS_THREADS * 4), (unsigned)c->sm_count * 2u));
+    const unsigned nb = std::max(1u, std::min(blocks_for((size_t)n, BOUNDS_THREADS * 4), (unsigned)c->sm_count * 8u));
     BoundsPartial *partials, *bres;
     unsigned int *done;
     ARENA(c, partials, BoundsPartial, nb);
@@ -723,9 +741,10 @@ int grid_build_common(axb_ctx *c, int64_t n, const double *d_xyz, const double *
     c->h->ctr.first_bad = 0xffffffffu;
     CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(c, cudaMemsetAsync(done, 0, sizeof(unsigned int), c->stream));
-    k_bounds<<<nb, BOUNDS_THREADS, 0, c->stream>>>(d_xyz, d_radii, (int)n, partials, done, bres);
+    // the folded result goes straight into mapped host memory (no copy operation between the kernel and the sync)
+    (void)bres;
+    k_bounds<<<nb, BOUNDS_THREADS, 0, c->stream>>>(d_xyz, d_radii, (int)n, partials, done, &c->h_dev->bounds);
     LAUNCH_CHECK(c);
-    CUDA_TRY(c, cudaMemcpyAsync(&c->h->bounds, bres, sizeof(BoundsPartial), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     const BoundsPartial &b = c->h->bounds;
     c->tol.r2max = b.rmax * b.rmax;
@@ -889,6 +908,8 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
     return AXB_OK;
 }
 
+int alloc_prune_arrays(axb_ctx *c, bool early);
+
 // potential triangles + tets into global lists (the standalone stage path); synchronises
 // optimistic = true (axb_compute): no host round trip after the kernel; the list sizes are a guess that almost
 // always holds, the pruning kernels check it on the device (lists_overflowed) and run_canonicalize reports it, upon
@@ -916,6 +937,14 @@ int run_tri_tet_lists(axb_ctx *c, bool optimistic = false, bool redo = false) {
             c->h->ctr.n_pt = 0; c->h->ctr.n_pq = 0; c->h->ctr.overflow = 0;
             c->h->ctr.err_key = ~0ull; c->h->ctr.err_count = 0;
             CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
+        }
+        if (optimistic && attempt == 0) {
+            // the pruning state sits behind the lists; its size only needs the edge count and the list capacities
+            c->k3_cap = c->pq_cap;
+            const size_t keep = c->arena_used;
+            if ((st = alloc_prune_arrays(c, /*early=*/true)) != AXB_OK) return st;
+            c->arena_after_prune = c->arena_used;
+            c->arena_used = keep;
         }
         st = launch_tri_tet(c, 0);
         if (st != AXB_OK) return st;
@@ -952,7 +981,10 @@ int run_potential(axb_ctx *c, int64_t lo, int64_t hi, bool optimistic = false) {
 }
 
 // kept-simplex state of the pruning stage (prune.cuh), zeroed
-int alloc_prune_arrays(axb_ctx *c) {
+// early = true (axb_compute): called BEFORE k_tri_tet3 is queued; the big memset then runs on the second stream beside that
+// kernel (which uses a few per cent of the DRAM bandwidth) instead of in front of the pruning kernels
+int alloc_prune_arrays(axb_ctx *c, bool early) {
+    if (c->prune_prealloc) { c->prune_prealloc = false; return AXB_OK; }      // done early for this run
     const int n = (int)c->n;
     const size_t rows = (size_t)std::max<uint32_t>(c->n_pe, 1);
     ARENA(c, c->k3, int4, std::max<uint32_t>(c->k3_cap, 1));
@@ -966,7 +998,17 @@ int alloc_prune_arrays(axb_ctx *c) {
     ARENA(c, c->cnt2, uint32_t, (size_t)n + 1);
     ARENA(c, c->cnt3, uint32_t, (size_t)n + 1);
     ARENA(c, c->vkeep, uint32_t, (size_t)n + 1);
-    CUDA_TRY(c, cudaMemsetAsync(c->arena + zero_from, 0, c->arena_used - zero_from, c->stream));
+    if (early) {
+        // everything queued so far (previous users of this part of the arena included) comes first
+        CUDA_TRY(c, cudaEventRecord(c->side_go, c->stream));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->side_go, 0));
+        CUDA_TRY(c, cudaMemsetAsync(c->arena + zero_from, 0, c->arena_used - zero_from, c->copy_stream));
+        CUDA_TRY(c, cudaEventRecord(c->side_done, c->copy_stream));
+        c->prune_prealloc = true;
+        c->side_pending = true;
+    } else {
+        CUDA_TRY(c, cudaMemsetAsync(c->arena + zero_from, 0, c->arena_used - zero_from, c->stream));
+    }
     CUDA_TRY(c, cudaMemsetAsync(&c->ctr->n_k3, 0, sizeof(unsigned int) * PRUNE_COUNTER_WORDS, c->stream));
     return AXB_OK;
 }
@@ -990,8 +1032,13 @@ int run_prune_lower(axb_ctx *c) {
 
 int run_prune(axb_ctx *c) {
     if (c->state < S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_prune before axb_potential");
-    int st = alloc_prune_arrays(c);
+    if (c->prune_prealloc) c->arena_used = c->arena_after_prune;
+    int st = alloc_prune_arrays(c, false);
     if (st != AXB_OK) return st;
+    if (c->side_pending) {
+        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->side_done, 0));
+        c->side_pending = false;
+    }
     PruneParams P = prune_params(c);
     // few tets per thread: static grid-stride; many (large alpha, dense cores): dynamic 64-tet claims
     if ((uint64_t)c->n_pq > (uint64_t)c->n + c->n / 2)
@@ -1016,11 +1063,12 @@ int run_canonicalize(axb_ctx *c, int64_t counts[4]) {
         uint32_t *const out[4] = {c->off1, c->off2, c->off3, c->voff};
         if ((st = device_scan4(c, in, n, out)) != AXB_OK) return st;
     }
-    CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[0], c->voff + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[1], c->off1 + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[2], c->off2 + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[3], c->off3 + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
-    if ((st = fetch_counters(c)) != AXB_OK) return st;
+    // the four totals and the counter block reach the host as zero-copy stores of ONE small kernel (five copy
+    // operations cost ~10 us of stream time before the sync)
+    k_publish_state<<<1, 32, 0, c->stream>>>(c->voff + n, c->off1 + n, c->off2 + n, c->off3 + n, c->ctr, c->h_dev->totals,
+                                             &c->h_dev->ctr);
+    LAUNCH_CHECK(c);
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     // deferred checks of the optimistic potential stage
     if (c->h->ctr.n_pq > c->pq_cap || c->h->ctr.n_pt > c->pt_cap || c->h->ctr.n_k3 > c->k3_cap)
         return AXB_ERR_ARENA + 1000;                       // sentinel: a guessed buffer was too small, caller re-runs
@@ -1614,7 +1662,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if (!c || !counts) return AXB_ERR_BAD_ARG;
     if (c->state != S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_compute_host_finish needs axb_compute_host_begin first");
     const size_t n = (size_t)c->n;
-    int st = alloc_prune_arrays(c);
+    int st = alloc_prune_arrays(c, false);
     if (st != AXB_OK) return st;
     int64_t *h[4] = {h_v, h_e, h_t, h_q};
     // What crosses PCIe per row: int32 values, widened by the host threads; nothing at all for the vertices

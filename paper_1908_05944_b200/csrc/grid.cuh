@@ -41,13 +41,24 @@ __global__ void __launch_bounds__(BOUNDS_THREADS) k_bounds(const double *__restr
                                                            BoundsPartial *__restrict__ result) {
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY}, rmax = -INFINITY;
     unsigned int bad = 0xffffffffu;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        double x = xyz[3 * (size_t)i], y = xyz[3 * (size_t)i + 1], z = xyz[3 * (size_t)i + 2], r = radii[i];
-        if (!(isfinite(x) && isfinite(y) && isfinite(z) && isfinite(r))) bad = min(bad, (unsigned)i);
-        lo[0] = fmin(lo[0], x); hi[0] = fmax(hi[0], x);
-        lo[1] = fmin(lo[1], y); hi[1] = fmax(hi[1], y);
-        lo[2] = fmin(lo[2], z); hi[2] = fmax(hi[2], z);
-        rmax = fmax(rmax, r);
+    // four balls per thread and step, their 16 loads issued before the first comparison
+    const int stride = gridDim.x * blockDim.x;
+    for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+        double x[4], y[4], z[4], r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = min(i0 + u * stride, n - 1);        // clamped: a repeated ball changes nothing
+            x[u] = xyz[3 * (size_t)i]; y[u] = xyz[3 * (size_t)i + 1]; z[u] = xyz[3 * (size_t)i + 2]; r[u] = radii[i];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = min(i0 + u * stride, n - 1);
+            if (!(isfinite(x[u]) && isfinite(y[u]) && isfinite(z[u]) && isfinite(r[u]))) bad = min(bad, (unsigned)i);
+            lo[0] = fmin(lo[0], x[u]); hi[0] = fmax(hi[0], x[u]);
+            lo[1] = fmin(lo[1], y[u]); hi[1] = fmax(hi[1], y[u]);
+            lo[2] = fmin(lo[2], z[u]); hi[2] = fmax(hi[2], z[u]);
+            rmax = fmax(rmax, r[u]);
+        }
     }
     __shared__ BoundsPartial s_part[BOUNDS_THREADS / 32];
     __shared__ bool s_last;

@@ -378,8 +378,14 @@ class Engine:
                 self.handle, n, centers.data_ptr(), radii.data_ptr(), C.byref(prm), counts))
             if st != N.OK:
                 self._raise(st, cfg, centers, radii)
-            outs = [torch.empty((int(counts[d]),) if d == 0 else (int(counts[d]), d + 1), dtype=torch.int64, device=dev)
-                    for d in range(4)]
+            # one allocation for the four lists (the GPU idles while the host allocates: every call counts)
+            sizes = [int(counts[d]) * (d + 1) for d in range(4)]
+            flat = torch.empty(sum(sizes), dtype=torch.int64, device=dev)
+            outs, at = [], 0
+            for d in range(4):
+                part = flat[at:at + sizes[d]]
+                outs.append(part if d == 0 else part.view(int(counts[d]), d + 1))
+                at += sizes[d]
             st = self.lib.axb_export(self.handle, *(o.data_ptr() if o.numel() else None for o in outs))
             if st == N.OK:
                 st = self.lib.axb_sync_check(self.handle)
