@@ -41,7 +41,7 @@ typedef enum axb_status {
     AXB_ERR_INTERNAL = 12
 } axb_status;
 
-#define AXB_MAX_PARTNERS 256
+#define AXB_MAX_PARTNERS 1023
 
 typedef struct axb_ctx axb_ctx;
 
@@ -102,8 +102,8 @@ const char *axb_last_message(const axb_ctx *ctx);
 int axb_last_error(const axb_ctx *ctx, int *status, int64_t verts[4], int *nverts);
 /* What ranks of a sharded run need to agree on ONE error (the one the reference would raise for the whole
  * input, pipeline.py:238-244 / 357, 414, 419, 477).  AXB_ERR_DEGENERATE: *key = (stage << 60 | generator rank in
- * this context's grid order << 24 | ordinal); the smallest key over all ranks -- after adding the slab's first
- * global grid rank << 24 -- is the solve the reference meets first.  AXB_ERR_DUPLICATE: xyz = the shared centre
+ * this context's grid order << 29 | ordinal); the smallest key over all ranks -- after adding the slab's first
+ * global grid rank << 29 -- is the solve the reference meets first.  AXB_ERR_DUPLICATE: xyz = the shared centre
  * (the reference reports the smallest one in (x, y, z) order).  Ball indices from axb_last_error are GLOBAL
  * (mapped through d_global_index) when the context holds a slab. */
 int axb_last_error_detail(const axb_ctx *ctx, uint64_t *key, double xyz[3]);

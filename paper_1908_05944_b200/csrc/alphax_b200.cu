@@ -10,6 +10,7 @@
 #include "estimate.cuh"
 #include "estimate3.cuh"
 #include "grid.cuh"
+#include "heavy.cuh"
 #include "predicates.cuh"
 #include "prune.cuh"
 #include "scan.cuh"
@@ -107,6 +108,9 @@ struct axb_ctx {
     int4 *pt = nullptr, *pq_r = nullptr;
     int *pq_l = nullptr;
     int W = 1;
+    int *heavy_list = nullptr;              // generators with more than 256 partners (heavy.cuh), when there are any
+    unsigned long long *heavy_scratch = nullptr;
+    unsigned heavy_blocks = 0;
     unsigned long long *trimask = nullptr;
     unsigned int *eflag = nullptr;
     unsigned char *vflag = nullptr;
@@ -487,7 +491,7 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
                               // alpha 0.6 = 0.99 vs 1.09 ms, heavy from alpha 0.8 = 1.32 vs 1.36 ms; tools/gpu_alpha_scan.py)
 #endif
     {   // warp-autonomous tiles (estimate3.cuh); the tile shape follows the work per generator
-        CUDA_TRY(c, cudaMemsetAsync(&c->ctr->tile_next, 0, sizeof(unsigned int), c->stream));
+        CUDA_TRY(c, cudaMemsetAsync(&c->ctr->tile_next, 0, 2 * sizeof(unsigned int), c->stream));     // tile_next, n_heavy
         auto launch = [&](auto kernel, size_t warp_bytes, int gens, int minb) -> int {
             const size_t smem = warp_bytes * T3_WARPS;
             const unsigned nblocks = (unsigned)std::max(1, (ngen + gens * T3_WARPS - 1) / (gens * T3_WARPS));
@@ -503,6 +507,13 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
         else st = launch(k_tri_tet3<1, T3_LIGHT>, sizeof(T3Warp<1, T3_LIGHT>), T3Cfg<1, T3_LIGHT>::GENS, T3Cfg<1, T3_LIGHT>::MINB);
         if (st != AXB_OK) return st;
         LAUNCH_CHECK(c);
+        if (c->heavy_list) {        // some generator has more partners than a tile holds: those go through heavy.cuh
+            k_list_heavy<<<blocks_for((size_t)std::max(ngen, 1), 256), 256, 0, c->stream>>>(c->gen_lo, c->rank_hi, c->deg, c->heavy_list,
+                                                                                          &c->ctr->n_heavy);
+            LAUNCH_CHECK(c);
+            k_tri_tet_heavy<<<c->heavy_blocks, HEAVY_THREADS, 0, c->stream>>>(P, c->heavy_list, &c->ctr->n_heavy, c->W, c->heavy_scratch);
+            LAUNCH_CHECK(c);
+        }
         return AXB_OK;
     }
 }
@@ -845,6 +856,21 @@ extern "C" int axb_grid_export(axb_ctx *c, int64_t *d_order, int64_t *d_rank, in
 
 namespace {
 
+// 64-bit words per row of the kept-triangle mask: one up to 64 partners per generator, four up to 256 (the two
+// shapes k_tri_tet3 is built for), then as many as the longest partner list needs
+int trimask_words(unsigned max_deg) { return max_deg <= 64 ? 1 : (max_deg <= 256 ? 4 : (int)((max_deg + 63) / 64)); }
+
+// list + bit-matrix scratch of the heavy-generator kernel (heavy.cuh), only when some generator needs it
+int alloc_heavy(axb_ctx *c) {
+    c->heavy_list = nullptr;
+    c->heavy_scratch = nullptr;
+    if (c->h->ctr.max_deg < (unsigned)HEAVY_MIN_DEG) return AXB_OK;
+    c->heavy_blocks = (unsigned)c->sm_count * 2u;
+    ARENA(c, c->heavy_list, int, (size_t)c->n + 1);
+    ARENA(c, c->heavy_scratch, unsigned long long, (size_t)c->heavy_blocks * 2 * (MAXP + 1) * (size_t)c->W);
+    return AXB_OK;
+}
+
 // potential edges for generators [lo, hi) (+ the upper halo rows of a slab); synchronises once
 int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
     if (c->state < S_GRID) return fail(c, AXB_ERR_STATE, "axb_potential before axb_grid_build");
@@ -876,7 +902,7 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
         ARENA(c, c->pe_u, int, c->pe_cap);
         CUDA_TRY(c, cudaMemsetAsync(c->deg, 0, sizeof(int) * (size_t)n, c->stream));
         if (attempt) {   // reset the counters the first attempt touched
-            c->h->ctr.n_pe = 0; c->h->ctr.max_deg = 0; c->h->ctr.pair_bound = 0; c->h->ctr.overflow = 0;
+            c->h->ctr.n_pe = 0; c->h->ctr.max_deg = 0; c->h->ctr.pair_bound = 0; c->h->ctr.overflow = 0; c->h->ctr.n_heavy = 0;
             c->h->ctr.err_key = ~0ull; c->h->ctr.err_count = 0;
             CUDA_TRY(c, cudaMemcpyAsync(c->ctr, &c->h->ctr, sizeof(Counters), cudaMemcpyHostToDevice, c->stream));
         }
@@ -888,6 +914,13 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
         if (st != AXB_OK) return st;
         st = fetch_counters(c);
         if (st != AXB_OK) return st;
+        if (c->h->ctr.n_heavy) {            // generators with more partners than the pair queue holds (edges.cuh)
+            const size_t smem = sizeof(ELWarp) * EL_WARPS;
+            CUDA_TRY(c, cudaFuncSetAttribute(k_edges_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_edges_heavy<<<(unsigned)c->sm_count * 2u, EL_WARPS * 32, smem, c->stream>>>(P, c->gen_lo, edge_hi);
+            LAUNCH_CHECK(c);
+            if ((st = fetch_counters(c)) != AXB_OK) return st;
+        }
         if (c->dup_pending) {              // pipeline.py:238-244 comes before any edge is looked at
             c->dup_pending = false;
             if (c->h->ctr.dup_count) return report_duplicate(c, c->h->ctr.dup_count);
@@ -902,7 +935,8 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
     st = check_run_flags(c);
     if (st != AXB_OK) return st;
     c->n_pe = c->h->ctr.n_pe;
-    c->W = c->h->ctr.max_deg <= 64 ? 1 : 4;
+    c->W = trimask_words(c->h->ctr.max_deg);
+    if ((st = alloc_heavy(c)) != AXB_OK) return st;
     c->mark_after_edges = c->arena_used;
     c->state = S_EDGES;
     return AXB_OK;
@@ -1234,7 +1268,8 @@ extern "C" int axb_potential_import_edges(axb_ctx *c, const int64_t *d_rows, int
     if (c->h->ctr.max_deg > (unsigned)AXB_MAX_PARTNERS)
         return fail(c, AXB_ERR_DENSITY, "a ball has more than %d potential-edge partners", AXB_MAX_PARTNERS);
     c->n_pe = (uint32_t)m;
-    c->W = c->h->ctr.max_deg <= 64 ? 1 : 4;
+    c->W = trimask_words(c->h->ctr.max_deg);
+    if ((st = alloc_heavy(c)) != AXB_OK) return st;
     c->mark_after_edges = c->arena_used;
     c->state = S_EDGES;
     return AXB_OK;

@@ -51,6 +51,7 @@ struct Counters {
     unsigned int overflow;             // bit0: partner cap, bit1: PT cap, bit2: PQ cap, bit3: lookup miss
     unsigned int first_bad;            // first non-finite ball index (0xffffffff = none)
     unsigned int tile_next;            // k_tri_tet3: next unclaimed tile (dynamic scheduling)
+    unsigned int n_heavy;              // generators with more partners than a k_tri_tet3 tile holds (heavy.cuh)
     // --- the pruning stage's own counters: adjacent, zeroed with one memset per prune run
     unsigned int n_k3;                 // kept tets
     unsigned int lookup_miss;          // inherited faces whose generator row has no such partner
@@ -87,11 +88,21 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
-// error key: stage (3 bits) | generator rank (36 bits) | ordinal (24 bits); smaller = raised first
+// error key: stage (3 bits) | generator rank (31 bits) | ordinal (29 bits); smaller = raised first
 // by the reference when the whole input is one chunk (pipeline.py:357, 414, 419, 477).
 enum { ST_EDGE = 1, ST_VW = 2, ST_TRI = 3, ST_TET = 4 };
+constexpr int ERR_ORD_BITS = 29;
 __device__ __forceinline__ unsigned long long make_err_key(int stage, int gen_rank, unsigned ordinal) {
-    return ((unsigned long long)stage << 60) | ((unsigned long long)(unsigned)gen_rank << 24) | (ordinal & 0xffffffu);
+    return ((unsigned long long)stage << 60) | ((unsigned long long)(unsigned)gen_rank << ERR_ORD_BITS) |
+           (ordinal & ((1u << ERR_ORD_BITS) - 1u));
 }
+
+// partner slots of a tet inside its generator's list, three to a word (a generator has fewer than 1024 partners:
+// AXB_MAX_PARTNERS)
+constexpr int SLOT_BITS = 10;
+constexpr int SLOT_MASK = (1 << SLOT_BITS) - 1;
+__host__ __device__ __forceinline__ int pack_slots(int i, int j, int k) { return i | (j << SLOT_BITS) | (k << (2 * SLOT_BITS)); }
+// ordinal of a tet in its generator's enumeration: (ordinal of the generating triangle, third partner slot)
+__device__ __forceinline__ unsigned tet_ordinal(unsigned tri_ord, int k) { return (tri_ord << SLOT_BITS) | (unsigned)k; }
 
 }  // namespace axb

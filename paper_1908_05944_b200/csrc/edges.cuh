@@ -67,6 +67,120 @@ struct __align__(16) ELWarp {
 };
 static_assert(EL_ROWS * 32 * 2 >= EL_QCAP, "the sorted list aliases the row table");
 
+// Phase A of k_edges for one lane: loads generator t (if `active`), publishes its record in the warp's slot table,
+// trims its 13 candidate rows exactly and parks the non-empty ones in the lane's column of S.u.rows.
+// Returns the number of parked rows; ux, uy, uz, ureach = the generator (ureach < 0: not viable / idle lane).
+__device__ __forceinline__ int lane_rows(const EstParams &P, ELWarp &S, int t, int lane, bool active, double &ux, double &uy,
+                                         double &uz, double &ureach) {
+    const GridView &g = P.g;
+    int nr = 0;
+    if (active) ureach = __ldg(P.reach + t);
+    if (ureach >= 0.0) {                            // viable generator (pipeline.py:336-337)
+        const Atom au = load_atom(P.atoms, t);
+        const int4 cell = __ldg(P.cell_of_rank + t);
+        ux = au.x; uy = au.y; uz = au.z;
+        S.gx[lane] = au.x; S.gy[lane] = au.y; S.gz[lane] = au.z; S.gr2[lane] = au.r2;
+        S.gorig[lane] = __ldg(P.orig + t);
+        // trimming table: a candidate v passes the pre-filter only if |v - u| <= reach_u + reach_v <= reach_u +
+        // reach_max =: R, so cells whose nearest point is farther than R from u (1e-9 slack, far above rounding)
+        // hold no partner.  rem = (R2 - gy2) - gz2 is what is left for the x direction in row (oy, oz).
+        const double R = ureach + P.tol.reach_max;
+        const double R2 = R * R * (1.0 + 1e-9) + 1e-9;
+        const double xa = g.ox + (double)cell.x * g.side, ya = g.oy + (double)cell.y * g.side;
+        const double za = g.oz + (double)(cell.z + g.z_lo) * g.side;
+        const double dxl = fmax(au.x - xa, 0.0), dxh = fmax(xa + g.side - au.x, 0.0);
+        const double dyl = fmax(au.y - ya, 0.0), dyh = fmax(ya + g.side - au.y, 0.0);
+        const double dzh = fmax(za + g.side - au.z, 0.0);
+        const double xl0 = dxl * dxl, xl1 = (dxl + g.side) * (dxl + g.side);
+        const double xh0 = dxh * dxh, xh1 = (dxh + g.side) * (dxh + g.side);
+        const double gy2[5] = {(dyl + g.side) * (dyl + g.side), dyl * dyl, 0.0, dyh * dyh, (dyh + g.side) * (dyh + g.side)};
+        const double gz2[3] = {0.0, dzh * dzh, (dzh + g.side) * (dzh + g.side)};
+        int rs[EL_ROWS], re[EL_ROWS];
+#pragma unroll
+        for (int hl = 0; hl < EL_ROWS; ++hl) {      // rows in ascending key order: (oz 0: oy 0..2), (oz 1, 2: oy -2..2)
+            const int oz = hl < 3 ? 0 : 1 + (hl - 3) / 5;
+            const int oy = hl < 3 ? hl : (hl - 3) % 5 - 2;
+            const int y = cell.y + oy, z = cell.z + oz;
+            const double rem = (R2 - gy2[oy + 2]) - gz2[oz];
+            const bool ok = y >= 0 && y < g.dy && z < g.dz && rem >= 0.0;
+            const int nl = (xl0 <= rem) + (xl1 <= rem), nh = (xh0 <= rem) + (xh1 <= rem);
+            const int x0 = max(cell.x - nl, 0), x1 = min(cell.x + nh, g.dx - 1);
+            int s = 0, e = 0;
+            if (g.cell_start) {                     // dense table: clamped addresses, all 26 loads in flight together
+                const int row = ok ? g.dx * (y + g.dy * z) : 0;
+                s = (int)__ldg(g.cell_start + (ok ? row + x0 : 0));
+                e = (int)__ldg(g.cell_start + (ok ? row + x1 + 1 : 0));
+            } else if (ok) {
+                row_range(g, x0, x1, y, z, s, e);
+            }
+            if (hl == 0) s = max(s, t + 1);         // own row: only ranks above t
+            rs[hl] = s;
+            re[hl] = ok ? e : s;
+        }
+#pragma unroll
+        for (int hl = 0; hl < EL_ROWS; ++hl)
+            if (re[hl] > rs[hl]) { S.u.rows[nr][lane] = make_int2(rs[hl], re[hl]); ++nr; }
+    }
+    return nr;
+}
+
+// One generator with more partners than the pair queue holds (large alpha: hundreds of partners): k_edges marks it
+// (deg = -1) and k_edges_heavy, launched only when the counters say there is one, takes it.  The warp sweeps
+// its candidate rows twice, 32 candidates per round in rank order: the first sweep counts the kept pairs, one
+// atomicAdd reserves the list, the second sweep writes it (ballot/popc keeps the ascending order).  Generator 0 of
+// the pass: its record is in S.g*[0], its rows in S.u.rows[.][0].  Returns the number of partners.
+__device__ __forceinline__ unsigned heavy_generator(const EstParams &P, ELWarp &S, int t, int lane) {
+    Atom au;
+    au.x = S.gx[0]; au.y = S.gy[0]; au.z = S.gz[0]; au.r2 = S.gr2[0];
+    const int ou = S.gorig[0];
+    const double ureach = __ldg(P.reach + t);
+    const int nr = S.nrow[0];
+    unsigned total = 0, base = 0;
+    for (int sweep = 0; sweep < 2; ++sweep) {
+        unsigned w = 0, ord = 0;
+        for (int k = 0; k < nr; ++k) {
+            const int2 rw = S.u.rows[k][0];
+            for (int p0 = rw.x; p0 < rw.y; p0 += 32) {
+                const int p = p0 + lane;
+                bool keep = false;
+                if (p < rw.y) {
+                    const Atom xr = load_atom(P.xyzr, p);
+                    const double dx = xr.x - au.x, dy = xr.y - au.y, dz = xr.z - au.z;
+                    const double lims = xr.r2 + ureach;
+                    if (xr.r2 >= 0.0 && (dx * dx + dy * dy) + dz * dz <= lims * lims) {                 // pipeline.py:341-344
+                        const Atom av = load_atom(P.atoms, p);
+                        const int ov = __ldg(P.orig + p);
+                        const Ortho o = ortho_edge(ou, au, ov, av, P.tol.eps_sing);                     // pipeline.py:355-356
+                        if (sweep == 0 && o.singular && t < P.err_rank_hi)
+                            record_singular(P, make_err_key(ST_EDGE, t, ord + (unsigned)(p - p0)), ou, ov, -1, -1, 2);
+                        keep = o.size <= P.tol.lim_a;                                                   // pipeline.py:358
+                    }
+                }
+                const unsigned m = __ballot_sync(FULL, keep);
+                if (sweep == 1 && keep && (unsigned long long)base + total <= P.pe_cap) {
+                    const unsigned at = base + w + (unsigned)__popc(m & lanemask_lt());
+                    P.pe_v[at] = p;
+                    P.pe_u[at] = t;
+                }
+                w += (unsigned)__popc(m);
+                ord += (unsigned)min(32, rw.y - p0);
+            }
+        }
+        if (sweep == 0) {
+            total = w;
+            if (lane == 0 && total) base = atomicAdd(&P.ctr->n_pe, total);
+            base = __shfl_sync(FULL, base, 0);
+            if ((unsigned long long)base + total > P.pe_cap) {
+                if (lane == 0) atomicOr(&P.ctr->overflow, 1u << 4);   // potential-edge buffer too small: caller re-runs
+            } else if (lane == 0 && total) {
+                P.adj_off[t] = base;
+                P.deg[t] = (int)total;
+            }
+        }
+    }
+    return total;
+}
+
 // dyn: tiles are claimed from a global counter (dense regions make them very unequal); with at most one tile per
 // warp the plain assignment is used -- the claims of thousands of warps on one address would only cost time
 __global__ void __launch_bounds__(EL_WARPS * 32, EL_MINB) k_edges(EstParams P, int rank_lo, int rank_hi, int dyn) {
@@ -94,54 +208,7 @@ __global__ void __launch_bounds__(EL_WARPS * 32, EL_MINB) k_edges(EstParams P, i
             const int t = ts + lane;
             // ---- A: the lane's generator and its candidate rows
             double ux = 0.0, uy = 0.0, uz = 0.0, ureach = -1.0;
-            int nr = 0;
-            if (lane < gb) ureach = __ldg(P.reach + t);
-            if (ureach >= 0.0) {                            // viable generator (pipeline.py:336-337)
-                const Atom au = load_atom(P.atoms, t);
-                const int4 cell = __ldg(P.cell_of_rank + t);
-                ux = au.x; uy = au.y; uz = au.z;
-                S.gx[lane] = au.x; S.gy[lane] = au.y; S.gz[lane] = au.z; S.gr2[lane] = au.r2;
-                S.gorig[lane] = __ldg(P.orig + t);
-                // trimming table: a candidate v passes the pre-filter only if |v - u| <= reach_u + reach_v <= reach_u +
-                // reach_max =: R, so cells whose nearest point is farther than R from u (1e-9 slack, far above rounding)
-                // hold no partner.  rem = (R2 - gy2) - gz2 is what is left for the x direction in row (oy, oz).
-                const double R = ureach + P.tol.reach_max;
-                const double R2 = R * R * (1.0 + 1e-9) + 1e-9;
-                const double xa = g.ox + (double)cell.x * g.side, ya = g.oy + (double)cell.y * g.side;
-                const double za = g.oz + (double)(cell.z + g.z_lo) * g.side;
-                const double dxl = fmax(au.x - xa, 0.0), dxh = fmax(xa + g.side - au.x, 0.0);
-                const double dyl = fmax(au.y - ya, 0.0), dyh = fmax(ya + g.side - au.y, 0.0);
-                const double dzh = fmax(za + g.side - au.z, 0.0);
-                const double xl0 = dxl * dxl, xl1 = (dxl + g.side) * (dxl + g.side);
-                const double xh0 = dxh * dxh, xh1 = (dxh + g.side) * (dxh + g.side);
-                const double gy2[5] = {(dyl + g.side) * (dyl + g.side), dyl * dyl, 0.0, dyh * dyh, (dyh + g.side) * (dyh + g.side)};
-                const double gz2[3] = {0.0, dzh * dzh, (dzh + g.side) * (dzh + g.side)};
-                int rs[EL_ROWS], re[EL_ROWS];
-#pragma unroll
-                for (int hl = 0; hl < EL_ROWS; ++hl) {      // rows in ascending key order: (oz 0: oy 0..2), (oz 1, 2: oy -2..2)
-                    const int oz = hl < 3 ? 0 : 1 + (hl - 3) / 5;
-                    const int oy = hl < 3 ? hl : (hl - 3) % 5 - 2;
-                    const int y = cell.y + oy, z = cell.z + oz;
-                    const double rem = (R2 - gy2[oy + 2]) - gz2[oz];
-                    const bool ok = y >= 0 && y < g.dy && z < g.dz && rem >= 0.0;
-                    const int nl = (xl0 <= rem) + (xl1 <= rem), nh = (xh0 <= rem) + (xh1 <= rem);
-                    const int x0 = max(cell.x - nl, 0), x1 = min(cell.x + nh, g.dx - 1);
-                    int s = 0, e = 0;
-                    if (g.cell_start) {                     // dense table: clamped addresses, all 26 loads in flight together
-                        const int row = ok ? g.dx * (y + g.dy * z) : 0;
-                        s = (int)__ldg(g.cell_start + (ok ? row + x0 : 0));
-                        e = (int)__ldg(g.cell_start + (ok ? row + x1 + 1 : 0));
-                    } else if (ok) {
-                        row_range(g, x0, x1, y, z, s, e);
-                    }
-                    if (hl == 0) s = max(s, t + 1);         // own row: only ranks above t
-                    rs[hl] = s;
-                    re[hl] = ok ? e : s;
-                }
-#pragma unroll
-                for (int hl = 0; hl < EL_ROWS; ++hl)
-                    if (re[hl] > rs[hl]) { S.u.rows[nr][lane] = make_int2(rs[hl], re[hl]); ++nr; }
-            }
+            int nr = lane_rows(P, S, t, lane, lane < gb, ux, uy, uz, ureach);
             S.nrow[lane] = nr;
             __syncwarp();
             // a pass takes as many generators as fit the candidate budget (dense cores: three times the balls per cell):
@@ -243,12 +310,14 @@ __global__ void __launch_bounds__(EL_WARPS * 32, EL_MINB) k_edges(EstParams P, i
                 }
             }
             if (crowded) {
-                // more kept pairs than the queue holds: halve the pass and redo it; for a single generator it is the
-                // density limit (AXB_ERR_DENSITY)
+                // more kept pairs than the queue holds: halve the pass and redo it; a single generator that still does
+                // not fit is left to k_edges_heavy (count, allocate, write)
                 __syncwarp();
                 if (gb > 1) { gb = gb / 2; continue; }
-                if (lane == 0) atomicOr(&P.ctr->overflow, 1u);
-                qn = 0; solved = 0;
+                if (lane == 0) { P.deg[ts] = -1; atomicAdd(&P.ctr->n_heavy, 1u); }            // for k_edges_heavy
+                ts += 1;
+                gb = 32;
+                continue;
             }
             settle();
             // ---- D: partner lists.  Count per generator, prefix, stable scatter (rounds in queue order, match_any
@@ -313,6 +382,34 @@ __global__ void __launch_bounds__(EL_WARPS * 32, EL_MINB) k_edges(EstParams P, i
         pairs += __shfl_xor_sync(FULL, pairs, o);
     }
     if (lane == 0) {
+        atomicMax(&P.ctr->max_deg, max_deg);
+        atomicAdd(&P.ctr->pair_bound, pairs);
+    }
+}
+
+// The generators k_edges marked (deg == -1): a warp each, two sweeps (heavy_generator).
+__global__ void __launch_bounds__(EL_WARPS * 32) k_edges_heavy(EstParams P, int rank_lo, int rank_hi) {
+    extern __shared__ __align__(16) unsigned char s_raw_el[];
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    ELWarp &S = reinterpret_cast<ELWarp *>(s_raw_el)[warp];
+    unsigned max_deg = 0;
+    unsigned long long pairs = 0;
+    for (int t = rank_lo + blockIdx.x * EL_WARPS + warp; t < rank_hi; t += gridDim.x * EL_WARPS) {
+        if (P.deg[t] != -1) continue;
+        double ux, uy, uz, ureach = -1.0;
+        const int nr = lane_rows(P, S, t, lane, lane == 0, ux, uy, uz, ureach);
+        S.nrow[lane] = nr;
+        __syncwarp();
+        const unsigned d = heavy_generator(P, S, t, lane);
+        if (lane == 0) {
+            if (d == 0) P.deg[t] = 0;
+            if (d > (unsigned)MAXP) atomicOr(&P.ctr->overflow, 1u);                               // AXB_ERR_DENSITY
+            max_deg = max(max_deg, d);
+            pairs += (unsigned long long)d * (d - 1) / 2;
+        }
+        __syncwarp();
+    }
+    if (lane == 0 && max_deg) {
         atomicMax(&P.ctr->max_deg, max_deg);
         atomicAdd(&P.ctr->pair_bound, pairs);
     }

@@ -8,7 +8,7 @@
 
 namespace axb {
 
-constexpr int MAXP = 256;      // AXB_MAX_PARTNERS
+constexpr int MAXP = 1023;     // AXB_MAX_PARTNERS (partner slots are packed 10 bits each)
 
 struct EstParams {
     GridView g;
@@ -26,7 +26,7 @@ struct EstParams {
     int4 *pt;                   // potential triangles {u, v, w, i | j << 16}
     uint32_t pt_cap;
     int4 *pq_r;                 // potential tets, ranks {u, v, w, x}
-    int *pq_l;                  // potential tets, partner slots i | j << 8 | k << 16
+    int *pq_l;                  // potential tets, partner slots (pack_slots)
     uint32_t pq_cap;
     Counters *ctr;
     ErrRecord *errs;

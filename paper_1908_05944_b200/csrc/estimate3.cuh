@@ -238,8 +238,8 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
         {   // generators of the tile: atom index SCAP + g
             int d = 0;
             if (lane < ng_all) {
-                d = min(__ldg(P.deg + t0 + lane), PCAP);
-                if (d < 2) d = 0;                           // no partner pair, nothing to do
+                d = __ldg(P.deg + t0 + lane);
+                if (d < 2 || d > PCAP) d = 0;               // no partner pair: nothing to do; too many for a tile: heavy.cuh
                 S.gadj[lane] = __ldg(P.adj_off + t0 + lane);
                 // slab, lower halo: only simplices that reach an owned ball matter (partners ascend in rank)
                 if (d && t0 + lane < P.own_lo && __ldg(P.pe_v + S.gadj[lane] + d - 1) < P.own_lo) d = 0;
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                             const Ortho e4 = ortho_tet_s(S, SCAP + g, s, sj, sk, P.tol.eps_sing);        // pipeline.py:475-477
                             if (e4.singular) {
                                 const unsigned tri_ord = (unsigned)(tc0 + x - S.rowpre[sb]);             // ordinal among u's triangles
-                                record_singular(P, make_err_key(ST_TET, t, (tri_ord << 8) | (unsigned)k), S.aorig[SCAP + g],
+                                record_singular(P, make_err_key(ST_TET, t, tet_ordinal(tri_ord, k)), S.aorig[SCAP + g],
                                                 S.aorig[s], S.aorig[sj], S.aorig[sk], 4);
                             }
                             keep = e4.size <= P.tol.lim_a;                                               // pipeline.py:478
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                                 dominated_by_partner3(S, sb, sb + S.gdeg[g], s, sj, sk, e4.cx, e4.cy, e4.cz, e4.size - P.tol.eps_abs))
                                 keep = false;        // AC2 would fail at this partner (it lies in the 27-cell block): never kept
                             er = make_int4(t, S.srank[s], S.srank[sj], S.srank[sk]);
-                            el = (int)S.sli[s] | (j << 8) | (k << 16);
+                            el = pack_slots((int)S.sli[s], j, k);
                         }
                         const unsigned m = __ballot_sync(FULL, keep);
                         if (m) {

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) k_import_simplices(int k, const int64_t *
         pt[e] = make_int4(r[0], r[1], r[2], s[0] | (s[1] << 16));
     } else {
         pq_r[e] = make_int4(r[0], r[1], r[2], r[3]);
-        pq_l[e] = s[0] | (s[1] << 8) | (s[2] << 16);
+        pq_l[e] = pack_slots(s[0], s[1], s[2]);
     }
 }
 
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(128) k_tets_from_triangles(TetsFromTris P) {
                 const Atom p[4] = {ai, aj, ak, load_atom(P.atoms, rx)};
                 const Ortho o = orthoN<4>(p, P.eps_sing);
                 if (o.singular)
-                    record_singular_impl(P.ctr, P.errs, P.report_key, make_err_key(ST_TET, 0, 0) | ((unsigned long long)t << 24) | (ordinal & 0xffffffu),
+                    record_singular_impl(P.ctr, P.errs, P.report_key, make_err_key(ST_TET, (int)t, ordinal),
                                          (int)bi, (int)bj, (int)bk, (int)bx, 4);
                 ++ordinal;
                 if (!(o.size <= P.lim_a)) continue;
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(128) k_tets_from_triangles(TetsFromTris P) {
                 const unsigned pos = atomicAdd(&P.ctr->n_pq, 1u);
                 if (pos < P.pq_cap) {
                     P.pq_r[pos] = make_int4(r[0], r[1], r[2], r[3]);
-                    P.pq_l[pos] = max(s0, 0) | (max(s1, 0) << 8) | (max(s2, 0) << 16);
+                    P.pq_l[pos] = pack_slots(max(s0, 0), max(s1, 0), max(s2, 0));
                 }
             }
         }

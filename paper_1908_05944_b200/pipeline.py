@@ -584,7 +584,7 @@ class Engine:
 
             key, xyz = self._error_detail()
             if st == N.ERR_DEGENERATE:
-                key += int(slab.first_rank) << 24
+                key += int(slab.first_rank) << 29      # ERR_ORD_BITS of csrc/common.cuh
             return [], SlabError(status=int(st), key=key, vertices=self._error_vertices(), xyz=xyz, message=self._message())
         self._collect_stage_ms()
         return outs if raise_errors else (outs, None)

@@ -268,6 +268,73 @@ def test_dense_blob_crowded_edge_batches_against_oracle():
         assert_same_complex(k, ref, f"dense blob alpha={alpha}")
 
 
+def test_hundreds_of_partners_per_ball_against_oracle():
+    """The reference has no density limit (pipeline.py:316-359).  alpha = 40 A^2 at protein density gives every
+    ball several hundred potential-edge partners: more than the pair queue of k_edges (two-sweep path), more than
+    a k_tri_tet3 tile (heavy.cuh: bit matrices in global scratch) and a kept-triangle mask of 5+ words per row."""
+    import torch
+
+    tol = ax.TolerancePolicy(1e-9, 1e-300)
+    c, r = synth.jittered_lattice(700, 31)
+    k = ax.compute_alpha_complex_arrays(c[:450], r[:450], ax.PipelineConfig(alpha=40.0, tolerance=tol))
+    ref = oracle.compute(c[:450], r[:450], 40.0, eps_singular=1e-300, threads=os.cpu_count(), chunk=16)
+    assert ref.status == oracle.OK
+    assert_same_complex(k, ref, "alpha=40")
+    # (this input does take the heavy paths: potential edges = all pairs with ortho-size <= alpha + slack, the
+    # completeness property of reference pkg/tests/test_grid.py:159-171; partners are counted at the lower grid rank)
+    i, j = np.triu_indices(450, 1)
+    _, sizes, _ = oracle.ortho_batch(np.stack([c[i], c[j]], axis=1), np.stack([r[i] ** 2, r[j] ** 2], axis=1), 1e-300)
+    pot = sizes <= 40.0 + 1e-9
+    st, g = oracle.grid_build(c[:450], r[:450], 40.0)
+    assert np.bincount(np.minimum(g.rank[i[pot]], g.rank[j[pot]])).max() > 300
+    # the stage API sees the same potential levels (complete lists: no cull) at up to 256 partners per generator
+    eng = ax.default_engine()
+    cfg = ax.PipelineConfig(alpha=40.0, tolerance=tol)
+    c3, r3 = c[:300], r[:300]
+    ref = oracle.compute(c3, r3, 40.0, eps_singular=1e-300, keep_potentials=True, threads=os.cpu_count(), chunk=16)
+    eng.stage_grid(torch.as_tensor(c3, device="cuda"), torch.as_tensor(r3, device="cuda"), cfg, arena_factor=64.0)
+    eng.stage_potential()
+    for dim in (1, 2, 3):
+        rows = lexsorted(eng.stage_potential_export(dim)[0].cpu().numpy())[0]
+        assert np.array_equal(rows, ref.potentials[dim][0]), dim
+    # a dense blob in a sparse surrounding: only a few generators take the heavy path
+    rng = np.random.default_rng(5)
+    blob = rng.uniform(0.0, 9.0, size=(420, 3)) + 20.0
+    c2 = np.concatenate([synth.jittered_lattice(3000, 2)[0], blob])
+    r2 = rng.uniform(1.2, 1.9, size=len(c2))
+    k = ax.compute_alpha_complex_arrays(c2, r2, ax.PipelineConfig(alpha=6.0, tolerance=tol))
+    ref = oracle.compute(c2, r2, 6.0, eps_singular=1e-300, threads=os.cpu_count(), chunk=16)
+    assert ref.status == oracle.OK
+    assert_same_complex(k, ref, "dense blob in a lattice")
+    # 620 balls strung along a 2.9 A arc of a 50 A circle: every pair is a potential edge (up to 604 partners per
+    # generator, more than the pair queue of k_edges holds: its two-sweep path; kept-triangle mask of 10 words per row)
+    n, rho = 620, 50.0
+    th = np.linspace(0.0, 2.9 / rho, n)
+    arc = np.stack([rho * np.cos(th), rho * np.sin(th), rng.uniform(-3e-3, 3e-3, size=n)], axis=1)[rng.permutation(n)]
+    ra = rng.uniform(1.45, 1.55, size=n)
+    for bio in (False, True):
+        k = ax.compute_alpha_complex_arrays(arc, ra, ax.PipelineConfig(alpha=0.0, biomolecule_mode=bio, tolerance=tol))
+        ref = oracle.compute(arc, ra, 0.0, eps_singular=1e-300, biomolecule=bio, keep_potentials=True, threads=os.cpu_count(), chunk=16)
+        assert ref.status == oracle.OK and len(ref.edges) > 0
+        assert_same_complex(k, ref, "balls on an arc")
+    st, g = oracle.grid_build(arc, ra, 0.0)
+    assert np.bincount(g.rank[ref.potentials[1][0]].min(axis=1)).max() > 500
+    # flatter (z within 1e-4 A): four balls turn out affinely dependent to the last bit; the heavy path must name the
+    # tetrahedron the reference meets first in its enumeration
+    flat = arc.copy()
+    flat[:, 2] = rng.uniform(-1e-4, 1e-4, size=n)
+    bad = oracle.compute(flat, ra, 0.0, eps_singular=1e-300, threads=os.cpu_count(), chunk=16)
+    if bad.status == oracle.DEGENERATE:
+        with pytest.raises(ax.DegenerateSimplex) as err:
+            ax.compute_alpha_complex_arrays(flat, ra, ax.PipelineConfig(alpha=0.0, tolerance=tol))
+        assert tuple(err.value.vertices) == tuple(bad.error_vertices)
+    eng.stage_grid(torch.as_tensor(arc, device="cuda"), torch.as_tensor(ra, device="cuda"), ax.PipelineConfig(alpha=0.0, tolerance=tol), arena_factor=64.0)
+    eng.stage_potential()
+    for dim in (1, 2, 3):
+        rows = lexsorted(eng.stage_potential_export(dim)[0].cpu().numpy())[0]
+        assert np.array_equal(rows, ref.potentials[dim][0]), dim
+
+
 def test_randomised_shapes_against_oracle():
     """tools/gpu_fuzz.py as a test: 120 small inputs of many shapes (clusters, near-lattices with ties, far-away
     offsets, flat slabs, lines; wide radii, negative alpha, both vertex modes, both pivot thresholds): same

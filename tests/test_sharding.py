@@ -118,9 +118,9 @@ def test_pick_error_is_the_reference_order():
     E = sharding.SlabError
     dup_a = E(status=6, vertices=(5, 9), xyz=(1.0, 2.0, 3.0))
     dup_b = E(status=6, vertices=(2, 3), xyz=(1.0, 2.0, 2.5))
-    deg_a = E(status=7, key=(1 << 60) | (700 << 24) | 3, vertices=(1, 2))
-    deg_b = E(status=7, key=(1 << 60) | (650 << 24) | 9, vertices=(4, 8))
-    deg_tri = E(status=7, key=(3 << 60) | (10 << 24), vertices=(0, 1, 2))
+    deg_a = E(status=7, key=(1 << 60) | (700 << 29) | 3, vertices=(1, 2))
+    deg_b = E(status=7, key=(1 << 60) | (650 << 29) | 9, vertices=(4, 8))
+    deg_tri = E(status=7, key=(3 << 60) | (10 << 29), vertices=(0, 1, 2))
     limit = E(status=10, message="too dense")
     assert sharding.pick_error([None, None]) is None
     assert sharding.pick_error([None, E(0)]) is None
@@ -155,7 +155,7 @@ def _worker(rank, world, port, out_dir):
                                                                  *plan.rank_ranges[rank])]
         # one status for all ranks: nobody failed -> None everywhere; one rank failed -> everyone learns which error
         assert sharding.agree_on_error(None, dist) is None
-        mine = sharding.SlabError(status=7, key=(1 << 60) | ((100 - rank) << 24), vertices=(rank, rank + 5)) if rank else None
+        mine = sharding.SlabError(status=7, key=(1 << 60) | ((100 - rank) << 29), vertices=(rank, rank + 5)) if rank else None
         hit = sharding.agree_on_error(mine, dist)
         assert hit[0] == world - 1 and hit[1].vertices == (world - 1, world + 4)
         stats = {}
