@@ -293,8 +293,9 @@ def workload_config(args, n_local):
                         f"1 atom/12 A^3, radii U[1.2,1.9] A, alpha={args.alpha} A^2",
             "atoms_per_gpu": n_local, "alpha": args.alpha, "eps_singular": args.eps_singular,
             "l2": "flushed (256 MiB write) between timed steps; per-step working set ~1.5 GB also exceeds L2",
-            "sharding": ("one z-slab per rank, 2-cell halo replicated; every slab emits the simplices it generates (disjoint lists); "
-                         "one collective: gather of counts and rows to rank 0 (NCCL send/recv), merged there") if args.gpus > 1 else "single GPU"}
+            "sharding": ("one z-slab per rank, 2-cell halo replicated; every slab emits the simplices it generates (disjoint lists, no "
+                         "cross-GPU dedup); rows redistributed by index range (all_to_all), interleaved on every rank, "
+                         "gathered to rank 0 (NCCL send/recv)") if args.gpus > 1 else "single GPU"}
 
 
 def bench_b200(args, rank, world, local_rank):
@@ -496,6 +497,7 @@ def bench_b200(args, rank, world, local_rank):
     if job is not None:
         g = job.last_gather
         line["collectives"] = {"backend": backend, "per_step": ["all_gather of 10 status words (agreement on one error)",
+                                                                   "all_to_all of row counts + one all_to_all of rows per dimension (index ranges)",
                                                                    "all_gather of the 4 row counts", "grouped send/recv of the rows to rank 0"],
                                "rows_by_rank": g.get("rows").tolist() if g.get("rows") is not None else None,
                                "bytes_into_rank0_per_step": int(g.get("bytes", 0)), "wire": "int32" if n_total < 2 ** 31 else "int64"}

@@ -224,6 +224,10 @@ int axb_export_host(axb_ctx *ctx, int64_t *h_vertices, int64_t *h_edges, int64_t
  * Reuses the scratch arena from the start (drops the state of a previous run). */
 int axb_merge_rows(axb_ctx *ctx, int k, int64_t n_index, const int64_t *d_rows, int64_t m, int64_t *d_out,
                    int64_t *count_out);
+/* The same for rows whose first index lies in [index_lo, index_hi): what one rank of a sharded run interleaves after
+ * the rows were redistributed by index range (bucket arrays sized for the range, not for the whole job). */
+int axb_merge_rows_range(axb_ctx *ctx, int k, int64_t index_lo, int64_t index_hi, const int64_t *d_rows, int64_t m,
+                         int64_t *d_out, int64_t *count_out);
 
 /* ---- canonical text document (a "next" row of SURVEY 8(f)) ---------------- */
 /* The body of write_complex (reference io.py:228-236): one line "dim v0 [v1 [v2 [v3]]]\n" per

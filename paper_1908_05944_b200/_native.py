@@ -24,7 +24,7 @@ STAGE_KEYS = ("grid", "potential_edges", "potential_triangles", "potential_tets"
 SYMBOLS = (
     "axb_version", "axb_status_name", "axb_ctx_create", "axb_ctx_destroy", "axb_ctx_set_stream",
     "axb_ctx_set_arena", "axb_arena_needed", "axb_arena_used", "axb_arena_hint", "axb_last_message",
-    "axb_last_error", "axb_last_error_detail", "axb_grid_build", "axb_grid_build_slab", "axb_slab_rank_range", "axb_merge_rows", "axb_compute_slab",
+    "axb_last_error", "axb_last_error_detail", "axb_grid_build", "axb_grid_build_slab", "axb_slab_rank_range", "axb_merge_rows", "axb_merge_rows_range", "axb_compute_slab",
     "axb_grid_get_info", "axb_grid_export", "axb_potential",
     "axb_potential_counts", "axb_potential_export", "axb_potential_edges", "axb_potential_simplices",
     "axb_potential_import_edges", "axb_potential_import_simplices", "axb_potential_tets_from_triangles", "axb_ac2_mask",
@@ -84,6 +84,7 @@ def load() -> C.CDLL:
         "axb_slab_rank_range": (C.c_int, [vp, i64, i64, pi64, pi64]),
         "axb_compute_slab": (C.c_int, [vp, i64, vp, vp, vp, C.POINTER(Params), C.POINTER(Slab), i64, i64, pi64]),
         "axb_merge_rows": (C.c_int, [vp, C.c_int, i64, vp, i64, vp, pi64]),
+        "axb_merge_rows_range": (C.c_int, [vp, C.c_int, i64, i64, vp, i64, vp, pi64]),
         "axb_grid_get_info": (C.c_int, [vp, C.POINTER(GridInfo)]),
         "axb_grid_export": (C.c_int, [vp, vp, vp, vp]),
         "axb_potential": (C.c_int, [vp, i64, i64]),

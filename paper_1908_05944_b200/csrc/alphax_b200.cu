@@ -504,6 +504,8 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
         c->many_tets = c->h->ctr.pair_bound > (unsigned long long)TETS_DYN_PAIRS * (unsigned long long)std::max(ngen, 1);   // k_prune_tets variant
         if (c->W != 1) st = launch(k_tri_tet3<4, T3_LIGHT>, sizeof(T3Warp<4, T3_LIGHT>), T3Cfg<4, T3_LIGHT>::GENS, 1);
         else if (heavy) st = launch(k_tri_tet3<1, T3_HEAVY>, sizeof(T3Warp<1, T3_HEAVY>), T3Cfg<1, T3_HEAVY>::GENS, T3Cfg<1, T3_HEAVY>::MINB);
+        else if ((unsigned)ngen <= 16u * T3_WARPS * (unsigned)c->sm_count * (unsigned)T3Cfg<1, T3_LIGHT>::MINB * 2u)    // <= 2 tiles per warp
+            st = launch(k_tri_tet3<1, T3_SMALL>, sizeof(T3Warp<1, T3_SMALL>), T3Cfg<1, T3_SMALL>::GENS, T3Cfg<1, T3_SMALL>::MINB);
         else st = launch(k_tri_tet3<1, T3_LIGHT>, sizeof(T3Warp<1, T3_LIGHT>), T3Cfg<1, T3_LIGHT>::GENS, T3Cfg<1, T3_LIGHT>::MINB);
         if (st != AXB_OK) return st;
         LAUNCH_CHECK(c);
@@ -1973,7 +1975,13 @@ extern "C" int axb_export_host(axb_ctx *c, int64_t *h_v, int64_t *h_e, int64_t *
 
 extern "C" int axb_merge_rows(axb_ctx *c, int k, int64_t n_index, const int64_t *d_rows, int64_t m, int64_t *d_out,
                               int64_t *count_out) {
-    if (!c || k < 1 || k > 4 || n_index < 1 || m < 0 || !count_out) return AXB_ERR_BAD_ARG;
+    return axb_merge_rows_range(c, k, 0, n_index, d_rows, m, d_out, count_out);
+}
+
+extern "C" int axb_merge_rows_range(axb_ctx *c, int k, int64_t index_lo, int64_t index_hi, const int64_t *d_rows, int64_t m,
+                                    int64_t *d_out, int64_t *count_out) {
+    const int64_t n_index = index_hi - index_lo, base = index_lo;
+    if (!c || k < 1 || k > 4 || index_lo < 0 || n_index < 1 || m < 0 || !count_out) return AXB_ERR_BAD_ARG;
     if (n_index >= ((int64_t)1 << 31) - 1 || m >= ((int64_t)1 << 32) - 16) return fail(c, AXB_ERR_BAD_ARG, "merge input too large");
     c->state = S_NONE;          // the arena is reused from the start
     c->arena_used = 0;
@@ -1997,22 +2005,22 @@ extern "C" int axb_merge_rows(axb_ctx *c, int k, int64_t n_index, const int64_t 
     CUDA_TRY(c, cudaMemsetAsync(ucnt, 0, sizeof(uint32_t) * ((size_t)n_index + 2), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(tmp, 0xff, sizeof(int4) * (size_t)m, c->stream));   // owner -1 = skipped
     const unsigned nb = blocks_for((size_t)m, 256);
-    k_merge_count<<<nb, 256, 0, c->stream>>>(d_rows, (unsigned)m, k, (unsigned)n_index, cnt, c->ctr);
+    k_merge_count<<<nb, 256, 0, c->stream>>>(d_rows, (unsigned)m, k, (unsigned)n_index, base, cnt, c->ctr);
     LAUNCH_CHECK(c);
     int st = device_scan(c, cnt, (size_t)n_index, off);
     if (st != AXB_OK) return st;
-    k_merge_scatter<<<nb, 256, 0, c->stream>>>(d_rows, (unsigned)m, k, (unsigned)n_index, cnt, off, tmp);
+    k_merge_scatter<<<nb, 256, 0, c->stream>>>(d_rows, (unsigned)m, k, (unsigned)n_index, base, cnt, off, tmp);
     LAUNCH_CHECK(c);
     k_merge_mark<<<nb, 256, 0, c->stream>>>(tmp, off, (unsigned)m, ucnt, dup);
     LAUNCH_CHECK(c);
     st = device_scan(c, ucnt, (size_t)n_index, uoff);
     if (st != AXB_OK) return st;
-    k_merge_emit<<<nb, 256, 0, c->stream>>>(tmp, off, uoff, dup, (unsigned)m, k, d_out);
+    k_merge_emit<<<nb, 256, 0, c->stream>>>(tmp, off, uoff, dup, (unsigned)m, k, base, d_out);
     LAUNCH_CHECK(c);
     CUDA_TRY(c, cudaMemcpyAsync(&c->h->totals[0], uoff + n_index, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     st = fetch_counters(c);
     if (st != AXB_OK) return st;
-    if (c->h->ctr.overflow) return fail(c, AXB_ERR_BAD_ARG, "merge input holds an index outside [0, n_index)");
+    if (c->h->ctr.overflow) return fail(c, AXB_ERR_BAD_ARG, "merge input holds a first index outside the given range");
     *count_out = c->h->totals[0];
     return AXB_OK;
 }

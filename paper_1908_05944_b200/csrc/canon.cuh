@@ -271,22 +271,26 @@ __device__ __forceinline__ bool row_less(const int4 &a, const int4 &b) {   // sa
 }
 __device__ __forceinline__ bool row_equal(const int4 &a, const int4 &b) { return a.y == b.y && a.z == b.z && a.w == b.w; }
 
+// (`base`: the rows' first column lies in [base, base + n_index) -- a rank that merges one index range of a sharded
+// run sizes its bucket arrays for that range only)
 __global__ void __launch_bounds__(256) k_merge_count(const int64_t *__restrict__ rows, unsigned m, int k, unsigned n_index,
-                                                     uint32_t *__restrict__ cnt, Counters *ctr) {
+                                                     int64_t base, uint32_t *__restrict__ cnt, Counters *ctr) {
     unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= m) return;
-    const int64_t a = rows[(size_t)s * k];
+    const int64_t a = rows[(size_t)s * k] - base;
     if (a < 0 || a >= (int64_t)n_index) { atomicOr(&ctr->overflow, 1u << 6); return; }
     atomicAdd(cnt + a, 1u);
 }
 
 __global__ void __launch_bounds__(256) k_merge_scatter(const int64_t *__restrict__ rows, unsigned m, int k, unsigned n_index,
-                                                       uint32_t *__restrict__ cnt, const uint32_t *__restrict__ off,
+                                                       int64_t base, uint32_t *__restrict__ cnt, const uint32_t *__restrict__ off,
                                                        int4 *__restrict__ tmp) {
     unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= m) return;
-    const int4 r = load_row4(rows, s, k);
-    if (r.x < 0 || (unsigned)r.x >= n_index) return;
+    int4 r = load_row4(rows, s, k);
+    const int64_t a = rows[(size_t)s * k] - base;
+    if (a < 0 || a >= (int64_t)n_index) return;
+    r.x = (int)a;                                    // bucket = owner relative to the range
     const unsigned slot = atomicSub(cnt + r.x, 1u) - 1u;
     tmp[off[r.x] + slot] = r;
 }
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(256) k_merge_mark(const int4 *__restrict__ tmp
 
 __global__ void __launch_bounds__(256) k_merge_emit(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                     const uint32_t *__restrict__ uoff, const unsigned char *__restrict__ dup,
-                                                    unsigned m, int k, int64_t *__restrict__ out) {
+                                                    unsigned m, int k, int64_t base, int64_t *__restrict__ out) {
     unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= m || dup[s]) return;
     const int4 me = tmp[s];
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(256) k_merge_emit(const int4 *__restrict__ tmp
     unsigned pos = uoff[me.x];
     for (unsigned q = lo; q < hi; ++q)
         if (!dup[q] && row_less(tmp[q], me)) ++pos;
-    out[(size_t)pos * k] = me.x;
+    out[(size_t)pos * k] = (int64_t)me.x + base;
     if (k > 1) out[(size_t)pos * k + 1] = me.y;
     if (k > 2) out[(size_t)pos * k + 2] = me.z;
     if (k > 3) out[(size_t)pos * k + 3] = me.w;

@@ -34,7 +34,8 @@ constexpr int T3_WARPS = T3_WARPS_V;      // warps per block (each one is indepe
 // pairs (alpha = 0); the heavy shape shrinks the tile (6 generators) so that 24 instead of 16 warps fit an SM (80 registers,
 // ~7 KB of shared memory per warp) -- measured 8-10 % faster once generators have 40+ pairs (alpha = 1.4,
 // dense cores), 9 % slower at alpha = 0.
-enum { T3_LIGHT = 0, T3_HEAVY = 1 };
+enum { T3_LIGHT = 0, T3_HEAVY = 1, T3_SMALL = 2 };   // T3_SMALL: the light algorithm at 16 warps per SM, no spilled values
+                                                     // (few tiles per warp: nothing hides a slower tile)
 constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved as soon as 256 are waiting)
 
 // heavy tile shape (tuning knobs, tools/gpu_autotune.sh: 6 generators / 160 triangles per round beat 8 / 112 by 5 % at
@@ -53,18 +54,21 @@ constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved 
 #define T3H_MINB 6
 #endif
 
-// light tile shape
+// light tile shape.  The kernel's time goes with 1 / resident warps up to 16 per SM (4, 8, 12, 16 warps: 1.55, 0.82, 0.58,
+// 0.46 ms at 1M atoms, alpha 0) and flattens beyond: 24 warps need 80 registers (a few spilled values) and at most 9.4 KB
+// of shared memory per warp (96 partner slots, 160 triangles per round), worth another 3-5 % (0.445 ms; ncu r2c: issue
+// slots 48 -> 55 %, but long-scoreboard stalls per issue 1.7 -> 3.6)
 #ifndef T3L_SCAP
-#define T3L_SCAP 128
+#define T3L_SCAP 96
 #endif
 #ifndef T3L_TCAP
-#define T3L_TCAP 224
+#define T3L_TCAP 160
 #endif
 #ifndef T3L_MINB
-#define T3L_MINB 4
+#define T3L_MINB 6
 #endif
 #ifndef T3L_PTAB
-#define T3L_PTAB 1024
+#define T3L_PTAB 640
 #endif
 // cull mode bit 1 (triangles flagged as dominated by a partner, AXB_CULL=2|3) needs a third bit matrix per warp; it
 // never paid, so it is compiled out unless asked for
@@ -75,12 +79,12 @@ constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved 
 template <int W, int SHAPE>
 struct T3Cfg {
     static constexpr int GENS = (W == 1 && SHAPE == T3_HEAVY) ? T3H_GENS : 16;                      // generators per warp tile (<= 16)
-    static constexpr int SCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_SCAP : T3L_SCAP) : 256;   // partner slots per sub-pass (>= 64 * W)
-    static constexpr int TCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_TCAP : T3L_TCAP) : 512;  // triangles per round
-    static constexpr int MINB = W == 1 ? (SHAPE == T3_HEAVY ? T3H_MINB : T3L_MINB) : 1;        // resident blocks per SM the registers must allow
+    static constexpr int SCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_SCAP : SHAPE == T3_SMALL ? 128 : T3L_SCAP) : 256;   // partner slots per sub-pass (>= 64 * W)
+    static constexpr int TCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_TCAP : SHAPE == T3_SMALL ? 224 : T3L_TCAP) : 512;  // triangles per round
+    static constexpr int MINB = W == 1 ? (SHAPE == T3_HEAVY ? T3H_MINB : SHAPE == T3_SMALL ? 4 : T3L_MINB) : 1;        // resident blocks per SM the registers must allow
     static constexpr int NA = SCAP + GENS;              // atom index space: partner slots, then the tile's generators
-    static constexpr bool FLAT = W == 1 && SHAPE == T3_LIGHT;   // flattened pair enumeration (pays while degrees are small)
-    static constexpr int PTAB = FLAT ? T3L_PTAB : 32;   // partner pairs of a sub-pass covered by the stamped pair table
+    static constexpr bool FLAT = W == 1 && SHAPE != T3_HEAVY;   // flattened pair enumeration (pays while degrees are small)
+    static constexpr int PTAB = FLAT ? (SHAPE == T3_SMALL ? 1024 : T3L_PTAB) : 32;   // partner pairs of a sub-pass covered by the stamped pair table
 };
 
 template <int W, int SHAPE>

@@ -589,11 +589,14 @@ class Engine:
         self._collect_stage_ms()
         return outs if raise_errors else (outs, None)
 
-    def merge_rows(self, rows, k: int, n_index: int):
-        """Sorted duplicate-free union of canonical rows (CUDA int64 tensor (m,k) or (m,) for k=1)."""
+    def merge_rows(self, rows, k: int, n_index: int, index_lo: int = 0):
+        """Sorted duplicate-free union of canonical rows (CUDA int64 tensor (m,k) or (m,) for k=1) whose first index
+        lies in [index_lo, n_index)."""
         torch = self.torch
         rows = rows.contiguous().reshape(-1, k)
         m = int(rows.shape[0])
+        if m == 0:
+            return rows.reshape(-1) if k == 1 else rows
         out = torch.empty((m, k), dtype=torch.int64, device=rows.device)
         count = C.c_int64()
 
@@ -601,12 +604,12 @@ class Engine:
             alpha = 0.0
 
         def run():
-            return self.lib.axb_merge_rows(self.handle, k, int(n_index), rows.data_ptr() if m else None, m,
-                                           out.data_ptr() if m else None, C.byref(count))
+            return self.lib.axb_merge_rows_range(self.handle, k, int(index_lo), int(n_index), rows.data_ptr() if m else None, m,
+                                                 out.data_ptr() if m else None, C.byref(count))
 
         with torch.cuda.device(self.device):
             self._bind_stream()
-            st = self._with_arena(max(m, n_index) // 8 + 1, _Cfg, run)
+            st = self._with_arena(max(m, n_index - index_lo) // 8 + 1, _Cfg, run)
         if st != N.OK:
             raise AlphaxError(f"{self.lib.axb_status_name(st).decode()}: {self._message()}")
         out = out[: count.value]

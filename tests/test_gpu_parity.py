@@ -498,6 +498,13 @@ def test_device_merge_rows_matches_numpy():
         want = np.unique(rows, axis=0)
         assert np.array_equal(got.reshape(-1, k), want)
     assert eng.merge_rows(torch.empty((0, 3), dtype=torch.int64, device="cuda"), 3, 10).shape[0] == 0
+    # one index range of a sharded run: first indices in [200, 350)
+    rows = np.sort(rng.integers(200, 500, size=(5_000, 3)), axis=1)
+    rows = rows[rows[:, 0] < 350]
+    got = eng.merge_rows(torch.as_tensor(rows, device="cuda"), 3, 350, index_lo=200).cpu().numpy()
+    assert np.array_equal(got, np.unique(rows, axis=0))
+    with pytest.raises(ax.AlphaxError):
+        eng.merge_rows(torch.as_tensor(rows, device="cuda"), 3, 340, index_lo=200)
 
 
 def test_standalone_stage_api_against_reference_golden(gold_small):
