@@ -196,52 +196,39 @@ int mark_event(axb_ctx *c, int idx) {
     return AXB_OK;
 }
 
-// exclusive scan of n uint32 (out has n + 1 entries, may alias in)
-int device_scan(axb_ctx *c, const uint32_t *in, size_t n, uint32_t *out) {
-    size_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    if (ntiles == 0) ntiles = 1;
-    if (ntiles <= SCAN_SMALL_TILES) {                      // small input: one launch instead of three
-        Scan4 a{};
-        a.in[0] = in;
-        a.out[0] = out;
-        k_scan_small<<<1, SCAN_THREADS, 0, c->stream>>>(a, n);
+// exclusive scans of up to four equally long uint32 arrays in ONE launch (out has n + 1 entries, may alias in):
+// single pass with decoupled look-back (scan.cuh); a few tiles: one block per array walks them with a carry
+int device_scan_many(axb_ctx *c, int arrays, const uint32_t *const in[4], size_t n, uint32_t *const out[4]) {
+    Scan4 a{};
+    for (int k = 0; k < arrays; ++k) { a.in[k] = in[k]; a.out[k] = out[k]; }
+    const size_t ntiles = (n + 1 + SCAN_TILE - 1) / SCAN_TILE;
+    if (ntiles <= SCAN_SMALL_TILES) {
+        k_scan_small<<<arrays, SCAN_THREADS, 0, c->stream>>>(a, n);
         LAUNCH_CHECK(c);
         return AXB_OK;
     }
-    uint32_t *sums;
-    ARENA(c, sums, uint32_t, ntiles + 1);
-    k_scan_tile_sums<<<(unsigned)ntiles, SCAN_THREADS, 0, c->stream>>>(in, n, sums);
-    LAUNCH_CHECK(c);
-    k_scan_of_sums<<<1, SCAN_THREADS, 0, c->stream>>>(sums, ntiles);
-    LAUNCH_CHECK(c);
-    k_scan_apply<<<(unsigned)ntiles, SCAN_THREADS, 0, c->stream>>>(in, n, sums, out);
+    unsigned long long *status;
+    ARENA(c, status, unsigned long long, (size_t)arrays * ntiles + 1);     // + the four tickets
+    for (int k = 0; k < arrays; ++k) a.status[k] = status + (size_t)k * ntiles;
+    a.ticket = reinterpret_cast<unsigned int *>(status + (size_t)arrays * ntiles);
+    static_assert(sizeof(unsigned long long) * 2 >= sizeof(unsigned int) * 4, "tickets");
+    unsigned int *extra;
+    ARENA(c, extra, unsigned int, 4);
+    (void)extra;                                                           // keeps the tickets inside the allocation
+    CUDA_TRY(c, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * ((size_t)arrays * ntiles + 1) + 16, c->stream));
+    k_scan_lookback<<<dim3((unsigned)ntiles, (unsigned)arrays), LB_THREADS, 0, c->stream>>>(a, n);
     LAUNCH_CHECK(c);
     return AXB_OK;
 }
 
-// four exclusive scans of equally long arrays in three launches
+int device_scan(axb_ctx *c, const uint32_t *in, size_t n, uint32_t *out) {
+    const uint32_t *const i4[4] = {in, nullptr, nullptr, nullptr};
+    uint32_t *const o4[4] = {out, nullptr, nullptr, nullptr};
+    return device_scan_many(c, 1, i4, n, o4);
+}
+
 int device_scan4(axb_ctx *c, const uint32_t *const in[4], size_t n, uint32_t *const out[4]) {
-    size_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    if (ntiles == 0) ntiles = 1;
-    Scan4 a{};
-    if (ntiles <= SCAN_SMALL_TILES) {
-        for (int k = 0; k < 4; ++k) { a.in[k] = in[k]; a.out[k] = out[k]; }
-        k_scan_small<<<4, SCAN_THREADS, 0, c->stream>>>(a, n);
-        LAUNCH_CHECK(c);
-        return AXB_OK;
-    }
-    for (int k = 0; k < 4; ++k) {
-        a.in[k] = in[k];
-        a.out[k] = out[k];
-        ARENA(c, a.sums[k], uint32_t, ntiles + 1);
-    }
-    k_scan4_tile_sums<<<dim3((unsigned)ntiles, 4), SCAN_THREADS, 0, c->stream>>>(a, n);
-    LAUNCH_CHECK(c);
-    k_scan4_of_sums<<<4, SCAN_THREADS, 0, c->stream>>>(a, ntiles);
-    LAUNCH_CHECK(c);
-    k_scan4_apply<<<dim3((unsigned)ntiles, 4), SCAN_THREADS, 0, c->stream>>>(a, n);
-    LAUNCH_CHECK(c);
-    return AXB_OK;
+    return device_scan_many(c, 4, in, n, out);
 }
 
 __global__ void k_publish_state(const uint32_t *__restrict__ t0, const uint32_t *__restrict__ t1, const uint32_t *__restrict__ t2,

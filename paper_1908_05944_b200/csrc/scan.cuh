@@ -1,6 +1,5 @@
-// scan.cuh -- device-wide exclusive prefix sum over uint32 (three launches:
-// per-tile sums, scan of the tile sums by one block, per-tile rescan).  Warp
-// shuffles inside a tile; a tile is 1024 threads x 4 items.  Used for the
+// scan.cuh -- device-wide exclusive prefix sum over uint32: one launch, single pass with decoupled
+// look-back (warp shuffles inside a tile; a tile is 1024 threads x 4 items).  Used for the
 // dense cell table (counting sort, reference grid.py:128-134) and for the
 // per-owner offsets of the canonical output.
 #pragma once
@@ -42,113 +41,115 @@ __device__ __forceinline__ unsigned block_excl_scan_1024(unsigned v, unsigned *s
     return r;
 }
 
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_tile_sums(const uint32_t *__restrict__ in, size_t n,
-                                                                  uint32_t *__restrict__ tile_sums) {
-    __shared__ unsigned s_warp[33];
-    size_t base = (size_t)blockIdx.x * SCAN_TILE + (size_t)threadIdx.x * SCAN_ITEMS;
-    unsigned v = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i)
-        if (base + i < n) v += in[base + i];
-    unsigned total;
-    block_excl_scan_1024(v, s_warp, total);
-    if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
-}
-
-// one block; tile_sums[i] <- exclusive prefix; tile_sums[ntiles] <- grand total
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_of_sums(uint32_t *__restrict__ tile_sums, size_t ntiles) {
-    __shared__ unsigned s_warp[33];
-    unsigned carry = 0;
-    for (size_t base = 0; base < ntiles; base += SCAN_THREADS) {
-        size_t i = base + threadIdx.x;
-        unsigned v = i < ntiles ? tile_sums[i] : 0u;
-        unsigned total;
-        unsigned ex = block_excl_scan_1024(v, s_warp, total);
-        if (i < ntiles) tile_sums[i] = carry + ex;
-        carry += total;
-    }
-    if (threadIdx.x == 0) tile_sums[ntiles] = carry;
-}
-
-// out[i] = exclusive prefix of in (may alias); out[n] = total
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(const uint32_t *in, size_t n,
-                                                              const uint32_t *__restrict__ tile_sums, uint32_t *out) {
-    __shared__ unsigned s_warp[33];
-    size_t base = (size_t)blockIdx.x * SCAN_TILE + (size_t)threadIdx.x * SCAN_ITEMS;
-    unsigned item[SCAN_ITEMS];
-    unsigned v = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        item[i] = (base + i < n) ? in[base + i] : 0u;
-        v += item[i];
-    }
-    unsigned total;
-    unsigned ex = block_excl_scan_1024(v, s_warp, total) + tile_sums[blockIdx.x];
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        if (base + i < n) out[base + i] = ex;
-        ex += item[i];
-    }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = tile_sums[gridDim.x];
-}
-
-// ---- the same three steps over up to four equally long arrays in one go (blockIdx.y = array): the canonical
-// stage scans the per-owner counters of all four dimensions, and twelve tiny launches cost more than the work
+// ---- single pass with decoupled look-back over up to four equally long arrays (blockIdx.y = array): every tile
+// publishes its aggregate, then sums the aggregates of its predecessors until it meets one whose inclusive prefix is
+// already known, publishes its own inclusive prefix and writes its outputs -- each input is read once and each output
+// written once (the three-launch form read the input twice and cost three launches per scan: six of the ~22 launches of
+// a pass).  Tiles take their number from a ticket counter, so a tile's predecessors always run or have run.
 struct Scan4 {
     const uint32_t *in[4];
     uint32_t *out[4];
-    uint32_t *sums[4];       // (ntiles + 1) each
+    unsigned long long *status[4];   // per tile: state << 32 | value (0: nothing yet, 1: aggregate, 2: inclusive prefix)
+    unsigned int *ticket;            // [4]
 };
 
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan4_tile_sums(Scan4 a, size_t n) {
-    __shared__ unsigned s_warp[33];
-    const uint32_t *in = a.in[blockIdx.y];
-    size_t base = (size_t)blockIdx.x * SCAN_TILE + (size_t)threadIdx.x * SCAN_ITEMS;
+enum : unsigned long long { SCAN_AGG = 1ull << 32, SCAN_INCL = 2ull << 32 };
+
+constexpr int LB_THREADS = 256;                       // look-back kernel: 256 threads x 16 items = the same 4096-element tile,
+constexpr int LB_ITEMS = SCAN_TILE / LB_THREADS;      // but eight resident blocks per SM and 16-byte loads / stores
+
+__global__ void __launch_bounds__(LB_THREADS) k_scan_lookback(Scan4 a, size_t n) {
+    __shared__ unsigned s_warp[LB_THREADS / 32 + 1];
+    __shared__ unsigned s_tile, s_prefix;
+    const int arr = blockIdx.y;
+    const uint32_t *in = a.in[arr];
+    uint32_t *out = a.out[arr];
+    unsigned long long *status = a.status[arr];
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket + arr, 1u);
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const size_t base = (size_t)tile * SCAN_TILE + (size_t)threadIdx.x * LB_ITEMS;
+    unsigned item[LB_ITEMS];
+    if (base + LB_ITEMS <= n) {                              // whole run inside the array: four 16-byte loads
+#pragma unroll
+        for (int q = 0; q < LB_ITEMS / 4; ++q) {
+            const uint4 v4 = *reinterpret_cast<const uint4 *>(in + base + 4 * q);
+            item[4 * q] = v4.x; item[4 * q + 1] = v4.y; item[4 * q + 2] = v4.z; item[4 * q + 3] = v4.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < LB_ITEMS; ++i) item[i] = (base + i < n) ? in[base + i] : 0u;
+    }
     unsigned v = 0;
 #pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i)
-        if (base + i < n) v += in[base + i];
-    unsigned total;
-    block_excl_scan_1024(v, s_warp, total);
-    if (threadIdx.x == 0) a.sums[blockIdx.y][blockIdx.x] = total;
-}
-
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan4_of_sums(Scan4 a, size_t ntiles) {
-    __shared__ unsigned s_warp[33];
-    uint32_t *tile_sums = a.sums[blockIdx.x];
-    unsigned carry = 0;
-    for (size_t base = 0; base < ntiles; base += SCAN_THREADS) {
-        size_t i = base + threadIdx.x;
-        unsigned v = i < ntiles ? tile_sums[i] : 0u;
-        unsigned total;
-        unsigned ex = block_excl_scan_1024(v, s_warp, total);
-        if (i < ntiles) tile_sums[i] = carry + ex;
-        carry += total;
-    }
-    if (threadIdx.x == 0) tile_sums[ntiles] = carry;
-}
-
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan4_apply(Scan4 a, size_t n) {
-    __shared__ unsigned s_warp[33];
-    const uint32_t *in = a.in[blockIdx.y];
-    uint32_t *out = a.out[blockIdx.y];
-    const uint32_t *tile_sums = a.sums[blockIdx.y];
-    size_t base = (size_t)blockIdx.x * SCAN_TILE + (size_t)threadIdx.x * SCAN_ITEMS;
-    unsigned item[SCAN_ITEMS];
-    unsigned v = 0;
+    for (int i = 0; i < LB_ITEMS; ++i) v += item[i];
+    // block scan: warp inclusive scans, then the eight warp totals by every thread
+    unsigned x = v;
 #pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        item[i] = (base + i < n) ? in[base + i] : 0u;
-        v += item[i];
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += t;
     }
-    unsigned total;
-    unsigned ex = block_excl_scan_1024(v, s_warp, total) + tile_sums[blockIdx.x];
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    unsigned ex = x - v, total = 0;
 #pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        if (base + i < n) out[base + i] = ex;
-        ex += item[i];
+    for (int k = 0; k < LB_THREADS / 32; ++k) {
+        const unsigned t = s_warp[k];
+        if (k < w) ex += t;
+        total += t;
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = tile_sums[gridDim.x];
+    if (threadIdx.x == 0) {
+        volatile unsigned long long *st = status;
+        st[tile] = (tile == 0 ? SCAN_INCL : SCAN_AGG) | total;
+        __threadfence();
+    }
+    if (w == 0) {                                            // warp 0 looks back, 32 predecessors at a time
+        unsigned prefix = 0;
+        if (tile > 0) {
+            volatile unsigned long long *st = status;
+            long long idx = (long long)tile - 1 - lane;
+            for (;;) {
+                unsigned long long sw = idx >= 0 ? st[idx] : SCAN_INCL;     // before the first tile: prefix 0, known
+                while (__any_sync(FULL, (sw >> 32) == 0ull)) sw = idx >= 0 ? st[idx] : SCAN_INCL;
+                const unsigned known = __ballot_sync(FULL, (sw >> 32) == 2ull);
+                const int stop = known ? __ffs(known) - 1 : 32;             // nearest predecessor with an inclusive prefix
+                unsigned add = lane <= stop ? (unsigned)(sw & 0xffffffffull) : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(FULL, add, o);
+                prefix += add;
+                if (known) break;
+                idx -= 32;
+            }
+            if (lane == 0) {
+                st[tile] = SCAN_INCL | (unsigned long long)(prefix + total);
+                __threadfence();
+            }
+        }
+        if (lane == 0) s_prefix = prefix;
+    }
+    __syncthreads();
+    ex += s_prefix;
+    if (base + LB_ITEMS <= n) {
+#pragma unroll
+        for (int q = 0; q < LB_ITEMS / 4; ++q) {
+            uint4 o4;
+            o4.x = ex; ex += item[4 * q];
+            o4.y = ex; ex += item[4 * q + 1];
+            o4.z = ex; ex += item[4 * q + 2];
+            o4.w = ex; ex += item[4 * q + 3];
+            *reinterpret_cast<uint4 *>(out + base + 4 * q) = o4;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < LB_ITEMS; ++i) {
+            if (base + i < n) out[base + i] = ex;
+            ex += item[i];
+        }
+    }
+    if (base <= n && n < base + LB_ITEMS) out[n] = ex;       // items at and beyond n count as zero: ex is the grand total
+                                                             // (the grid covers index n: ceil((n + 1) / SCAN_TILE) tiles)
 }
 
 // ---- small arrays (one protein: a few tiles) in ONE launch: a single block walks the tiles with a carry;
