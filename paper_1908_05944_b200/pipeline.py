@@ -279,10 +279,11 @@ class Engine:
         name = self.lib.axb_status_name(st).decode()
         raise AlphaxError(f"{name}: {rec.message or 'reported by another rank'}")
 
-    def _with_arena(self, n: int, cfg: PipelineConfig, call):
-        """Run ``call()`` (returns a status), growing the arena on AXB_ERR_ARENA."""
+    def _with_arena(self, n: int, alpha: float, call):
+        """Run ``call()`` (returns a status), growing the arena on AXB_ERR_ARENA: the library reports the size that
+        would have sufficed, so the second attempt normally fits."""
         if self.arena is None:
-            self._set_arena(self.lib.axb_arena_hint(n, float(cfg.alpha), 1.9))
+            self._set_arena(self.lib.axb_arena_hint(n, float(alpha), 1.9))
         for _ in range(12):
             st = call()
             if st != N.ERR_ARENA:
@@ -353,9 +354,9 @@ class Engine:
 
         with torch.cuda.device(self.device):
             self._bind_stream()
-            st = self._with_arena(n, cfg, run_pipelined if pipelined else run_two_calls)
+            st = self._with_arena(n, cfg.alpha, run_pipelined if pipelined else run_two_calls)
             if st == N.ERR_STATE and pipelined:
-                st = self._with_arena(n, cfg, run_two_calls)
+                st = self._with_arena(n, cfg.alpha, run_two_calls)
             if st != N.OK:
                 self._raise(st, cfg, centers, radii)
             self._collect_stage_ms()
@@ -374,7 +375,7 @@ class Engine:
         dev = f"cuda:{self.device}"
         with torch.cuda.device(self.device):
             self._bind_stream()
-            st = self._with_arena(n, cfg, lambda: self.lib.axb_compute(
+            st = self._with_arena(n, cfg.alpha, lambda: self.lib.axb_compute(
                 self.handle, n, centers.data_ptr(), radii.data_ptr(), C.byref(prm), counts))
             if st != N.OK:
                 self._raise(st, cfg, centers, radii)
@@ -576,7 +577,7 @@ class Engine:
 
         with torch.cuda.device(self.device):
             self._bind_stream()
-            st = self._with_arena(n, cfg, run)
+            st = self._with_arena(n, cfg.alpha, run)
         if st != N.OK:
             if raise_errors:
                 self._raise(st, cfg, centers, radii)
@@ -600,16 +601,13 @@ class Engine:
         out = torch.empty((m, k), dtype=torch.int64, device=rows.device)
         count = C.c_int64()
 
-        class _Cfg:      # only what _with_arena needs
-            alpha = 0.0
-
         def run():
             return self.lib.axb_merge_rows_range(self.handle, k, int(index_lo), int(n_index), rows.data_ptr() if m else None, m,
                                                  out.data_ptr() if m else None, C.byref(count))
 
         with torch.cuda.device(self.device):
             self._bind_stream()
-            st = self._with_arena(max(m, n_index - index_lo) // 8 + 1, _Cfg, run)
+            st = self._with_arena(max(m, n_index - index_lo) // 8 + 1, 0.0, run)
         if st != N.OK:
             raise AlphaxError(f"{self.lib.axb_status_name(st).decode()}: {self._message()}")
         out = out[: count.value]

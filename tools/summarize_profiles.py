@@ -24,7 +24,8 @@ KEYS = [("gpu__time_duration.sum", "gpu__time_duration"), ("dram__bytes_read.sum
         ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pipe_pct"),
         ("l1tex__t_sector_hit_rate.pct", "l1_hit_pct"), ("lts__t_sector_hit_rate.pct", "l2_hit_pct"),
         ("smsp__thread_inst_executed_per_inst_executed.ratio", "lanes_per_inst"),
-        ("smsp__issue_active.avg.pct", "issue_active_pct"),
+        ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_active_pct"),
+        ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "l1_data_pipe_pct"),
         ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall_long_sb"),
         ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "stall_short_sb"),
         ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall_wait"),
@@ -62,7 +63,7 @@ def main():
                 f.write(f"{k[:60]:60s} n={len(v):3d} avg_us={sum(v) / len(v):9.1f} share={100 * sum(v) / total:5.1f}%\n")
     # ---- per-kernel summary + traffic
     path = os.path.join(OUT, f"{tag}_ncu_full_raw.csv")
-    traffic = {}
+    traffic, pipes = {}, {}
     if os.path.exists(path):
         rows = list(csv.reader(open(path)))
         hdr, units = rows[0], rows[1]
@@ -83,8 +84,22 @@ def main():
                 f.write(f"{name}: " + ", ".join(parts) + "\n")
                 i0, i1 = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
                 traffic[name] = int(to_bytes(r[i0], units[i0]) + to_bytes(r[i1], units[i1]))
+
+                def val(key):
+                    try:
+                        return round(float(r[hdr.index(key)].replace(",", "")), 2)
+                    except Exception:
+                        return None
+                # what bench.py reports as roofline.secondary: the pipe / issue view of the kernel
+                pipes[name] = {"fp64_pipe_pct": val("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                               "issue_slots_pct": val("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                               "l1_shared_data_pipe_pct": val("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+                               "warps_active_pct": val("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                               "registers": val("launch__registers_per_thread"),
+                               "warp_instructions": val("smsp__inst_executed.sum")}
         traffic["_note"] = (f"dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes), ncu --set full, bench workload "
                             f"(1M atoms, alpha 0), capture {tag}")
+        traffic["_pipes"] = pipes
         json.dump(traffic, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
     # ---- per-kernel roofline table (alpha 0 from <tag>_ncu_full_raw.csv, alpha 1.4 from <tag>_a14_ncu_full_raw.csv)
     peak = 6548.2
