@@ -560,7 +560,7 @@ def spawn_ranks(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default 100; 3 for --impl reference)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--atoms-per-gpu", type=int, default=1_000_000)
@@ -576,9 +576,9 @@ def main():
                     help="b200 arm: size of the sample the real reference is timed on beside the GPU (10-30 s of CPU work)")
     ap.add_argument("--no-port", action="store_true", help="--impl reference: skip the C port beside the real package")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 3 if args.impl == "reference" else 100      # a pass of the CPU implementation takes seconds
     if args.impl == "reference":
-        if args.steps == 100:
-            args.steps = 3                  # default run: a few passes of the CPU implementation are minutes already
         bench_reference(args, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
         return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

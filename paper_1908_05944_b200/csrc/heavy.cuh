@@ -12,7 +12,7 @@
 namespace axb {
 
 constexpr int HEAVY_THREADS = 256;
-constexpr int HEAVY_MIN_DEG = 257;            // k_tri_tet3 handles up to 256 partners per generator
+constexpr int HEAVY_MIN_DEG = 257;            // k_tri_tet3<4> handles up to 64 * 4 = 256 partners per generator (its PCAP)
 
 __global__ void __launch_bounds__(256) k_list_heavy(int lo, int hi, const int *__restrict__ deg, int *__restrict__ list,
                                                     unsigned *__restrict__ n_heavy) {

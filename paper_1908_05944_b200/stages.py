@@ -167,7 +167,9 @@ def _current(handle, eng, key) -> bool:
 
 
 def _ensure_grid(grid, balls: Sequence[Ball], cfg: PipelineConfig, rebuild: bool = False):
-    """The engine with the grid of (balls, cfg) resident; rebuilt unless exactly that state is resident already."""
+    """The engine with the grid of (balls, cfg) resident; rebuilt unless exactly that state is resident already.
+    (`grid` is what the caller holds: the reference reads its geometry, here the geometry is a function of
+    (balls, cfg.alpha) and is recomputed on the device whenever the resident state is another one.)"""
     if len(balls) == 0:
         raise EmptyInput("at least one ball is required")
     eng = default_engine()
