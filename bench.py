@@ -61,7 +61,7 @@ def measured_peak():
 
 class ClockSampler:
     """SM clock and throttle reasons sampled DURING the timed region.  The region lasts only tens of
-    milliseconds, so NVML is polled from a thread every millisecond (nvidia-smi -lms 200 would see
+    milliseconds, so NVML is polled from a thread every 5 ms (more often steals the GIL from the timed loop) (nvidia-smi -lms 200 would see
     nothing); nvidia-smi is the fallback when pynvml is missing."""
 
     REASONS = ((0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"), (0x20, "sw_thermal_slowdown"), (0x4, "sw_power_cap"))
@@ -99,7 +99,7 @@ class ClockSampler:
                         self.bits |= int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(h))
                     except Exception:
                         pass
-                    time.sleep(0.001)
+                    time.sleep(0.005)
 
             self.thread = threading.Thread(target=loop, daemon=True)
             self.thread.start()

@@ -185,6 +185,20 @@ int axb_sync_check(axb_ctx *ctx);
  * grid_build -> potential(0,n) -> prune -> canonicalize. */
 int axb_compute(axb_ctx *ctx, int64_t n, const double *d_xyz, const double *d_radii,
                 const axb_params *params, int64_t counts[4]);
+/* axb_compute + axb_export in one call when the caller can bound the list lengths (e.g. from the previous call on a
+ * similar input: frames of a trajectory, repeated benchmark steps): the four int64 lists go straight into DEVICE buffers
+ * of capacity[d] rows, and nothing waits for the host between the pruning stage and the last row -- one stream sync at the
+ * very end instead of two plus the caller's allocation in between.  counts[d] = rows written.  AXB_ERR_STATE: a list was
+ * longer than its buffer (counts[] holds the lengths; nothing in the buffers is valid): call axb_compute + axb_export. */
+int axb_compute_into(axb_ctx *ctx, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *params,
+                     int64_t *d_vertices, int64_t *d_edges, int64_t *d_triangles, int64_t *d_tets,
+                     const int64_t capacity[4], int64_t counts[4]);
+/* The same in two calls, so that the caller can allocate the buffers WHILE the GPU works: `start` returns after the edge
+ * stage's sync with the triangle / tet and pruning kernels (two thirds of the step) still queued; `finish_into` queues
+ * the canonical lists into the buffers and ends with the one sync that reads the row counts. */
+int axb_compute_start(axb_ctx *ctx, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *params);
+int axb_compute_finish_into(axb_ctx *ctx, int64_t *d_vertices, int64_t *d_edges, int64_t *d_triangles, int64_t *d_tets,
+                            const int64_t capacity[4], int64_t counts[4]);
 /* One z-slab of a sharded run in one call (what one GPU of a multi-GPU job executes):
  * axb_grid_build_slab -> potential simplices of the lower halo and of the OWNED layers [z_own_lo, z_own_hi) ->
  * prune -> canonicalize.  The slab emits exactly the kept simplices whose minimum-rank vertex (their generator,

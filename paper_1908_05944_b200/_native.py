@@ -30,7 +30,7 @@ SYMBOLS = (
     "axb_potential_import_edges", "axb_potential_import_simplices", "axb_potential_tets_from_triangles", "axb_ac2_mask",
     "axb_sweep_prepare", "axb_sweep_prune",
     "axb_prune", "axb_canonicalize", "axb_export",
-    "axb_sync_check", "axb_compute", "axb_compute_host", "axb_export_host", "axb_compute_host_begin",
+    "axb_sync_check", "axb_compute", "axb_compute_into", "axb_compute_start", "axb_compute_finish_into", "axb_compute_host", "axb_export_host", "axb_compute_host_begin",
     "axb_compute_host_finish", "axb_last_d2h_bytes", "axb_stage_ms",
     "axb_kernel_launches", "axb_ortho_batch", "axb_format_complex",
 )
@@ -103,6 +103,9 @@ def load() -> C.CDLL:
         "axb_export": (C.c_int, [vp, vp, vp, vp, vp]),
         "axb_sync_check": (C.c_int, [vp]),
         "axb_compute": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params), pi64]),
+        "axb_compute_into": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params), vp, vp, vp, vp, pi64, pi64]),
+        "axb_compute_start": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params)]),
+        "axb_compute_finish_into": (C.c_int, [vp, vp, vp, vp, vp, pi64, pi64]),
         "axb_compute_host": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params), pi64]),
         "axb_export_host": (C.c_int, [vp, vp, vp, vp, vp]),
         "axb_compute_host_begin": (C.c_int, [vp, i64, vp, vp, C.POINTER(Params), pi64]),

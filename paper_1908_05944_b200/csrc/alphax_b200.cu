@@ -1109,13 +1109,72 @@ int run_canonicalize(axb_ctx *c, int64_t counts[4]) {
     P.tmp1 = c->tmp1; P.tmp2 = c->tmp2; P.tmp3 = c->tmp3; P.ctr = c->ctr;
     P.own_lo = c->slab_mode ? c->rank_lo : 0; P.own_hi = c->slab_mode ? c->rank_hi : 0x7fffffff;
     const unsigned grid = (unsigned)c->sm_count * 8u;
-    k_scatter_edges_tris<<<grid, 256, 0, c->stream>>>(P);
+    k_scatter_edges_tris<<<grid, 256, 0, c->stream>>>(P, 0xffffffffu, 0xffffffffu);
     LAUNCH_CHECK(c);
-    k_scatter_tets<<<grid, 256, 0, c->stream>>>(P);
+    k_scatter_tets<<<grid, 256, 0, c->stream>>>(P, c->k3_cap, 0xffffffffu);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_CANONICAL + 1)) != AXB_OK) return st;
     if (counts) for (int d = 0; d < 4; ++d) counts[d] = c->counts[d];
     c->state = S_CANON;
+    return AXB_OK;
+}
+
+// The same, and the four int64 lists straight into caller buffers of the given capacities, with NO host round trip in
+// between: buckets and emit kernels take their sizes from the device (clamped to the capacities), one sync at the very
+// end reads the totals and the flags.  A capacity that did not hold: sentinel AXB_ERR_ARENA + 1002 (nothing is valid).
+int run_canonicalize_into(axb_ctx *c, int64_t counts[4], int64_t *const d_out[4], const int64_t cap[4]) {
+    if (c->state < S_PRUNED) return fail(c, AXB_ERR_STATE, "axb_canonicalize before axb_prune");
+    const size_t n = (size_t)c->n;
+    int st;
+    ARENA(c, c->off1, uint32_t, n + 2);
+    ARENA(c, c->off2, uint32_t, n + 2);
+    ARENA(c, c->off3, uint32_t, n + 2);
+    ARENA(c, c->voff, uint32_t, n + 2);
+    {
+        const uint32_t *const in[4] = {c->cnt1, c->cnt2, c->cnt3, c->vkeep};
+        uint32_t *const out[4] = {c->off1, c->off2, c->off3, c->voff};
+        if ((st = device_scan4(c, in, n, out)) != AXB_OK) return st;
+    }
+    unsigned ucap[4];
+    for (int d = 0; d < 4; ++d) ucap[d] = (unsigned)std::min<int64_t>(std::max<int64_t>(cap[d], 0), 0xfffffff0ll);
+    ARENA(c, c->tmp1, int2, std::max(ucap[1], 1u));
+    ARENA(c, c->tmp2, int4, std::max(ucap[2], 1u));
+    ARENA(c, c->tmp3, int4, std::max(ucap[3], 1u));
+    CanonParams P;
+    P.n = (int)n; P.orig = c->orig; P.adj_off = c->adj_off; P.pe_u = c->pe_u; P.pe_v = c->pe_v; P.pe_cap = c->pe_cap;
+    P.W = c->W; P.trimask = c->trimask; P.eflag = c->eflag; P.k3 = c->k3;
+    P.cnt1 = c->cnt1; P.cnt2 = c->cnt2; P.cnt3 = c->cnt3; P.off1 = c->off1; P.off2 = c->off2; P.off3 = c->off3;
+    P.tmp1 = c->tmp1; P.tmp2 = c->tmp2; P.tmp3 = c->tmp3; P.ctr = c->ctr;
+    P.own_lo = 0; P.own_hi = 0x7fffffff;
+    const unsigned grid = (unsigned)c->sm_count * 8u;
+    k_scatter_edges_tris<<<grid, 256, 0, c->stream>>>(P, ucap[1], ucap[2]);
+    LAUNCH_CHECK(c);
+    k_scatter_tets<<<grid, 256, 0, c->stream>>>(P, c->k3_cap, ucap[3]);
+    LAUNCH_CHECK(c);
+    if ((st = mark_event(c, AXB_ST_CANONICAL + 1)) != AXB_OK) return st;
+    if ((st = mark_event(c, AXB_ST_COUNT)) != AXB_OK) return st;
+    k_emit_vertices<int64_t><<<blocks_for(n, 256), 256, 0, c->stream>>>((int)n, c->vkeep, c->voff, nullptr, d_out[0], ucap[0]);
+    LAUNCH_CHECK(c);
+    k_emit_edges<PlainOut<int64_t>><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, ucap[1], c->off1 + n, nullptr, PlainOut<int64_t>{d_out[1]}, c->ctr);
+    LAUNCH_CHECK(c);
+    k_emit_tris<PlainOut<int64_t>><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, ucap[2], c->off2 + n, nullptr, PlainOut<int64_t>{d_out[2]}, c->ctr);
+    LAUNCH_CHECK(c);
+    k_emit_tets<PlainOut<int64_t>><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, ucap[3], c->off3 + n, nullptr, PlainOut<int64_t>{d_out[3]}, c->ctr);
+    LAUNCH_CHECK(c);
+    if ((st = mark_event(c, AXB_ST_COUNT + 1)) != AXB_OK) return st;
+    k_publish_state<<<1, 32, 0, c->stream>>>(c->voff + n, c->off1 + n, c->off2 + n, c->off3 + n, c->ctr, c->h_dev->totals,
+                                             &c->h_dev->ctr);
+    LAUNCH_CHECK(c);
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->state = S_PRUNED;                                    // the buckets were consumed
+    if (c->h->ctr.n_pq > c->pq_cap || c->h->ctr.n_pt > c->pt_cap || c->h->ctr.n_k3 > c->k3_cap)
+        return AXB_ERR_ARENA + 1000;                       // a guessed list was too small: the caller redoes the stage
+    if ((st = check_run_flags(c)) != AXB_OK) return st;
+    c->n_pt = c->h->ctr.n_pt;
+    c->n_pq = c->h->ctr.n_pq;
+    for (int d = 0; d < 4; ++d) { c->counts[d] = c->h->totals[d]; counts[d] = c->counts[d]; }
+    for (int d = 0; d < 4; ++d)
+        if (c->counts[d] > (int64_t)ucap[d]) return AXB_ERR_ARENA + 1002;
     return AXB_OK;
 }
 
@@ -1447,7 +1506,7 @@ extern "C" int axb_export(axb_ctx *c, int64_t *d_v, int64_t *d_e, int64_t *d_t, 
     int st;
     if ((st = mark_event(c, AXB_ST_COUNT)) != AXB_OK) return st;
     if (d_v) {
-        k_emit_vertices<int64_t><<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>((int)c->n, c->vkeep, c->voff, c->gidx, d_v);
+        k_emit_vertices<int64_t><<<blocks_for((size_t)c->n, 256), 256, 0, c->stream>>>((int)c->n, c->vkeep, c->voff, c->gidx, d_v, 0xffffffffu);
         LAUNCH_CHECK(c);
     }
     if (d_e && c->counts[1]) {
@@ -1472,9 +1531,10 @@ extern "C" int axb_sync_check(axb_ctx *c) {
     return check_run_flags(c);
 }
 
-extern "C" int axb_compute(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *prm,
-                           int64_t counts[4]) {
-    if (!c) return AXB_ERR_BAD_ARG;
+namespace {
+// grid -> potential levels (optimistic list sizes, cull mode) -> pruning kernels, all queued; returns after the edge
+// stage's sync, with about two thirds of the step's GPU work still in flight
+int compute_start(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *prm) {
     c->defer_dup = true;
     int st = axb_grid_build(c, n, d_xyz, d_radii, prm);
     c->defer_dup = false;
@@ -1483,15 +1543,55 @@ extern "C" int axb_compute(axb_ctx *c, int64_t n, const double *d_xyz, const dou
     if (const char *e = getenv("AXB_CULL")) c->cull_mask = atoi(e);
     st = run_potential(c, 0, n, /*optimistic=*/true);
     if (st == AXB_OK) st = run_prune(c);
-    if (st == AXB_OK) st = run_canonicalize(c, counts);
-    if (st == AXB_ERR_ARENA + 1000) {                       // a guessed list size did not hold: redo the stage with exact sizes
+    if (st != AXB_OK) c->cull = false;
+    return st;
+}
+
+// canonical lists (bucketed for axb_export, or straight into caller buffers); redoes the triangle / tet stage with exact
+// sizes if a guessed list size did not hold
+int compute_finish(axb_ctx *c, int64_t counts[4], int64_t *const d_out[4], const int64_t cap[4]) {
+    auto canon = [&]() { return d_out ? run_canonicalize_into(c, counts, d_out, cap) : run_canonicalize(c, counts); };
+    int st = canon();
+    if (st == AXB_ERR_ARENA + 1000) {
         st = run_tri_tet_lists(c, false, /*redo=*/true);
         if (st == AXB_OK) st = run_prune(c);
-        if (st == AXB_OK) st = run_canonicalize(c, counts);
+        if (st == AXB_OK) st = canon();
         if (st == AXB_ERR_ARENA + 1000) st = fail(c, AXB_ERR_INTERNAL, "a potential list overflowed after it was sized exactly");
     }
+    if (st == AXB_ERR_ARENA + 1002)
+        st = fail(c, AXB_ERR_STATE, "a result list is longer than the caller's buffer (%lld %lld %lld %lld rows); use axb_compute + axb_export",
+                  (long long)counts[0], (long long)counts[1], (long long)counts[2], (long long)counts[3]);
     c->cull = false;
     return st;
+}
+}  // namespace
+
+extern "C" int axb_compute(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *prm,
+                           int64_t counts[4]) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    int st = compute_start(c, n, d_xyz, d_radii, prm);
+    return st != AXB_OK ? st : compute_finish(c, counts, nullptr, nullptr);
+}
+
+extern "C" int axb_compute_start(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *prm) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    return compute_start(c, n, d_xyz, d_radii, prm);
+}
+
+extern "C" int axb_compute_finish_into(axb_ctx *c, int64_t *d_v, int64_t *d_e, int64_t *d_t, int64_t *d_q,
+                                       const int64_t capacity[4], int64_t counts[4]) {
+    if (!c || !capacity || !counts || !d_v || !d_e || !d_t || !d_q) return AXB_ERR_BAD_ARG;
+    if (c->state != S_PRUNED || !c->cull) return fail(c, AXB_ERR_STATE, "axb_compute_finish_into needs axb_compute_start first");
+    int64_t *const out[4] = {d_v, d_e, d_t, d_q};
+    return compute_finish(c, counts, out, capacity);
+}
+
+extern "C" int axb_compute_into(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii, const axb_params *prm,
+                                int64_t *d_v, int64_t *d_e, int64_t *d_t, int64_t *d_q, const int64_t capacity[4],
+                                int64_t counts[4]) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    int st = compute_start(c, n, d_xyz, d_radii, prm);
+    return st != AXB_OK ? st : axb_compute_finish_into(c, d_v, d_e, d_t, d_q, capacity, counts);
 }
 
 extern "C" int axb_compute_slab(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_radii,
@@ -1787,7 +1887,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_event(c, AXB_ST_PRUNE_TETS + 1)) != AXB_OK) return st;
     if ((st = device_scan(c, c->cnt3, n, c->off3)) != AXB_OK) return st;
     if ((st = mark_total(3, c->off3 + n)) != AXB_OK) return st;
-    k_scatter_tets<<<grid, 256, 0, c->stream>>>(Q);
+    k_scatter_tets<<<grid, 256, 0, c->stream>>>(Q, c->k3_cap, (unsigned)std::min<int64_t>(c->host_cap[3], 0xfffffff0ll));
     LAUNCH_CHECK(c);
     if (p24) k_emit_tets<Packed24Out><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->host_cap[3], c->off3 + n, nullptr, Packed24Out{reinterpret_cast<unsigned char *>(d_out[3]), rows_shift[3]}, c->ctr);
     else k_emit_tets<PlainOut<int32_t>><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, (unsigned)c->host_cap[3], c->off3 + n, nullptr, PlainOut<int32_t>{d_out[3]}, c->ctr);
@@ -1825,7 +1925,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((st = mark_event(c, AXB_ST_PRUNE_VERTICES + 1)) != AXB_OK) return st;
     if ((st = device_scan(c, c->vkeep, n, c->voff)) != AXB_OK) return st;
     if ((st = mark_total(0, c->voff + n)) != AXB_OK) return st;
-    k_emit_vertices<int32_t><<<blocks_for(n, 256), 256, 0, c->stream>>>((int)n, c->vkeep, c->voff, nullptr, d_out[0]);
+    k_emit_vertices<int32_t><<<blocks_for(n, 256), 256, 0, c->stream>>>((int)n, c->vkeep, c->voff, nullptr, d_out[0], 0xffffffffu);
     LAUNCH_CHECK(c);
     if ((st = mark_ready(0)) != AXB_OK) return st;
     if ((st = mark_event(c, AXB_ST_CANONICAL + 1)) != AXB_OK) return st;

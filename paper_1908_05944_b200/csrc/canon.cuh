@@ -38,7 +38,9 @@ struct CanonParams {
 
 __device__ __forceinline__ bool canon_emits(const CanonParams &P, int gen) { return gen >= P.own_lo && gen < P.own_hi; }
 
-__global__ void __launch_bounds__(256) k_scatter_edges_tris(CanonParams P) {
+// cap1 / cap2: capacities of the bucket arrays (they are sized from the exact counts, or -- axb_compute_into -- from
+// what the caller's buffers hold, before the counts are known on the host)
+__global__ void __launch_bounds__(256) k_scatter_edges_tris(CanonParams P, unsigned cap1, unsigned cap2) {
     const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pe; e += gridDim.x * blockDim.x) {
         const int u = __ldg(P.pe_u + e), v = __ldg(P.pe_v + e);
@@ -46,8 +48,8 @@ __global__ void __launch_bounds__(256) k_scatter_edges_tris(CanonParams P) {
         const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + v);
         if (P.eflag[e]) {
             const int a = min(ou, ov), b = max(ou, ov);
-            const unsigned slot = atomicSub(P.cnt1 + a, 1u) - 1u;
-            P.tmp1[P.off1[a] + slot] = make_int2(a, b);
+            const unsigned pos = P.off1[a] + atomicSub(P.cnt1 + a, 1u) - 1u;
+            if (pos < cap1) P.tmp1[pos] = make_int2(a, b);
         }
         const unsigned bu = __ldg(P.adj_off + u);
         for (int w = 0; w < P.W; ++w) {
@@ -60,8 +62,8 @@ __global__ void __launch_bounds__(256) k_scatter_edges_tris(CanonParams P) {
                 if (a > b) { t = a; a = b; b = t; }
                 if (b > c) { t = b; b = c; c = t; }
                 if (a > b) { t = a; a = b; b = t; }
-                const unsigned slot = atomicSub(P.cnt2 + a, 1u) - 1u;
-                P.tmp2[P.off2[a] + slot] = make_int4(a, b, c, 0);
+                const unsigned pos = P.off2[a] + atomicSub(P.cnt2 + a, 1u) - 1u;
+                if (pos < cap2) P.tmp2[pos] = make_int4(a, b, c, 0);
             }
         }
     }
@@ -109,12 +111,12 @@ __global__ void __launch_bounds__(256) k_scatter_tris(CanonParams P, unsigned ca
     }
 }
 
-__global__ void __launch_bounds__(256) k_scatter_tets(CanonParams P) {
-    const unsigned n_k3 = P.ctr->n_k3;
+__global__ void __launch_bounds__(256) k_scatter_tets(CanonParams P, unsigned k3_cap, unsigned cap3) {
+    const unsigned n_k3 = min(P.ctr->n_k3, k3_cap);
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_k3; e += gridDim.x * blockDim.x) {
         const int4 r = P.k3[e];
-        const unsigned slot = atomicSub(P.cnt3 + r.x, 1u) - 1u;
-        P.tmp3[P.off3[r.x] + slot] = r;
+        const unsigned pos = P.off3[r.x] + atomicSub(P.cnt3 + r.x, 1u) - 1u;
+        if (pos < cap3) P.tmp3[pos] = r;
     }
 }
 
@@ -248,10 +250,10 @@ __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp,
 template <class OutT>
 __global__ void __launch_bounds__(256) k_emit_vertices(int n, const uint32_t *__restrict__ vkeep,
                                                        const uint32_t *__restrict__ voff,
-                                                       const int64_t *__restrict__ map, OutT *__restrict__ out) {
+                                                       const int64_t *__restrict__ map, OutT *__restrict__ out, unsigned cap) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    if (vkeep[i]) out[voff[i]] = (OutT)mapped(map, i);
+    if (vkeep[i] && voff[i] < cap) out[voff[i]] = (OutT)mapped(map, i);
 }
 
 // ---- merge of canonical row lists from several slabs / chunks (reference pipeline.py:611-614):

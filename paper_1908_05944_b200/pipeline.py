@@ -188,6 +188,7 @@ class Engine:
         self.last_stage_ms: dict = {}
         # identity of what is resident on the device, for the stage API's handles (stages.py): a new token for every
         # run that rebuilds the grid, a new id for every edge level / simplex level computed or imported
+        self._remembered_counts: dict = {}     # (n, configuration) -> row counts of the last result (compute_device)
         self.token = 0
         self.edge_id = 0
         self.simplex_id = 0
@@ -363,7 +364,13 @@ class Engine:
         return outs
 
     def compute_device(self, centers, radii, cfg: PipelineConfig):
-        """CUDA tensors in (centers (n,3) f64, radii (n,) f64), four CUDA int64 tensors out."""
+        """CUDA tensors in (centers (n,3) f64, radii (n,) f64), four CUDA int64 tensors out.
+
+        The first call for a problem shape runs ``axb_compute`` (which ends with the row counts on the host), allocates the
+        lists and runs ``axb_export``.  It remembers the counts; the next call with the same (n, configuration) --
+        another frame of a trajectory, the next step of a benchmark -- runs ``axb_compute_start``, allocates 2 % above
+        them while the GPU works, and ``axb_compute_finish_into``: nothing waits for the host between the pruning stage
+        and the last row.  If a list outgrew its buffer the first form is used again."""
         torch = self.torch
         centers = centers.to(dtype=torch.float64).contiguous().reshape(-1, 3)
         radii = radii.to(dtype=torch.float64).contiguous().reshape(-1)
@@ -373,25 +380,56 @@ class Engine:
         prm = self._params(cfg)
         counts = (C.c_int64 * 4)()
         dev = f"cuda:{self.device}"
+        shape_key = (n, float(cfg.alpha), float(cfg.tolerance.eps_abs), float(cfg.tolerance.eps_singular), bool(cfg.biomolecule_mode))
+
+        def carve(flat, rows):
+            outs, at = [], 0
+            for d in range(4):
+                part = flat[at:at + rows[d] * (d + 1)]
+                outs.append(part if d == 0 else part.view(rows[d], d + 1))
+                at += rows[d] * (d + 1)
+            return outs
+
         with torch.cuda.device(self.device):
             self._bind_stream()
+            last = self._remembered_counts.get(shape_key)
+            if last is not None:
+                cap = [min(n, last[0] + last[0] // 50 + 64)] + [last[d] + last[d] // 50 + 1024 for d in (1, 2, 3)]
+                ccap = (C.c_int64 * 4)(*cap)
+                bufs = None
+
+                def run_warm():
+                    nonlocal bufs
+                    st = self.lib.axb_compute_start(self.handle, n, centers.data_ptr(), radii.data_ptr(), C.byref(prm))
+                    if st != N.OK:
+                        return st
+                    if bufs is None:                   # allocated while the triangle / tet and pruning kernels run
+                        bufs = carve(torch.empty(sum(cap[d] * (d + 1) for d in range(4)), dtype=torch.int64, device=dev), cap)
+                    return self.lib.axb_compute_finish_into(self.handle, *(b.data_ptr() for b in bufs), ccap, counts)
+
+                st = self._with_arena(n, cfg.alpha, run_warm)
+                if st == N.OK:
+                    self._remembered_counts[shape_key] = tuple(int(v) for v in counts)
+                    self._collect_stage_ms()
+                    return [b[: int(counts[d])] for d, b in enumerate(bufs)]
+                if st != N.ERR_STATE:
+                    self._raise(st, cfg, centers, radii)
+                del bufs                                   # a list outgrew its buffer: the two-call form below
             st = self._with_arena(n, cfg.alpha, lambda: self.lib.axb_compute(
                 self.handle, n, centers.data_ptr(), radii.data_ptr(), C.byref(prm), counts))
             if st != N.OK:
                 self._raise(st, cfg, centers, radii)
             # one allocation for the four lists (the GPU idles while the host allocates: every call counts)
-            sizes = [int(counts[d]) * (d + 1) for d in range(4)]
-            flat = torch.empty(sum(sizes), dtype=torch.int64, device=dev)
-            outs, at = [], 0
-            for d in range(4):
-                part = flat[at:at + sizes[d]]
-                outs.append(part if d == 0 else part.view(int(counts[d]), d + 1))
-                at += sizes[d]
+            rows = [int(counts[d]) for d in range(4)]
+            outs = carve(torch.empty(sum(rows[d] * (d + 1) for d in range(4)), dtype=torch.int64, device=dev), rows)
             st = self.lib.axb_export(self.handle, *(o.data_ptr() if o.numel() else None for o in outs))
             if st == N.OK:
                 st = self.lib.axb_sync_check(self.handle)
             if st != N.OK:
                 self._raise(st, cfg, centers, radii)
+            self._remembered_counts[shape_key] = tuple(rows)
+            if len(self._remembered_counts) > 64:
+                self._remembered_counts.pop(next(iter(self._remembered_counts)))
             self._collect_stage_ms()
         return outs
 
