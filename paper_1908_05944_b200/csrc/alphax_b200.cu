@@ -131,6 +131,18 @@ struct axb_ctx {
     bool dup_pending = false;
     const int64_t *gidx = nullptr;        // slab mode: global ball index per local ball (ascending)
     // alpha sweep (sweep.cuh)
+    // What the edge stage found last time, per problem shape: with it the one-call path sizes the lists and picks the kernel
+    // shapes WITHOUT waiting for this run's edge counters, and verifies everything at its final sync (edges_assumed)
+    struct EdgeMemo {
+        bool valid = false;
+        int64_t n = 0, dims[3] = {0, 0, 0};
+        double alpha = 0, eps_abs = 0, eps_sing = 0;
+        int biomolecule = 0;
+        uint32_t n_pe = 0;
+        unsigned max_deg = 0;
+        unsigned long long pair_bound = 0;
+    } memo;
+    bool edges_assumed = false, allow_assume = false;
     cudaEvent_t side_go = nullptr, side_done = nullptr;     // hand-over to / from the second stream (early memset)
     bool prune_prealloc = false, side_pending = false;
     bool sweep_ready = false, sweep_on = false;
@@ -883,6 +895,33 @@ int run_edges(axb_ctx *c, int64_t lo, int64_t hi) {
     ARENA(c, c->deg, int, n);
     const size_t mark_pe = c->arena_used;
     uint64_t want = (uint64_t)16 * (uint64_t)(c->slab_mode ? n : ngen) + 4096;
+    c->edges_assumed = false;
+    {   // the same problem shape as last time (another frame, the next step of a sweep or a benchmark): no round trip
+        const axb_ctx::EdgeMemo &m = c->memo;
+        const bool same = c->allow_assume && m.valid && !c->slab_mode && lo == 0 && hi == c->n && m.n == c->n &&
+                          m.alpha == c->prm.alpha && m.eps_abs == c->prm.eps_abs && m.eps_sing == c->prm.eps_singular &&
+                          m.biomolecule == c->prm.biomolecule && m.dims[0] == c->ginfo.dims[0] && m.dims[1] == c->ginfo.dims[1] &&
+                          m.dims[2] == c->ginfo.dims[2] && m.max_deg + 8 <= 64;       // (one-word masks with room to grow)
+        if (same && !getenv("AXB_NO_MEMO")) {
+            c->pe_cap = m.n_pe + m.n_pe / 32 + 4096;
+            ARENA(c, c->pe_v, int, c->pe_cap);
+            ARENA(c, c->pe_u, int, c->pe_cap);
+            CUDA_TRY(c, cudaMemsetAsync(c->deg, 0, sizeof(int) * (size_t)n, c->stream));
+            EstParams P = est_params(c, 0);
+            if ((st = launch_edges(c, P, c->gen_lo, c->rank_hi)) != AXB_OK) return st;
+            if ((st = mark_event(c, AXB_ST_POT_EDGES + 1)) != AXB_OK) return st;
+            c->edges_assumed = true;
+            c->n_pe = c->pe_cap;                                        // upper bound until the final sync
+            c->h->ctr.pair_bound = m.pair_bound + m.pair_bound / 32 + 4096;   // sizes the triangle / tet lists, picks tile shapes
+            c->h->ctr.max_deg = m.max_deg;
+            c->W = 1;
+            c->heavy_list = nullptr;
+            c->heavy_scratch = nullptr;
+            c->mark_after_edges = c->arena_used;
+            c->state = S_EDGES;
+            return AXB_OK;
+        }
+    }
     for (int attempt = 0;; ++attempt) {
         if (want > 0xfffffff0ull) return fail(c, AXB_ERR_DENSITY, "more than 2^32 potential edges");
         c->arena_used = mark_pe;
@@ -1073,6 +1112,29 @@ int run_prune(axb_ctx *c) {
     return run_prune_lower(c);
 }
 
+// After the final sync of a run whose edge stage was not waited for: did the remembered sizes hold?  AXB_OK, an error
+// the reference raises before any triangle (duplicate centre), or the sentinel AXB_ERR_ARENA + 1001 (redo, exactly)
+int verify_assumed_edges(axb_ctx *c) {
+    if (!c->edges_assumed) return AXB_OK;
+    const Counters &k = c->h->ctr;
+    if (c->dup_pending) {
+        c->dup_pending = false;
+        if (k.dup_count) return report_duplicate(c, k.dup_count);
+    }
+    if ((k.overflow & (1u << 4)) || k.n_pe > c->pe_cap || k.max_deg > 64u || k.n_heavy) return AXB_ERR_ARENA + 1001;
+    return AXB_OK;
+}
+
+// what the next run with this problem shape may assume
+void remember_edges(axb_ctx *c) {
+    axb_ctx::EdgeMemo &m = c->memo;
+    m.valid = !c->slab_mode && c->rank_lo == 0 && c->rank_hi == (int)c->n;
+    m.n = c->n;
+    for (int a = 0; a < 3; ++a) m.dims[a] = c->ginfo.dims[a];
+    m.alpha = c->prm.alpha; m.eps_abs = c->prm.eps_abs; m.eps_sing = c->prm.eps_singular; m.biomolecule = c->prm.biomolecule;
+    m.n_pe = c->h->ctr.n_pe; m.max_deg = c->h->ctr.max_deg; m.pair_bound = c->h->ctr.pair_bound;
+}
+
 int run_canonicalize(axb_ctx *c, int64_t counts[4]) {
     if (c->state < S_PRUNED) return fail(c, AXB_ERR_STATE, "axb_canonicalize before axb_prune");
     const size_t n = (size_t)c->n;
@@ -1092,10 +1154,12 @@ int run_canonicalize(axb_ctx *c, int64_t counts[4]) {
                                              &c->h_dev->ctr);
     LAUNCH_CHECK(c);
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if ((st = verify_assumed_edges(c)) != AXB_OK) return st;
     // deferred checks of the optimistic potential stage
     if (c->h->ctr.n_pq > c->pq_cap || c->h->ctr.n_pt > c->pt_cap || c->h->ctr.n_k3 > c->k3_cap)
         return AXB_ERR_ARENA + 1000;                       // sentinel: a guessed buffer was too small, caller re-runs
     if ((st = check_run_flags(c)) != AXB_OK) return st;
+    c->n_pe = c->h->ctr.n_pe;
     c->n_pt = c->h->ctr.n_pt;
     c->n_pq = c->h->ctr.n_pq;
     for (int d = 0; d < 4; ++d) c->counts[d] = c->h->totals[d];
@@ -1167,9 +1231,11 @@ int run_canonicalize_into(axb_ctx *c, int64_t counts[4], int64_t *const d_out[4]
     LAUNCH_CHECK(c);
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->state = S_PRUNED;                                    // the buckets were consumed
+    if ((st = verify_assumed_edges(c)) != AXB_OK) return st;
     if (c->h->ctr.n_pq > c->pq_cap || c->h->ctr.n_pt > c->pt_cap || c->h->ctr.n_k3 > c->k3_cap)
         return AXB_ERR_ARENA + 1000;                       // a guessed list was too small: the caller redoes the stage
     if ((st = check_run_flags(c)) != AXB_OK) return st;
+    c->n_pe = c->h->ctr.n_pe;
     c->n_pt = c->h->ctr.n_pt;
     c->n_pq = c->h->ctr.n_pq;
     for (int d = 0; d < 4; ++d) { c->counts[d] = c->h->totals[d]; counts[d] = c->counts[d]; }
@@ -1541,7 +1607,9 @@ int compute_start(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_ra
     if (st != AXB_OK) return st;
     c->cull = true;
     if (const char *e = getenv("AXB_CULL")) c->cull_mask = atoi(e);
+    c->allow_assume = true;
     st = run_potential(c, 0, n, /*optimistic=*/true);
+    c->allow_assume = false;
     if (st == AXB_OK) st = run_prune(c);
     if (st != AXB_OK) c->cull = false;
     return st;
@@ -1552,12 +1620,21 @@ int compute_start(axb_ctx *c, int64_t n, const double *d_xyz, const double *d_ra
 int compute_finish(axb_ctx *c, int64_t counts[4], int64_t *const d_out[4], const int64_t cap[4]) {
     auto canon = [&]() { return d_out ? run_canonicalize_into(c, counts, d_out, cap) : run_canonicalize(c, counts); };
     int st = canon();
+    if (st == AXB_ERR_ARENA + 1001) {                       // the remembered edge-stage sizes did not hold: once more, waiting for them
+        c->memo.valid = false;
+        c->edges_assumed = false;
+        st = run_potential(c, 0, c->n, /*optimistic=*/true);
+        if (st == AXB_OK) st = run_prune(c);
+        if (st == AXB_OK) st = canon();
+    }
     if (st == AXB_ERR_ARENA + 1000) {
         st = run_tri_tet_lists(c, false, /*redo=*/true);
         if (st == AXB_OK) st = run_prune(c);
         if (st == AXB_OK) st = canon();
         if (st == AXB_ERR_ARENA + 1000) st = fail(c, AXB_ERR_INTERNAL, "a potential list overflowed after it was sized exactly");
     }
+    if (st == AXB_OK || st == AXB_ERR_ARENA + 1002) remember_edges(c);
+    else c->memo.valid = false;
     if (st == AXB_ERR_ARENA + 1002)
         st = fail(c, AXB_ERR_STATE, "a result list is longer than the caller's buffer (%lld %lld %lld %lld rows); use axb_compute + axb_export",
                   (long long)counts[0], (long long)counts[1], (long long)counts[2], (long long)counts[3]);

@@ -41,7 +41,9 @@ __device__ __forceinline__ bool canon_emits(const CanonParams &P, int gen) { ret
 // cap1 / cap2: capacities of the bucket arrays (they are sized from the exact counts, or -- axb_compute_into -- from
 // what the caller's buffers hold, before the counts are known on the host)
 __global__ void __launch_bounds__(256) k_scatter_edges_tris(CanonParams P, unsigned cap1, unsigned cap2) {
-    const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
+    if (P.ctr->n_pe > P.pe_cap) return;      // the edge list overflowed its buffer (only a run on remembered sizes gets this
+                                             // far: its tail was never written; the host redoes the run after its final sync)
+    const unsigned n_pe = P.ctr->n_pe;
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pe; e += gridDim.x * blockDim.x) {
         const int u = __ldg(P.pe_u + e), v = __ldg(P.pe_v + e);
         if (!canon_emits(P, u)) continue;
@@ -72,7 +74,9 @@ __global__ void __launch_bounds__(256) k_scatter_edges_tris(CanonParams P, unsig
 // one dimension at a time (the pipelined host path canonicalises a dimension as soon as it is final);
 // `cap` guards the bucket array, whose size was fixed before the exact count was known
 __global__ void __launch_bounds__(256) k_scatter_edges(CanonParams P, unsigned cap) {
-    const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
+    if (P.ctr->n_pe > P.pe_cap) return;      // the edge list overflowed its buffer (only a run on remembered sizes gets this
+                                             // far: its tail was never written; the host redoes the run after its final sync)
+    const unsigned n_pe = P.ctr->n_pe;
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pe; e += gridDim.x * blockDim.x) {
         if (!P.eflag[e]) continue;
         const int u = __ldg(P.pe_u + e);
@@ -85,7 +89,9 @@ __global__ void __launch_bounds__(256) k_scatter_edges(CanonParams P, unsigned c
 }
 
 __global__ void __launch_bounds__(256) k_scatter_tris(CanonParams P, unsigned cap) {
-    const unsigned n_pe = min(P.ctr->n_pe, P.pe_cap);
+    if (P.ctr->n_pe > P.pe_cap) return;      // the edge list overflowed its buffer (only a run on remembered sizes gets this
+                                             // far: its tail was never written; the host redoes the run after its final sync)
+    const unsigned n_pe = P.ctr->n_pe;
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pe; e += gridDim.x * blockDim.x) {
         unsigned long long any = 0ull;
         for (int w = 0; w < P.W; ++w) any |= P.trimask[(size_t)e * P.W + w];

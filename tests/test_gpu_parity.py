@@ -371,10 +371,45 @@ def test_optimistic_list_sizes_are_redone_when_they_do_not_hold(monkeypatch):
     cfg = ax.PipelineConfig(alpha=1.0)
     want = eng.compute_host(c, r, cfg)
     monkeypatch.setenv("AXB_TEST_SMALL_PQ", "1")
+    eng.arena.fill_(0x7F)
     dev = [t.cpu().numpy() for t in eng.compute_device(torch.as_tensor(c, device="cuda"), torch.as_tensor(r, device="cuda"), cfg)]
     host = eng.compute_host(c, r, cfg)
     for a, b, h in zip(want, dev, host):
         assert np.array_equal(a, b) and np.array_equal(a, h)
+
+
+def test_remembered_sizes_are_verified_and_redone():
+    """The device path remembers list lengths per problem shape (n, configuration, grid dims) and, on the next call with
+    that shape, neither waits for the edge counters nor for the row counts before it emits.  A different point set of the
+    same shape must still come out right: denser interior (more partners than remembered -> the run is redone exactly),
+    and a sparser one (the remembered sizes hold)."""
+    import torch
+
+    eng = ax.default_engine()
+    c, r = synth.jittered_lattice(30_000, 14)
+    r = r.copy()
+    r[0] = 1.9                                          # the same r_max, hence the same cell side, in every variant
+    mid = 0.5 * (c.min(axis=0) + c.max(axis=0))
+    keep = np.unique(np.concatenate([c.argmin(axis=0), c.argmax(axis=0)]))      # the balls that span the bounding box
+
+    def variant(scale):
+        v = mid + (c - mid) * scale
+        v[keep] = c[keep]
+        return np.ascontiguousarray(v)
+
+    cfg = ax.PipelineConfig(alpha=0.3, tolerance=ax.TolerancePolicy(1e-9, 1e-300))
+    launches = []
+    for scale in (1.0, 1.0, 0.8, 0.8, 1.15, 1.0):
+        v = variant(scale)
+        want = eng.compute_host(v, r, cfg)
+        eng.arena.fill_(0x7F)            # whatever a run on remembered sizes leaves unwritten must not be read either
+        before = eng.kernel_launches
+        got = [t.cpu().numpy() for t in eng.compute_device(torch.as_tensor(v, device="cuda"), torch.as_tensor(r, device="cuda"), cfg)]
+        launches.append(eng.kernel_launches - before)
+        for a, b in zip(want, got):
+            assert a.dtype == b.dtype == np.int64 and np.array_equal(a, b), scale
+    # the second call ran once (remembered sizes held), the third had to be redone (about twice the launches)
+    assert launches[2] > launches[1] + 8 and launches[3] <= launches[1] + 2
 
 
 def test_device_path_equals_host_path_and_is_deterministic():

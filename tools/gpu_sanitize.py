@@ -64,9 +64,27 @@ def main():
         good = all(np.array_equal(x, y) for x, y in zip((ks.vertices, ks.edges, ks.triangles, ks.tets), (ref.vertices, ref.edges, ref.triangles, ref.tets)))
         print(f"sweep alpha={a}", ks.counts(), "bit-exact" if good else "MISMATCH", flush=True)
         ok &= good
+    # the device path on remembered list lengths: same shape, denser / sparser point sets (held, redone, held)
+    import torch
+
+    eng = ax.default_engine()
+    c, r = synth.jittered_lattice(6000, 14)
+    r = r.copy()
+    r[0] = 1.9
+    mid = 0.5 * (c.min(axis=0) + c.max(axis=0))
+    keep = np.unique(np.concatenate([c.argmin(axis=0), c.argmax(axis=0)]))
+    cfg = ax.PipelineConfig(alpha=0.3, tolerance=ax.TolerancePolicy(1e-9, 1e-300))
+    for scale in (1.0, 1.0, 0.8, 0.8, 1.15):
+        v = mid + (c - mid) * scale
+        v[keep] = c[keep]
+        v = np.ascontiguousarray(v)
+        want = eng.compute_host(v, r, cfg)
+        got = [t.cpu().numpy() for t in eng.compute_device(torch.as_tensor(v, device="cuda"), torch.as_tensor(r, device="cuda"), cfg)]
+        good = all(np.array_equal(a, b) for a, b in zip(want, got))
+        print(f"remembered sizes, scale {scale}", [g.shape[0] for g in got], "bit-exact" if good else "MISMATCH", flush=True)
+        ok &= good
     c, r = synth.jittered_lattice(4000, 5)
     cfg = ax.PipelineConfig(alpha=0.5)
-    eng = ax.default_engine()
     single = eng.compute_host(c, r, cfg)
     merged, _ = sharding.compute_sharded_single_gpu(c, r, cfg, 3, eng)
     same = all(np.array_equal(m.cpu().numpy(), s) for m, s in zip(merged, single))
