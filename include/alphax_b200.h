@@ -167,6 +167,14 @@ int axb_ac2_mask(axb_ctx *ctx, int what, uint8_t *d_mask);
  * may be called for any number of alphas.  Results are bit-identical to independent runs at each alpha. */
 int axb_sweep_prepare(axb_ctx *ctx);
 int axb_sweep_prune(axb_ctx *ctx, double alpha);
+/* The sweep as a filtration, when its alphas are known up front (ascending, k <= 254, all <= the alpha of the
+ * preparation): axb_sweep_rank gives every listed simplex the index of the first alpha at which the reference keeps it
+ * -- own(s) = first index at which s is potential (if AC2(s)), a(s) = min(own(s), a(listed cofaces)), top-down, once --
+ * and axb_sweep_select(index) marks { s : a(s) <= index }: one threshold pass per alpha, then axb_canonicalize /
+ * axb_export.  AXB_ERR_STATE from axb_sweep_rank: a face of a listed tet is not a listed triangle (possible only by
+ * rounding); use axb_sweep_prune. */
+int axb_sweep_rank(axb_ctx *ctx, const double *alphas, int k);
+int axb_sweep_select(axb_ctx *ctx, int index);
 
 /* _prune_levels (pipeline.py:482-527): AC2 at every ortho-centre, inheritance of faces */
 int axb_prune(axb_ctx *ctx);

@@ -28,7 +28,7 @@ SYMBOLS = (
     "axb_grid_get_info", "axb_grid_export", "axb_potential",
     "axb_potential_counts", "axb_potential_export", "axb_potential_edges", "axb_potential_simplices",
     "axb_potential_import_edges", "axb_potential_import_simplices", "axb_potential_tets_from_triangles", "axb_ac2_mask",
-    "axb_sweep_prepare", "axb_sweep_prune",
+    "axb_sweep_prepare", "axb_sweep_prune", "axb_sweep_rank", "axb_sweep_select",
     "axb_prune", "axb_canonicalize", "axb_export",
     "axb_sync_check", "axb_compute", "axb_compute_into", "axb_compute_start", "axb_compute_finish_into", "axb_compute_host", "axb_export_host", "axb_compute_host_begin",
     "axb_compute_host_finish", "axb_last_d2h_bytes", "axb_stage_ms",
@@ -98,6 +98,8 @@ def load() -> C.CDLL:
         "axb_ac2_mask": (C.c_int, [vp, C.c_int, vp]),
         "axb_sweep_prepare": (C.c_int, [vp]),
         "axb_sweep_prune": (C.c_int, [vp, C.c_double]),
+        "axb_sweep_rank": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int]),
+        "axb_sweep_select": (C.c_int, [vp, C.c_int]),
         "axb_prune": (C.c_int, [vp]),
         "axb_canonicalize": (C.c_int, [vp, pi64]),
         "axb_export": (C.c_int, [vp, vp, vp, vp, vp]),

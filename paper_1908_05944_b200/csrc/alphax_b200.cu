@@ -145,7 +145,7 @@ struct axb_ctx {
     bool edges_assumed = false, allow_assume = false;
     cudaEvent_t side_go = nullptr, side_done = nullptr;     // hand-over to / from the second stream (early memset)
     bool prune_prealloc = false, side_pending = false;
-    bool sweep_ready = false, sweep_on = false;
+    bool sweep_ready = false, sweep_on = false, sweep_ranked = false;
     bool lists_complete = false;          // the resident potential lists were built without cull mode
     SweepArrays sw = {};
     size_t mark_after_sweep = 0;
@@ -718,6 +718,7 @@ int grid_build_common(axb_ctx *c, int64_t n, const double *d_xyz, const double *
     c->gidx = d_gidx;
     c->sweep_ready = false;
     c->sweep_on = false;
+    c->sweep_ranked = false;
     c->prune_prealloc = false;
     c->side_pending = false;
     if (n <= 0) return fail(c, AXB_ERR_EMPTY, "at least one ball is required");
@@ -1507,6 +1508,7 @@ extern "C" int axb_sweep_prepare(axb_ctx *c) {
     c->state = S_POTENTIAL;
     c->sweep_on = false;
     c->sweep_ready = false;
+    c->sweep_ranked = false;
     const unsigned E = c->n_pe, T = c->n_pt, Q = c->n_pq;
     // the lists end at pt_cap / pq_cap; everything the sweep keeps across alphas sits behind them
     ARENA(c, c->sw.esize, double, std::max(E, 1u));
@@ -1552,6 +1554,75 @@ extern "C" int axb_sweep_prune(axb_ctx *c, double alpha) {
     st = run_prune(c);
     c->sweep_on = false;
     return st;
+}
+
+extern "C" int axb_sweep_rank(axb_ctx *c, const double *alphas, int k) {
+    if (!c || !alphas || k < 1 || k > 254) return AXB_ERR_BAD_ARG;
+    if (!c->sweep_ready || c->state < S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_sweep_rank before axb_sweep_prepare");
+    for (int q = 0; q < k; ++q) {
+        if (!(alphas[q] <= c->prm.alpha) || (q && !(alphas[q - 1] < alphas[q])))
+            return fail(c, AXB_ERR_BAD_ARG, "alphas must ascend strictly and stay <= %.17g, the alpha the sweep was prepared for", c->prm.alpha);
+        if (c->prm.biomolecule && alphas[q] < 0.0) return fail(c, AXB_ERR_BAD_ARG, "biomolecule mode requires alpha >= 0");
+    }
+    c->state = S_POTENTIAL;
+    c->sweep_ranked = false;
+    c->arena_used = c->mark_after_sweep;
+    const unsigned E = c->n_pe, T = c->n_pt, Q = c->n_pq;
+    const size_t n = (size_t)c->n;
+    SweepArrays &S = c->sw;
+    double *d_alphas;
+    ARENA(c, d_alphas, double, (size_t)k);
+    ARENA(c, S.ke, unsigned char, std::max(E, 1u));
+    ARENA(c, S.ae, unsigned, std::max(E, 1u));
+    ARENA(c, S.at, unsigned, std::max(T, 1u));
+    ARENA(c, S.aq, unsigned, std::max(Q, 1u));
+    const size_t ones_from = c->arena_used;                   // "never" / "no triangle yet": all bits set
+    ARENA(c, S.av, unsigned, n + 1);
+    ARENA(c, S.row_first, unsigned, std::max(E, 1u));
+    const size_t ones_to = c->arena_used;
+    ARENA(c, S.ptmask, unsigned long long, (size_t)std::max(E, 1u) * c->W);
+    S.alphas = d_alphas;
+    S.K = k;
+    CUDA_TRY(c, cudaMemcpyAsync(d_alphas, alphas, sizeof(double) * (size_t)k, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->arena + ones_from, 0xff, ones_to - ones_from, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(S.ptmask, 0, sizeof(unsigned long long) * (size_t)std::max(E, 1u) * c->W, c->stream));
+    PruneParams P = prune_params(c);
+    if (E) { k_sweep_rank_edges<<<blocks_for(E, 256), 256, 0, c->stream>>>(P, E, S); LAUNCH_CHECK(c); }
+    if (T) {
+        k_sweep_tri_index<<<blocks_for(T, 256), 256, 0, c->stream>>>(P, T, S); LAUNCH_CHECK(c);
+        k_sweep_rank_tris<<<blocks_for(T, 256), 256, 0, c->stream>>>(P, T, S); LAUNCH_CHECK(c);
+    }
+    if (Q) { k_sweep_rank_tets<<<blocks_for(Q, 256), 256, 0, c->stream>>>(P, Q, S); LAUNCH_CHECK(c); }
+    if (T) { k_sweep_inherit_tris<<<blocks_for(T, 256), 256, 0, c->stream>>>(P, T, S); LAUNCH_CHECK(c); }
+    if (E) { k_sweep_inherit_edges<<<blocks_for(E, 256), 256, 0, c->stream>>>(P, E, S); LAUNCH_CHECK(c); }
+    k_sweep_rank_vertices<<<blocks_for(n, 256), 256, 0, c->stream>>>(P, S);
+    LAUNCH_CHECK(c);
+    int st = fetch_counters(c);
+    if (st != AXB_OK) return st;
+    if (c->h->ctr.overflow & (1u << 8))
+        return fail(c, AXB_ERR_STATE, "a face of a listed tetrahedron is not a listed triangle (rounding): use axb_sweep_prune for this input");
+    c->mark_after_sweep = c->arena_used;                      // the ranks stay; every alpha's kept state comes behind them
+    c->sweep_ranked = true;
+    return AXB_OK;
+}
+
+extern "C" int axb_sweep_select(axb_ctx *c, int index) {
+    if (!c) return AXB_ERR_BAD_ARG;
+    if (!c->sweep_ranked || c->state < S_POTENTIAL) return fail(c, AXB_ERR_STATE, "axb_sweep_select before axb_sweep_rank");
+    if (index < 0 || index >= c->sw.K) return fail(c, AXB_ERR_BAD_ARG, "alpha index out of range");
+    c->state = S_POTENTIAL;
+    c->arena_used = c->mark_after_sweep;
+    for (int i = AXB_ST_PRUNE_TETS; i < AXB_ST_COUNT + 2; ++i) c->ev_set[i] = false;
+    int st = mark_event(c, AXB_ST_PRUNE_TETS);
+    if (st != AXB_OK) return st;
+    if ((st = alloc_prune_arrays(c, false)) != AXB_OK) return st;
+    PruneParams P = prune_params(c);
+    k_sweep_select<<<(unsigned)c->sm_count * 8u, 256, 0, c->stream>>>(P, c->sw, (unsigned)index, c->n_pe, c->n_pt, c->n_pq);
+    LAUNCH_CHECK(c);
+    for (int i = AXB_ST_PRUNE_TETS + 1; i <= AXB_ST_PRUNE_VERTICES + 1; ++i)
+        if ((st = mark_event(c, i)) != AXB_OK) return st;
+    c->state = S_PRUNED;
+    return AXB_OK;
 }
 
 extern "C" int axb_prune(axb_ctx *c) {

@@ -580,9 +580,26 @@ class Engine:
         self.stage_grid(centers, radii, top)
         self.stage_potential()
         self._stage_call(self.lib.axb_sweep_prepare)
+        # the sweep as a filtration: every listed simplex gets the index of the first alpha that keeps it, once; each
+        # alpha is then one threshold pass (axb_sweep_select).  Fallback (a face of a listed tet that rounding left
+        # unlisted, or more than 254 alphas): the pruning kernels per alpha on the prepared arrays (axb_sweep_prune).
+        ranked = sorted(set(alphas))
+        use_ranks = len(ranked) <= 254
+        if use_ranks:
+            arr = (C.c_double * len(ranked))(*ranked)
+            with self.torch.cuda.device(self.device):
+                self._bind_stream(fresh=False)
+                st = self.lib.axb_sweep_rank(self.handle, arr, len(ranked))
+            if st == N.ERR_STATE:
+                use_ranks = False
+            else:
+                self._check(st, self._stage_cfg, *self._stage_inputs)
         out = []
         for a in alphas:
-            self._stage_call(self.lib.axb_sweep_prune, C.c_double(a))
+            if use_ranks:
+                self._stage_call(self.lib.axb_sweep_select, ranked.index(a))
+            else:
+                self._stage_call(self.lib.axb_sweep_prune, C.c_double(a))
             out.append(self.stage_export(self.stage_canonicalize()))
         return out
 
