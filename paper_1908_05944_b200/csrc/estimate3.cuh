@@ -103,12 +103,10 @@ struct T3Warp {
     int gdeg[C::GENS];
     unsigned gadj[C::GENS];
     int sp[C::GENS + 1];                       // slot prefix over the whole tile
+    unsigned short tl[C::TCAP];                // triangles of the round: slot i | slot j << 8 (filled in phase B while they fit)
     union {
-        unsigned wq[T3_WQCAP];                 // phase B: queue of reach-passing pairs (slot i | slot j << 16)
-        struct {
-            unsigned short tri_si[C::TCAP], tri_sj[C::TCAP];
-            int cpre[C::TCAP + 1];
-        } t;
+        unsigned short wq[T3_WQCAP];           // phase B: queue of reach-passing pairs (slot i | slot j << 8)
+        int cpre[C::TCAP + 1];                 // phases C, D: tet candidates per triangle, scanned
     } u;
     unsigned char sgen[C::SCAP], sli[C::SCAP];
     unsigned char ptab[C::PTAB];               // pair number -> first slot of the pair (phase B, flattened enumeration)
@@ -217,6 +215,18 @@ __device__ __forceinline__ bool dominated_by_partner3(const SW &S, int sb, int s
     return false;
 }
 
+// ordinal of triangle (s, sj) among its generator's triangles in (i, j) order, from the listed triangles of the tile
+// (error path only: the ordinal goes into the key that picks the first singular simplex, pipeline.py:475-477)
+__device__ __noinline__ unsigned listed_tri_ordinal(const unsigned short *tl, const unsigned char *sgen, int ntri, int s, int sj) {
+    const int g = sgen[s];
+    unsigned before = 0;
+    for (int y = 0; y < ntri; ++y) {
+        const int a = tl[y] & 0xff, b = tl[y] >> 8;
+        if (sgen[a] == g && (a < s || (a == s && b < sj))) ++before;
+    }
+    return before;
+}
+
 template <int W, int SHAPE>
 __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_tet3(EstParams P, int rank_lo, int rank_hi) {
     using C = T3Cfg<W, SHAPE>;
@@ -296,15 +306,21 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                 __syncwarp();
                 // ---- B: partner pairs.  Lane = partner slot i; round r pairs it with slot i + r of the same
                 // generator (np.triu_indices order is irrelevant here: results are bits).
+                int nt;                                                   // potential triangles of the sub-pass (warp-uniform)
+                bool listed;                                              // ... and all of them are in S.tl, in (i, j) order
                 {
-                    unsigned *wq = S.u.wq;
+                    unsigned short *wq = S.u.wq;
                     int qn = 0;                                           // warp-uniform queue fill
+                    nt = 0;
+                    listed = false;
                     auto solve_queue = [&](int count) {                    // dense ortho2 + ortho3 over wq[0..count)
                         for (int x0 = 0; x0 < count; x0 += 32) {
                             const int x = x0 + lane;
+                            bool tri = false;
+                            unsigned short pr = 0;
                             if (x < count) {
-                                const unsigned pr = wq[x];
-                                const int si = (int)(pr & 0xffffu), sj = (int)(pr >> 16);
+                                pr = wq[x];
+                                const int si = (int)(pr & 0xffu), sj = (int)(pr >> 8);
                                 const int g = S.sgen[si];
                                 const int i = S.sli[si], j = S.sli[sj];
                                 const int t = t0 + g;
@@ -320,6 +336,7 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                                         record_singular(P, make_err_key(ST_TRI, t, q), S.aorig[SCAP + g], S.aorig[si], S.aorig[sj], -1, 3);
                                     if (e3.size <= P.tol.lim_a) {                                        // pipeline.py:420
                                         set_bit(&S.T[si * W], j);
+                                        tri = true;
 #if T3_CULL_TRIS
                                         if (P.cull & 2) {
                                             const int sb = S.sp[g] - base;
@@ -329,6 +346,18 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
 #endif
                                     }
                                 }
+                            }
+                            // the triangle goes straight into the round's list (the queue is in (i, j) order, so is the
+                            // list) while the tile's triangles fit one round -- they nearly always do; the T rows are
+                            // only expanded otherwise
+                            const unsigned tm = __ballot_sync(FULL, tri);
+                            if (tm) {
+                                if (listed && nt + __popc(tm) <= TCAP) {
+                                    if (tri) S.tl[nt + __popc(tm & lanemask_lt())] = pr;
+                                } else {
+                                    listed = false;
+                                }
+                                nt += __popc(tm);
                             }
                         }
                         __syncwarp();
@@ -347,6 +376,7 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                         npairs = warp_scan_excl(S.rowpre, nslots);
                     }
                     if (C::FLAT && npairs <= C::PTAB) {
+                        listed = true;                      // pairs are queued in (i, j) order: so are the triangles
                         for (int s = lane; s < nslots; s += 32) {
                             const int pb = S.rowpre[s], pe = S.rowpre[s + 1];
                             for (int p = pb; p < pe; ++p) S.ptab[p] = (unsigned char)s;
@@ -364,7 +394,7 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                             const unsigned m = __ballot_sync(FULL, pass);
                             if (m) {
                                 if (qn + 32 > T3_WQCAP) { __syncwarp(); solve_queue(qn); qn = 0; }
-                                if (pass) wq[qn + __popc(m & lanemask_lt())] = (unsigned)si | ((unsigned)sj << 16);
+                                if (pass) wq[qn + __popc(m & lanemask_lt())] = (unsigned short)(si | (sj << 8));
                                 qn += __popc(m);
                                 __syncwarp();
                                 if (qn >= 32 * 8) { solve_queue(qn); qn = 0; }
@@ -392,7 +422,7 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                                 const unsigned m = __ballot_sync(FULL, pass);
                                 if (m) {
                                     if (qn + 32 > T3_WQCAP) { __syncwarp(); solve_queue(qn); qn = 0; }
-                                    if (pass) wq[qn + __popc(m & lanemask_lt())] = (unsigned)si | ((unsigned)sj << 16);
+                                    if (pass) wq[qn + __popc(m & lanemask_lt())] = (unsigned short)(si | (sj << 8));
                                     qn += __popc(m);
                                     __syncwarp();
                                     if (qn >= 32 * 8) { solve_queue(qn); qn = 0; }
@@ -404,14 +434,17 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                     solve_queue(qn);
                 }
                 // ---- C: triangle list of the tile
-                for (int s = lane; s < nslots; s += 32) {
-                    int c = 0;
+                if (!listed) {
+                    for (int s = lane; s < nslots; s += 32) {
+                        int c = 0;
 #pragma unroll
-                    for (int w = 0; w < W; ++w) c += __popcll(S.T[s * W + w]);
-                    S.rowpre[s] = c;
+                        for (int w = 0; w < W; ++w) c += __popcll(S.T[s * W + w]);
+                        S.rowpre[s] = c;
+                    }
+                    __syncwarp();
+                    warp_scan_excl(S.rowpre, nslots);
                 }
-                __syncwarp();
-                const int ntri = warp_scan_excl(S.rowpre, nslots);
+                const int ntri = nt;
                 // one contiguous run of the global triangle list per tile: the prune kernel that reads it
                 // then works on one neighbourhood at a time (L1 locality)
                 unsigned pt_base = 0;
@@ -419,6 +452,33 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                 pt_base = __shfl_sync(FULL, pt_base, 0);
                 for (int tc0 = 0; tc0 < ntri; tc0 += TCAP) {
                     const int ntc = min(TCAP, ntri - tc0);
+                    if (listed) {
+                        // lane = triangle: its tet candidates are the partners above j adjacent (in M) to both i and j:
+                        // rank[x] > rank_hi (pipeline.py:447)
+                        for (int x = lane; x < ntc; x += 32) {
+                            const int srow = S.tl[x] & 0xff, sj = S.tl[x] >> 8;
+                            const int j = S.sli[sj];
+                            int cnt = 0;
+#pragma unroll
+                            for (int w2 = 0; w2 < W; ++w2) {
+                                unsigned long long m = S.M[srow * W + w2] & S.M[sj * W + w2];
+                                const int lowbit = j + 1 - 64 * w2;
+                                if (lowbit >= 64) m = 0ull;
+                                else if (lowbit > 0) m &= ~0ull << lowbit;
+                                cnt += __popcll(m);
+                            }
+                            S.u.cpre[x] = cnt;
+                            const unsigned pos = pt_base + (unsigned)x;
+#if T3_CULL_TRIS
+                            const int dom = (int)((S.D[srow * W + (j >> 6)] >> (j & 63)) & 1ull);
+#else
+                            const int dom = 0;
+#endif
+                            if (pos < P.pt_cap)
+                                P.pt[pos] = make_int4(t0 + (int)S.sgen[srow], S.srank[srow], S.srank[sj],
+                                                      (int)S.sli[srow] | (j << 16) | (dom << 31));
+                        }
+                    } else
                     // every partner slot expands its own triangles (bits of its T row) into the round's list
                     for (int srow = lane; srow < nslots; srow += 32) {
                         int tt = S.rowpre[srow];
@@ -435,8 +495,7 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                                 ++tt;
                                 if (x < 0 || x >= ntc) continue;
                                 const int sj = sg + j;
-                                S.u.t.tri_si[x] = (unsigned short)srow;
-                                S.u.t.tri_sj[x] = (unsigned short)sj;
+                                S.tl[x] = (unsigned short)(srow | (sj << 8));
                                 // partners above j adjacent (in M) to both: rank[x] > rank_hi (pipeline.py:447)
                                 int cnt = 0;
 #pragma unroll
@@ -447,7 +506,7 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                                     else if (lowbit > 0) m &= ~0ull << lowbit;
                                     cnt += __popcll(m);
                                 }
-                                S.u.t.cpre[x] = cnt;
+                                S.u.cpre[x] = cnt;
                                 const unsigned pos = pt_base + (unsigned)(tc0 + x);
 #if T3_CULL_TRIS
                                 const int dom = (int)((S.D[srow * W + (j >> 6)] >> (j & 63)) & 1ull);
@@ -461,7 +520,7 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                         }
                     }
                     __syncwarp();
-                    const int ncand = warp_scan_excl(S.u.t.cpre, ntc);
+                    const int ncand = warp_scan_excl(S.u.cpre, ntc);
                     // ---- D: dense over tet candidates (pipeline.py:447-479)
                     for (int c0 = 0; c0 < ncand; c0 += 32) {
                         const int c = c0 + lane;
@@ -469,8 +528,8 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                         int4 er = make_int4(0, 0, 0, 0);
                         int el = 0;
                         if (c < ncand) {
-                            const int x = owner_of(S.u.t.cpre, ntc, c);
-                            const int s = S.u.t.tri_si[x], sj = S.u.t.tri_sj[x];
+                            const int x = owner_of(S.u.cpre, ntc, c);
+                            const int s = S.tl[x] & 0xff, sj = S.tl[x] >> 8;
                             const int j = S.sli[sj];
                             unsigned long long cm[W];
 #pragma unroll
@@ -481,14 +540,15 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                                 else if (lowbit > 0) m &= ~0ull << lowbit;
                                 cm[w] = m;
                             }
-                            const int k = nth_bit_multi<W>(cm, c - S.u.t.cpre[x]);
+                            const int k = nth_bit_multi<W>(cm, c - S.u.cpre[x]);
                             const int g = S.sgen[s];
                             const int sb = S.sp[g] - base;
                             const int sk = sb + k;
                             const int t = t0 + g;
                             const Ortho e4 = ortho_tet_s(S, SCAP + g, s, sj, sk, P.tol.eps_sing);        // pipeline.py:475-477
                             if (e4.singular) {
-                                const unsigned tri_ord = (unsigned)(tc0 + x - S.rowpre[sb]);             // ordinal among u's triangles
+                                const unsigned tri_ord = listed ? listed_tri_ordinal(S.tl, S.sgen, ntc, s, sj)
+                                                                : (unsigned)(tc0 + x - S.rowpre[sb]);    // ordinal among u's triangles
                                 record_singular(P, make_err_key(ST_TET, t, tet_ordinal(tri_ord, k)), S.aorig[SCAP + g],
                                                 S.aorig[s], S.aorig[sj], S.aorig[sk], 4);
                             }

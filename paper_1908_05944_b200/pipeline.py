@@ -180,12 +180,14 @@ class Engine:
         self.torch = torch
         self.lib = N.load()
         self.device = torch.cuda.current_device() if device is None else int(device)
+        self._device_str = f"cuda:{self.device}"
         self.handle = C.c_void_p()
         st = self.lib.axb_ctx_create(C.byref(self.handle), self.device)
         if st != N.OK:
             raise AlphaxError(f"axb_ctx_create failed: {self.lib.axb_status_name(st).decode()}")
         self.arena = None
-        self.last_stage_ms: dict = {}
+        self._stage_ms: dict = {}
+        self._stage_ms_stale = False
         # identity of what is resident on the device, for the stage API's handles (stages.py): a new token for every
         # run that rebuilds the grid, a new id for every edge level / simplex level computed or imported
         self._remembered_counts: dict = {}     # (n, configuration) -> row counts of the last result (compute_device)
@@ -295,9 +297,23 @@ class Engine:
         raise AlphaxError("scratch arena kept overflowing: " + self._message())
 
     def _collect_stage_ms(self):
-        ms = (C.c_float * len(N.STAGE_KEYS))()
-        self.lib.axb_stage_ms(self.handle, ms)
-        self.last_stage_ms = {k: float(ms[i]) for i, k in enumerate(N.STAGE_KEYS)}
+        # read on demand: ten cudaEventElapsedTime calls cost ~30 us, which the GPU would spend idle between two calls
+        self._stage_ms_stale = True
+
+    @property
+    def last_stage_ms(self) -> dict:
+        """Device time per stage of the most recent call (CUDA events; the reference's stage_times keys)."""
+        if self._stage_ms_stale:
+            ms = (C.c_float * len(N.STAGE_KEYS))()
+            self.lib.axb_stage_ms(self.handle, ms)
+            self._stage_ms = {k: float(ms[i]) for i, k in enumerate(N.STAGE_KEYS)}
+            self._stage_ms_stale = False
+        return self._stage_ms
+
+    @last_stage_ms.setter
+    def last_stage_ms(self, value: dict):
+        self._stage_ms = dict(value)
+        self._stage_ms_stale = False
 
     @property
     def kernel_launches(self) -> int:
@@ -372,14 +388,16 @@ class Engine:
         them while the GPU works, and ``axb_compute_finish_into``: nothing waits for the host between the pruning stage
         and the last row.  If a list outgrew its buffer the first form is used again."""
         torch = self.torch
-        centers = centers.to(dtype=torch.float64).contiguous().reshape(-1, 3)
-        radii = radii.to(dtype=torch.float64).contiguous().reshape(-1)
+        if centers.dtype != torch.float64 or centers.dim() != 2 or not centers.is_contiguous():
+            centers = centers.to(dtype=torch.float64).contiguous().reshape(-1, 3)
+        if radii.dtype != torch.float64 or radii.dim() != 1 or not radii.is_contiguous():
+            radii = radii.to(dtype=torch.float64).contiguous().reshape(-1)
         n = centers.shape[0]
         if n == 0:
             raise EmptyInput("at least one ball is required")
         prm = self._params(cfg)
         counts = (C.c_int64 * 4)()
-        dev = f"cuda:{self.device}"
+        dev = self._device_str
         shape_key = (n, float(cfg.alpha), float(cfg.tolerance.eps_abs), float(cfg.tolerance.eps_singular), bool(cfg.biomolecule_mode))
 
         def carve(flat, rows):
