@@ -187,7 +187,6 @@ __global__ void __launch_bounds__(EL_WARPS * 32, EL_MINB) k_edges(EstParams P, i
     extern __shared__ __align__(16) unsigned char s_raw_el[];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     ELWarp &S = reinterpret_cast<ELWarp *>(s_raw_el)[warp];
-    const GridView &g = P.g;
     unsigned max_deg = 0;
     unsigned long long pairs = 0;
 

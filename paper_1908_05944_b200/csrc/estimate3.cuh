@@ -51,13 +51,16 @@ constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved 
 #define T3H_TCAP 160
 #endif
 #ifndef T3H_MINB
-#define T3H_MINB 6
+#define T3H_MINB 8
 #endif
 
 // light tile shape.  The kernel's time goes with 1 / resident warps up to 16 per SM (4, 8, 12, 16 warps: 1.55, 0.82, 0.58,
 // 0.46 ms at 1M atoms, alpha 0) and flattens beyond: 24 warps need 80 registers (a few spilled values) and at most 9.4 KB
 // of shared memory per warp (96 partner slots, 160 triangles per round), worth another 3-5 % (0.445 ms; ncu r2c: issue
 // slots 48 -> 55 %, but long-scoreboard stalls per issue 1.7 -> 3.6)
+#ifndef T3L_GENS
+#define T3L_GENS 16
+#endif
 #ifndef T3L_SCAP
 #define T3L_SCAP 96
 #endif
@@ -65,20 +68,23 @@ constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved 
 #define T3L_TCAP 160
 #endif
 #ifndef T3L_MINB
-#define T3L_MINB 6
+#define T3L_MINB 5
 #endif
 #ifndef T3L_PTAB
 #define T3L_PTAB 640
 #endif
 // cull mode bit 1 (triangles flagged as dominated by a partner, AXB_CULL=2|3) needs a third bit matrix per warp; it
 // never paid, so it is compiled out unless asked for
+#ifndef T3_LIST_ALWAYS
+#define T3_LIST_ALWAYS 1
+#endif
 #ifndef T3_CULL_TRIS
 #define T3_CULL_TRIS 0
 #endif
 
 template <int W, int SHAPE>
 struct T3Cfg {
-    static constexpr int GENS = (W == 1 && SHAPE == T3_HEAVY) ? T3H_GENS : 16;                      // generators per warp tile (<= 16)
+    static constexpr int GENS = (W == 1 && SHAPE == T3_HEAVY) ? T3H_GENS : (W == 1 && SHAPE == T3_LIGHT) ? T3L_GENS : 16;   // generators per warp tile (<= 16)
     static constexpr int SCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_SCAP : SHAPE == T3_SMALL ? 128 : T3L_SCAP) : 256;   // partner slots per sub-pass (>= 64 * W)
     static constexpr int TCAP = W == 1 ? (SHAPE == T3_HEAVY ? T3H_TCAP : SHAPE == T3_SMALL ? 224 : T3L_TCAP) : 512;  // triangles per round
     static constexpr int MINB = W == 1 ? (SHAPE == T3_HEAVY ? T3H_MINB : SHAPE == T3_SMALL ? 4 : T3L_MINB) : 1;        // resident blocks per SM the registers must allow
@@ -375,63 +381,81 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                         __syncwarp();
                         npairs = warp_scan_excl(S.rowpre, nslots);
                     }
-                    if (C::FLAT && npairs <= C::PTAB) {
+                    // The enumeration is RESUMABLE and the queue is solved at ONE call site: five inlined copies of the two
+                    // ortho solves made the kernel 4,500 instructions long, and with every warp in a phase of its own
+                    // instruction fetch was the third largest stall reason (ncu r2g: no_instruction 1.6 per issue).
+                    const bool flat = C::FLAT && npairs <= C::PTAB;
+                    if (flat) {
                         listed = true;                      // pairs are queued in (i, j) order: so are the triangles
                         for (int s = lane; s < nslots; s += 32) {
                             const int pb = S.rowpre[s], pe = S.rowpre[s + 1];
                             for (int p = pb; p < pe; ++p) S.ptab[p] = (unsigned char)s;
                         }
                         __syncwarp();
-                        for (int p0 = 0; p0 < npairs; p0 += 32) {
-                            const int p = p0 + lane;
-                            bool pass = false;
-                            int si = 0, sj = 0;
-                            if (p < npairs) {
-                                si = S.ptab[p];
-                                sj = si + 1 + (p - S.rowpre[si]);
-                                pass = reach_pair(atom_at(S, si), S.sreach[si], atom_at(S, sj), S.sreach[sj]);   // pipeline.py:398-401
-                            }
-                            const unsigned m = __ballot_sync(FULL, pass);
-                            if (m) {
-                                if (qn + 32 > T3_WQCAP) { __syncwarp(); solve_queue(qn); qn = 0; }
+                    }
+                    int p0 = 0;                             // flat: next pair number
+                    int s0 = -32, r = 1, rounds = 0;        // slot by offset: group of 32 slots, round inside the group
+                    bool done = false;
+                    while (!done) {
+                        if (flat) {
+                            while (p0 < npairs && qn < 32 * 8) {
+                                const int p = p0 + lane;
+                                p0 += 32;
+                                bool pass = false;
+                                int si = 0, sj = 0;
+                                if (p < npairs) {
+                                    si = S.ptab[p];
+                                    sj = si + 1 + (p - S.rowpre[si]);
+                                    pass = reach_pair(atom_at(S, si), S.sreach[si], atom_at(S, sj), S.sreach[sj]);   // pipeline.py:398-401
+                                }
+                                const unsigned m = __ballot_sync(FULL, pass);
                                 if (pass) wq[qn + __popc(m & lanemask_lt())] = (unsigned short)(si | (sj << 8));
                                 qn += __popc(m);
-                                __syncwarp();
-                                if (qn >= 32 * 8) { solve_queue(qn); qn = 0; }
                             }
-                        }
-                    } else {
-                        for (int s0 = 0; s0 < nslots; s0 += 32) {
-                            const int si = s0 + lane;
+                            done = p0 >= npairs;
+                        } else {
+                            // lane = slot i of the group, round r pairs it with slot i + r (its record is re-read after a
+                            // solve instead of being kept alive across it)
                             int more = 0;
                             Atom av;
                             double rv = 0.0;
                             av.x = av.y = av.z = av.r2 = 0.0;
-                            if (si < nslots) {
+                            const int si = s0 + lane;
+                            if (s0 >= 0 && si < nslots) {
                                 more = S.gdeg[S.sgen[si]] - 1 - (int)S.sli[si];   // partners after slot i in its generator
                                 av = atom_at(S, si);
                                 rv = S.sreach[si];
                             }
-                            int rounds = more;
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) rounds = max(rounds, __shfl_xor_sync(FULL, rounds, o));
-                            for (int r = 1; r <= rounds; ++r) {
+                            while (qn < 32 * 8) {
+                                if (r > rounds) {           // next group
+                                    s0 += 32;
+                                    if (s0 >= nslots) { done = true; break; }
+                                    break;                  // (re-enter with the new group's records)
+                                }
                                 bool pass = false;
                                 const int sj = si + r;
                                 if (r <= more) pass = reach_pair(av, rv, atom_at(S, sj), S.sreach[sj]);   // pipeline.py:398-401
+                                ++r;
                                 const unsigned m = __ballot_sync(FULL, pass);
-                                if (m) {
-                                    if (qn + 32 > T3_WQCAP) { __syncwarp(); solve_queue(qn); qn = 0; }
-                                    if (pass) wq[qn + __popc(m & lanemask_lt())] = (unsigned short)(si | (sj << 8));
-                                    qn += __popc(m);
-                                    __syncwarp();
-                                    if (qn >= 32 * 8) { solve_queue(qn); qn = 0; }
-                                }
+                                if (pass) wq[qn + __popc(m & lanemask_lt())] = (unsigned short)(si | (sj << 8));
+                                qn += __popc(m);
+                            }
+                            if (!done && r > rounds && qn < 32 * 8) {
+                                // the new group: how many rounds it needs
+                                int mr = 0;
+                                const int sn = s0 + lane;
+                                if (sn < nslots) mr = S.gdeg[S.sgen[sn]] - 1 - (int)S.sli[sn];
+#pragma unroll
+                                for (int o = 16; o > 0; o >>= 1) mr = max(mr, __shfl_xor_sync(FULL, mr, o));
+                                rounds = mr;
+                                r = 1;
+                                continue;                   // nothing to solve yet
                             }
                         }
+                        __syncwarp();
+                        solve_queue(qn);
+                        qn = 0;
                     }
-                    __syncwarp();
-                    solve_queue(qn);
                 }
                 // ---- C: triangle list of the tile
                 if (!listed) {
