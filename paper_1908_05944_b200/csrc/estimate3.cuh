@@ -31,9 +31,9 @@ namespace axb {
 #endif
 constexpr int T3_WARPS = T3_WARPS_V;      // warps per block (each one is independent)
 // Tile shapes (template parameter SHAPE): the light shape packs lanes best when a generator has ~11 partner
-// pairs (alpha = 0); the heavy shape shrinks the tile (6 generators) so that 24 instead of 16 warps fit an SM (80 registers,
-// ~7 KB of shared memory per warp) -- measured 8-10 % faster once generators have 40+ pairs (alpha = 1.4,
-// dense cores), 9 % slower at alpha = 0.
+// pairs (alpha = 0); the heavy shape shrinks the tile (6 generators, ~6 KB of shared memory per warp) so that 32 warps fit
+// an SM at 64 registers -- faster once generators have 40+ pairs (alpha = 1.4, dense cores; 1M atoms, alpha 1.4: 5 / 6 / 7 /
+// 8 blocks per SM = 2.31 / 2.19 / 2.12 / 2.04 ms), slower at alpha = 0.
 enum { T3_LIGHT = 0, T3_HEAVY = 1, T3_SMALL = 2 };   // T3_SMALL: the light algorithm at 16 warps per SM, no spilled values
                                                      // (few tiles per warp: nothing hides a slower tile)
 constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved as soon as 256 are waiting)
@@ -55,9 +55,10 @@ constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved 
 #endif
 
 // light tile shape.  The kernel's time goes with 1 / resident warps up to 16 per SM (4, 8, 12, 16 warps: 1.55, 0.82, 0.58,
-// 0.46 ms at 1M atoms, alpha 0) and flattens beyond: 24 warps need 80 registers (a few spilled values) and at most 9.4 KB
-// of shared memory per warp (96 partner slots, 160 triangles per round), worth another 3-5 % (0.445 ms; ncu r2c: issue
-// slots 48 -> 55 %, but long-scoreboard stalls per issue 1.7 -> 3.6)
+// 0.46 ms at 1M atoms, alpha 0) and flattens beyond: with the single solve site (see phase B) 20 warps at 96 registers are
+// the optimum (0.384 ms; 16 warps 0.415, 24 warps at 80 registers 0.46: the flat pair path spills there); at most 9.4 KB
+// of shared memory per warp (96 partner slots, 160 triangles per round).  Smaller tiles for more warps lose (12
+// generators at 24 warps 0.457 ms, 8 at 32 warps 0.489 ms).
 #ifndef T3L_GENS
 #define T3L_GENS 16
 #endif
@@ -75,9 +76,6 @@ constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved 
 #endif
 // cull mode bit 1 (triangles flagged as dominated by a partner, AXB_CULL=2|3) needs a third bit matrix per warp; it
 // never paid, so it is compiled out unless asked for
-#ifndef T3_LIST_ALWAYS
-#define T3_LIST_ALWAYS 1
-#endif
 #ifndef T3_CULL_TRIS
 #define T3_CULL_TRIS 0
 #endif
