@@ -327,10 +327,22 @@ __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__re
     }
     // only the non-empty rows are parked (trimming and sparse regions leave several of the nine empty), so the
     // walk switches rows exactly once per row that holds balls
+    // ... and in the order of their distance from the centre's own row: a dominating ball is most likely a close one, and
+    // the walk ends at the first (at alpha = 1.4 two thirds of the potential tets and nearly all free triangles are dominated)
     int nr = 0;
+#ifndef AC2_CENTER_FIRST
+#define AC2_CENTER_FIRST 1
+#endif
+#if AC2_CENTER_FIRST
+    constexpr int ORD[9] = {4, 3, 5, 1, 7, 0, 2, 6, 8};
+#else
+    constexpr int ORD[9] = {0, 1, 2, 3, 4, 5, 6, 7, 8};
+#endif
 #pragma unroll
-    for (int k = 0; k < 9; ++k)
+    for (int q = 0; q < 9; ++q) {
+        const int k = ORD[q];
         if (er[k] > sr[k]) { rows[nr * stride] = make_int2(sr[k], er[k]); ++nr; }
+    }
     // flattened walk over the balls of all rows
     int r = -1, pos = 0, end = 0;
     auto next = [&]() -> int {
