@@ -1212,20 +1212,18 @@ int run_canonicalize_into(axb_ctx *c, int64_t counts[4], int64_t *const d_out[4]
     P.tmp1 = c->tmp1; P.tmp2 = c->tmp2; P.tmp3 = c->tmp3; P.ctr = c->ctr;
     P.own_lo = 0; P.own_hi = 0x7fffffff;
     const unsigned grid = (unsigned)c->sm_count * 8u;
-    k_scatter_edges_tris<<<grid, 256, 0, c->stream>>>(P, ucap[1], ucap[2]);
-    LAUNCH_CHECK(c);
-    k_scatter_tets<<<grid, 256, 0, c->stream>>>(P, c->k3_cap, ucap[3]);
+    k_scatter_edges_tris<<<dim3(grid, 2), 256, 0, c->stream>>>(P, ucap[1], ucap[2], c->k3_cap, ucap[3]);     // + the tets
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_CANONICAL + 1)) != AXB_OK) return st;
     if ((st = mark_event(c, AXB_ST_COUNT)) != AXB_OK) return st;
-    k_emit_vertices<int64_t><<<blocks_for(n, 256), 256, 0, c->stream>>>((int)n, c->vkeep, c->voff, nullptr, d_out[0], ucap[0]);
-    LAUNCH_CHECK(c);
-    k_emit_edges<PlainOut<int64_t>><<<grid, 256, 0, c->stream>>>(c->tmp1, c->off1, ucap[1], c->off1 + n, nullptr, PlainOut<int64_t>{d_out[1]}, c->ctr);
-    LAUNCH_CHECK(c);
-    k_emit_tris<PlainOut<int64_t>><<<grid, 256, 0, c->stream>>>(c->tmp2, c->off2, ucap[2], c->off2 + n, nullptr, PlainOut<int64_t>{d_out[2]}, c->ctr);
-    LAUNCH_CHECK(c);
-    k_emit_tets<PlainOut<int64_t>><<<grid, 256, 0, c->stream>>>(c->tmp3, c->off3, ucap[3], c->off3 + n, nullptr, PlainOut<int64_t>{d_out[3]}, c->ctr);
-    LAUNCH_CHECK(c);
+    {
+        EmitAll E;
+        E.n = (int)n; E.vkeep = c->vkeep; E.voff = c->voff; E.tmp1 = c->tmp1; E.tmp2 = c->tmp2; E.tmp3 = c->tmp3;
+        E.off1 = c->off1; E.off2 = c->off2; E.off3 = c->off3; E.ctr = c->ctr;
+        for (int d = 0; d < 4; ++d) { E.cap[d] = ucap[d]; E.out[d] = d_out[d]; }
+        k_emit_all<<<dim3(grid, 4), 256, 0, c->stream>>>(E);
+        LAUNCH_CHECK(c);
+    }
     if ((st = mark_event(c, AXB_ST_COUNT + 1)) != AXB_OK) return st;
     k_publish_state<<<1, 32, 0, c->stream>>>(c->voff + n, c->off1 + n, c->off2 + n, c->off3 + n, c->ctr, c->h_dev->totals,
                                              &c->h_dev->ctr);

@@ -40,13 +40,82 @@ __device__ __forceinline__ bool canon_emits(const CanonParams &P, int gen) { ret
 
 // cap1 / cap2: capacities of the bucket arrays (they are sized from the exact counts, or -- axb_compute_into -- from
 // what the caller's buffers hold, before the counts are known on the host)
-__global__ void __launch_bounds__(256) k_scatter_edges_tris(CanonParams P, unsigned cap1, unsigned cap2) {
+#ifndef SCATTER_MLP
+#define SCATTER_MLP 1
+#endif
+__device__ __forceinline__ void scatter_tets_rows(const CanonParams &P, unsigned k3_cap, unsigned cap3) {
+    const unsigned n_k3 = min(P.ctr->n_k3, k3_cap);
+    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_k3; e += gridDim.x * blockDim.x) {
+        const int4 r = P.k3[e];
+        const unsigned pos = P.off3[r.x] + atomicSub(P.cnt3 + r.x, 1u) - 1u;
+        if (pos < cap3) P.tmp3[pos] = r;
+    }
+}
+
+// (launched with gridDim.y == 2, the second layer of blocks drops the kept tets into their buckets: one launch for the
+// three lists; k3_cap / cap3 are ignored otherwise)
+__global__ void __launch_bounds__(256) k_scatter_edges_tris(CanonParams P, unsigned cap1, unsigned cap2, unsigned k3_cap = 0,
+                                                            unsigned cap3 = 0) {
+    if (blockIdx.y == 1) { scatter_tets_rows(P, k3_cap, cap3); return; }
     if (P.ctr->n_pe > P.pe_cap) return;      // the edge list overflowed its buffer (only a run on remembered sizes gets this
                                              // far: its tail was never written; the host redoes the run after its final sync)
     const unsigned n_pe = P.ctr->n_pe;
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_pe; e += gridDim.x * blockDim.x) {
         const int u = __ldg(P.pe_u + e), v = __ldg(P.pe_v + e);
         if (!canon_emits(P, u)) continue;
+#if SCATTER_MLP
+        // A warp issues in order, so every level of the dependent chain (list entry -> ball indices -> bucket slot -> row)
+        // is issued for the edge AND up to three triangles of its row before anything waits for the previous level:
+        // the chain is six round trips deep whatever the row holds (it was four per triangle on top of the edge's four).
+        if (P.W == 1) {
+            unsigned flag = P.eflag[e];
+            unsigned long long m = P.trimask[e];
+            if (!flag && !m) continue;
+            const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + v);
+            const unsigned bu = __ldg(P.adj_off + u);
+            const int ea = min(ou, ov), eb = max(ou, ov);
+            do {
+                int j[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    j[k] = -1;
+                    if (m) { j[k] = __ffsll((long long)m) - 1; m &= m - 1; }
+                }
+                int pw[3], ow[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) pw[k] = j[k] >= 0 ? __ldg(P.pe_v + bu + j[k]) : 0;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) ow[k] = j[k] >= 0 ? __ldg(P.orig + pw[k]) : 0;
+                // owners, bucket offsets and slots: every load and atomic issued before the first result is needed
+                unsigned es = 0, eo = 0;
+                if (flag) { eo = P.off1[ea]; es = atomicSub(P.cnt1 + ea, 1u); }
+                int ta[3], tb[3], tc[3];
+                unsigned tsl[3], to[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    int a = ou, b = ov, c = ow[k], t;
+                    if (a > b) { t = a; a = b; b = t; }
+                    if (b > c) { t = b; b = c; c = t; }
+                    if (a > b) { t = a; a = b; b = t; }
+                    ta[k] = a; tb[k] = b; tc[k] = c;
+                    tsl[k] = 0; to[k] = 0;
+                    if (j[k] >= 0) { to[k] = P.off2[a]; tsl[k] = atomicSub(P.cnt2 + a, 1u); }
+                }
+                if (flag) {
+                    const unsigned pos = eo + es - 1u;
+                    if (pos < cap1) P.tmp1[pos] = make_int2(ea, eb);
+                }
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    if (j[k] >= 0) {
+                        const unsigned pos = to[k] + tsl[k] - 1u;
+                        if (pos < cap2) P.tmp2[pos] = make_int4(ta[k], tb[k], tc[k], 0);
+                    }
+                flag = 0u;                  // (more than three triangles in the row: another round, without the edge)
+            } while (m);
+            continue;
+        }
+#endif
         const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + v);
         if (P.eflag[e]) {
             const int a = min(ou, ov), b = max(ou, ov);
@@ -118,12 +187,7 @@ __global__ void __launch_bounds__(256) k_scatter_tris(CanonParams P, unsigned ca
 }
 
 __global__ void __launch_bounds__(256) k_scatter_tets(CanonParams P, unsigned k3_cap, unsigned cap3) {
-    const unsigned n_k3 = min(P.ctr->n_k3, k3_cap);
-    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n_k3; e += gridDim.x * blockDim.x) {
-        const int4 r = P.k3[e];
-        const unsigned pos = P.off3[r.x] + atomicSub(P.cnt3 + r.x, 1u) - 1u;
-        if (pos < cap3) P.tmp3[pos] = r;
-    }
+    scatter_tets_rows(P, k3_cap, cap3);
 }
 
 // One thread per bucket entry: its position inside the bucket is the number of
@@ -169,9 +233,9 @@ struct Packed24Out {
 // launch without knowing the count on the host; `total` then carries the capacity the buffers were sized for.
 // SKIP0: write only the columns after the owner (the host rebuilds column 0 from the offsets)
 template <class Out, bool SKIP0 = false>
-__global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp, const uint32_t *__restrict__ off,
-                                                    unsigned total, const uint32_t *__restrict__ total_dev,
-                                                    const int64_t *__restrict__ map, Out out, Counters *ctr) {
+__device__ __forceinline__ void emit_edges_rows(const int2 *__restrict__ tmp, const uint32_t *__restrict__ off,
+                                                unsigned total, const uint32_t *__restrict__ total_dev,
+                                                const int64_t *__restrict__ map, Out out, Counters *ctr) {
     if (total_dev) {                        // device-side row count; `total` then is the CAPACITY of tmp / out: when the
         const unsigned cap = total;         // count exceeds it the host falls back (AXB_ERR_STATE) and nothing is read
         total = *total_dev;
@@ -197,9 +261,16 @@ __global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp
 }
 
 template <class Out, bool SKIP0 = false>
-__global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
-                                                   unsigned total, const uint32_t *__restrict__ total_dev,
-                                                   const int64_t *__restrict__ map, Out out, Counters *ctr) {
+__global__ void __launch_bounds__(256) k_emit_edges(const int2 *__restrict__ tmp, const uint32_t *__restrict__ off,
+                                                    unsigned total, const uint32_t *__restrict__ total_dev,
+                                                    const int64_t *__restrict__ map, Out out, Counters *ctr) {
+    emit_edges_rows<Out, SKIP0>(tmp, off, total, total_dev, map, out, ctr);
+}
+
+template <class Out, bool SKIP0 = false>
+__device__ __forceinline__ void emit_tris_rows(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
+                                               unsigned total, const uint32_t *__restrict__ total_dev,
+                                               const int64_t *__restrict__ map, Out out, Counters *ctr) {
     if (total_dev) {                        // device-side row count; `total` then is the CAPACITY of tmp / out: when the
         const unsigned cap = total;         // count exceeds it the host falls back (AXB_ERR_STATE) and nothing is read
         total = *total_dev;
@@ -227,10 +298,17 @@ __global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp,
     }
 }
 
-template <class Out>
-__global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
+template <class Out, bool SKIP0 = false>
+__global__ void __launch_bounds__(256) k_emit_tris(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
                                                    unsigned total, const uint32_t *__restrict__ total_dev,
                                                    const int64_t *__restrict__ map, Out out, Counters *ctr) {
+    emit_tris_rows<Out, SKIP0>(tmp, off, total, total_dev, map, out, ctr);
+}
+
+template <class Out>
+__device__ __forceinline__ void emit_tets_rows(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
+                                               unsigned total, const uint32_t *__restrict__ total_dev,
+                                               const int64_t *__restrict__ map, Out out, Counters *ctr) {
     if (total_dev) {                        // device-side row count; `total` then is the CAPACITY of tmp / out: when the
         const unsigned cap = total;         // count exceeds it the host falls back (AXB_ERR_STATE) and nothing is read
         total = *total_dev;
@@ -250,6 +328,38 @@ __global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp,
     w.put(1, mapped(map, me.y));
     w.put(2, mapped(map, me.z));
     w.put(3, mapped(map, me.w));
+    }
+}
+
+template <class Out>
+__global__ void __launch_bounds__(256) k_emit_tets(const int4 *__restrict__ tmp, const uint32_t *__restrict__ off,
+                                                   unsigned total, const uint32_t *__restrict__ total_dev,
+                                                   const int64_t *__restrict__ map, Out out, Counters *ctr) {
+    emit_tets_rows<Out>(tmp, off, total, total_dev, map, out, ctr);
+}
+
+// The four int64 lists in ONE launch (device-resident results, axb_compute_finish_into): layer blockIdx.y emits
+// dimension y; the layers' tails overlap instead of following each other.
+struct EmitAll {
+    int n;
+    const uint32_t *vkeep, *voff;
+    const int2 *tmp1;
+    const int4 *tmp2, *tmp3;
+    const uint32_t *off1, *off2, *off3;
+    unsigned cap[4];
+    int64_t *out[4];
+    Counters *ctr;
+};
+__global__ void __launch_bounds__(256) k_emit_all(EmitAll E) {
+    if (blockIdx.y == 0) {
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < E.n; i += gridDim.x * blockDim.x)
+            if (E.vkeep[i] && E.voff[i] < E.cap[0]) E.out[0][E.voff[i]] = (int64_t)i;
+    } else if (blockIdx.y == 1) {
+        emit_edges_rows<PlainOut<int64_t>>(E.tmp1, E.off1, E.cap[1], E.off1 + E.n, nullptr, PlainOut<int64_t>{E.out[1]}, E.ctr);
+    } else if (blockIdx.y == 2) {
+        emit_tris_rows<PlainOut<int64_t>>(E.tmp2, E.off2, E.cap[2], E.off2 + E.n, nullptr, PlainOut<int64_t>{E.out[2]}, E.ctr);
+    } else {
+        emit_tets_rows<PlainOut<int64_t>>(E.tmp3, E.off3, E.cap[3], E.off3 + E.n, nullptr, PlainOut<int64_t>{E.out[3]}, E.ctr);
     }
 }
 
