@@ -76,6 +76,9 @@ constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved 
 #endif
 // cull mode bit 1 (triangles flagged as dominated by a partner, AXB_CULL=2|3) needs a third bit matrix per warp; it
 // never paid, so it is compiled out unless asked for
+#ifndef T3_STAGE_MLP
+#define T3_STAGE_MLP 1
+#endif
 #ifndef T3_CULL_TRIS
 #define T3_CULL_TRIS 0
 #endif
@@ -285,6 +288,58 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
             if (lane >= g0 && lane < g1) npairs_any = S.gdeg[lane];
             if (__ballot_sync(FULL, npairs_any > 0) != 0u) {
                 // ---- A: stage the partner atoms (ascending rank inside a generator = pipeline.py:362-370)
+#if T3_STAGE_MLP
+                if constexpr (W == 1) {
+                    // A warp issues in order: with one slot per loop iteration the second slot's rank is only requested
+                    // after the first slot's record has arrived (its store to shared memory waits for it).  So: the
+                    // ranks of ALL the lane's slots first, then all records, then the stores -- two round trips per
+                    // sub-pass instead of two per 32 slots.
+                    constexpr int SL = (SCAP + 31) / 32;
+                    int srk[SL], sg[SL];
+#pragma unroll
+                    for (int k = 0; k < SL; ++k) {
+                        const int s = lane + 32 * k;
+                        sg[k] = -1;
+                        srk[k] = 0;
+                        if (s < nslots) {
+                            int g = g0;                     // last generator with sp[g] - base <= s
+#pragma unroll
+                            for (int step = 8; step > 0; step >>= 1)
+                                if (g + step < g1 && S.sp[g + step] - base <= s) g += step;
+                            sg[k] = g;
+                            srk[k] = __ldg(P.pe_v + S.gadj[g] + (s - (S.sp[g] - base)));
+                        }
+                    }
+                    Atom sa[SL];
+                    double sr[SL];
+                    int so[SL];
+#pragma unroll
+                    for (int k = 0; k < SL; ++k) {
+                        sa[k].x = sa[k].y = sa[k].z = sa[k].r2 = 0.0; sr[k] = 0.0; so[k] = 0;
+                        if (sg[k] >= 0) {
+                            sa[k] = load_atom(P.atoms, srk[k]);
+                            sr[k] = __ldg(P.reach + srk[k]);
+                            so[k] = __ldg(P.orig + srk[k]);
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < SL; ++k) {
+                        const int s = lane + 32 * k;
+                        if (sg[k] >= 0) {
+                            S.ax[s] = sa[k].x; S.ay[s] = sa[k].y; S.az[s] = sa[k].z; S.ar2[s] = sa[k].r2;
+                            S.sreach[s] = sr[k];
+                            S.aorig[s] = so[k];
+                            S.srank[s] = srk[k];
+                            S.sgen[s] = (unsigned char)sg[k];
+                            S.sli[s] = (unsigned char)(s - (S.sp[sg[k]] - base));
+                            S.M[s] = 0ull; S.T[s] = 0ull;
+#if T3_CULL_TRIS
+                            S.D[s] = 0ull;
+#endif
+                        }
+                    }
+                } else
+#endif
                 for (int s = lane; s < nslots; s += 32) {
                     int g = g0;                             // last generator with sp[g] - base <= s
 #pragma unroll

@@ -81,6 +81,41 @@ __device__ __forceinline__ int find_partner(const int *__restrict__ pe_v, unsign
     return hit;
 }
 
+// The three look-ups a kept tet needs -- w and x in v's row, x in w's row -- as ONE loop: both rows are read four
+// entries at a time in the same round (a warp issues in order: three look-ups one after the other were three to six
+// dependent round trips, this is one or two).  Rows are duplicate-free, so a clamped re-read finds the same slot.
+__device__ __forceinline__ void find_partners3(const int *__restrict__ pe_v, unsigned bv, int dv, int tw, int tx, unsigned bw,
+                                               int dw, int tx2, int &iw, int &ix, int &jx) {
+    iw = -1; ix = -1; jx = -1;
+    const int dmax = max(dv, dw);
+    for (int q = 0; q < dmax; q += 4) {
+        int a[4], b[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            a[k] = dv > 0 ? __ldg(pe_v + bv + min(q + k, dv - 1)) : -1;
+            b[k] = dw > 0 ? __ldg(pe_v + bw + min(q + k, dw - 1)) : -1;
+        }
+#pragma unroll
+        for (int k = 3; k >= 0; --k) {
+            if (a[k] == tw) iw = min(q + k, dv - 1);
+            if (a[k] == tx) ix = min(q + k, dv - 1);
+            if (b[k] == tx2) jx = min(q + k, dw - 1);
+        }
+        const bool v_done = (iw >= 0 && ix >= 0) || q + 4 >= dv, w_done = jx >= 0 || q + 4 >= dw;
+        if (v_done && w_done) break;
+    }
+}
+
+#ifndef PRUNE_EARLY_MARKS
+#define PRUNE_EARLY_MARKS 1      // triangles: the look-up's row base is requested before the solve
+#endif
+#ifndef PRUNE_EARLY_TETS
+#define PRUNE_EARLY_TETS 0       // tets: the same (five more live values across the walk)
+#endif
+#ifndef PRUNE_MERGED_TETS
+#define PRUNE_MERGED_TETS 1      // tets: the three look-ups as one loop (find_partners3)
+#endif
+
 // does this call emit the simplices generated by rank `gen`?
 __device__ __forceinline__ bool emits(const PruneParams &P, int gen) {
     return !P.own_only || (gen >= P.rank_lo && gen < P.rank_hi);
@@ -162,6 +197,11 @@ __global__ void __launch_bounds__(256, TETS_MINB) k_prune_tets(PruneParams P) {
         const int l = P.pq_l[e];
         const int i = l & SLOT_MASK, j = (l >> SLOT_BITS) & SLOT_MASK, k = (l >> (2 * SLOT_BITS)) & SLOT_MASK;
         const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z), ox = __ldg(P.orig + r.w);
+#if PRUNE_EARLY_TETS
+        // what the marks of a kept tet need is requested now: it arrives behind the solve and the walk
+        const unsigned bu = __ldg(P.adj_off + r.x), bv = __ldg(P.adj_off + r.y), bw = __ldg(P.adj_off + r.z);
+        const int dv = __ldg(P.deg + r.y), dw = __ldg(P.deg + r.z);
+#endif
         if (P.sweep) {       // potential at this alpha (pipeline.py:447-478: six potential edges, both sizes) and AC2
             if (!P.sw_ac2q[e] || !(P.sw_qsize[e] <= P.tol.lim_a) || !(P.sw_qtsize[e] <= P.tol.lim_a)) continue;
             const unsigned b0 = __ldg(P.adj_off + r.x);
@@ -171,6 +211,10 @@ __global__ void __launch_bounds__(256, TETS_MINB) k_prune_tets(PruneParams P) {
             const Atom au = load_atom(P.atoms, r.x), av = load_atom(P.atoms, r.y);
             const Atom aw = load_atom(P.atoms, r.z), ax = load_atom(P.atoms, r.w);
             const Ortho o = ortho_tet(ou, au, ov, av, ow, aw, ox, ax, P.tol.eps_sing);
+#if PRUNE_EARLY_TETS
+            if (dv > 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.pe_v + bv));     // the rows of the look-ups
+            if (dw > 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.pe_v + bw));
+#endif
             if (!ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, r.w, &s_rows[0][threadIdx.x], 256)) continue;
         }
         int row[4] = {ou, ov, ow, ox};
@@ -187,13 +231,20 @@ __global__ void __launch_bounds__(256, TETS_MINB) k_prune_tets(PruneParams P) {
         }
         // Inheritance marks (pipeline.py:501, 509): 4 faces, 6 edges.  All lookups first, then all
         // atomics back to back (their round trips overlap), then the owner counters of what was new.
+#if !PRUNE_EARLY_TETS
         const unsigned bu = __ldg(P.adj_off + r.x);
         const unsigned bv = __ldg(P.adj_off + r.y);
         const unsigned bw = __ldg(P.adj_off + r.z);
-        const int dv = __ldg(P.deg + r.y);
+        const int dv = __ldg(P.deg + r.y), dw = __ldg(P.deg + r.z);
+#endif
+#if PRUNE_MERGED_TETS
+        int iw, ix, jx;     // face (v, w, x) and edges (v, w), (v, x) live in v's rows, edge (w, x) in w's row
+        find_partners3(P.pe_v, bv, dv, r.z, r.w, bw, dw, r.w, iw, ix, jx);
+#else
         const int iw = find_partner(P.pe_v, bv, dv, r.z);       // face (v, w, x) and edges (v, w), (v, x) live in v's rows
         const int ix = find_partner(P.pe_v, bv, dv, r.w);
-        const int jx = find_partner(P.pe_v, bw, __ldg(P.deg + r.z), r.w);   // edge (w, x) in w's row
+        const int jx = find_partner(P.pe_v, bw, dw, r.w);       // edge (w, x) in w's row
+#endif
         const unsigned long long bj = 1ull << (j & 63), bk = 1ull << (k & 63);
         const size_t W = (size_t)P.W;
         const unsigned long long t0 = atomicOr(P.trimask + (size_t)(bu + i) * W + (j >> 6), bj);
@@ -271,18 +322,29 @@ __global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_tris(PruneP
         const int i = r.w & 0xffff, j = (r.w >> 16) & 0x7fff;
         const unsigned bu = __ldg(P.adj_off + r.x);
         const int ou = __ldg(P.orig + r.x), ov = __ldg(P.orig + r.y), ow = __ldg(P.orig + r.z);
+#if PRUNE_EARLY_MARKS
+        const unsigned bv = __ldg(P.adj_off + r.y);          // for the marks: requested now, arrives behind the solve
+        const int dv = __ldg(P.deg + r.y);
+#endif
         if (P.sweep) {       // potential at this alpha (pipeline.py:398-420: three potential edges, own size) and AC2
             if (!P.sw_ac2t[e] || !(P.sw_tsize[e] <= P.tol.lim_a)) return;
             if (!(P.sw_pf[bu + i] & P.sw_pf[bu + j] & P.sw_pf[P.sw_tvw[e]])) return;
         } else {
             const Atom au = load_atom(P.atoms, r.x), av = load_atom(P.atoms, r.y), aw = load_atom(P.atoms, r.z);
             const Ortho o = ortho_tri(ou, au, ov, av, ow, aw, P.tol.eps_sing);
+#if PRUNE_EARLY_MARKS
+            if (dv > 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.pe_v + bv));     // the row of the look-up
+#endif
             if (!ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, -1, &s_rows[0][threadIdx.x], PRUNE_THREADS)) return;
         }
         // kept: mark the triangle and its three edges.  The lookup first, then all four atomics back to back (their
         // round trips overlap), then the owner counters of what was new (no return value needed: fire and forget)
+#if PRUNE_EARLY_MARKS
+        const int iw = find_partner(P.pe_v, bv, dv, r.z);
+#else
         const unsigned bv = __ldg(P.adj_off + r.y);
         const int iw = find_partner(P.pe_v, bv, __ldg(P.deg + r.y), r.z);
+#endif
         const unsigned long long bit = 1ull << (j & 63);
         const unsigned long long t0 = atomicOr(P.trimask + (size_t)(bu + i) * P.W + (j >> 6), bit);
         const unsigned e0 = atomicExch(P.eflag + bu + i, 1u);
