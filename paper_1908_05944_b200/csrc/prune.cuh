@@ -305,7 +305,11 @@ inline int prune_claim(unsigned long long entries, unsigned warps, int large) {
     const unsigned long long per = entries / ((unsigned long long)warps * 32ull * 4ull);
     return (int)(per < 1 ? 1 : per > (unsigned long long)large ? (unsigned long long)large : per);
 }
-constexpr int PRUNE_STACK = 64;              // free entries parked per warp (processed as soon as 32 are waiting)
+#ifndef PRUNE_SCAN_U
+#define PRUNE_SCAN_U 4
+#endif
+constexpr int PRUNE_STACK = 32 + 32 * PRUNE_SCAN_U;   // free entries parked per warp (processed as soon as 32 are waiting;
+                                                      // a scan step adds up to 32 * PRUNE_SCAN_U)
 
 // pipeline.py:502-505: AC2 for the triangles no kept tet inherited
 __global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_tris(PruneParams P) {
@@ -375,22 +379,42 @@ __global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_tris(PruneP
                 if (lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[1], 1u);
                 b = 0;
             }
-            const unsigned e = chunk * span + (unsigned)(b * 32 + lane);
-            ++b;
-            bool is_free = false;
-            if (e < n_pt) {
-                const int4 r = P.pt[e];
-                if (r.w >= 0 && r.z >= P.rank_lo) {           // bit 31: already known to be dominated (cull mode); slab:
-                                                              // a triangle below every owned ball is the lower neighbour's
-                    const int i = r.w & 0xffff, j = (r.w >> 16) & 0x7fff;
-                    const unsigned bu = __ldg(P.adj_off + r.x);
-                    const unsigned long long word = P.trimask[(size_t)(bu + i) * P.W + (j >> 6)];
-                    is_free = !((word >> (j & 63)) & 1ull);   // not inherited from a kept tet
-                }
+            // PRUNE_SCAN_U sub-steps of the claim at once, level by level (list entry -> row base -> mask word): a warp
+            // issues in order, so one entry per iteration made every iteration wait for three dependent round trips
+            constexpr int U = PRUNE_SCAN_U;
+            const unsigned ebase = chunk * span + (unsigned)(b * 32 + lane);
+            const int nsub = min(U, claim - b);
+            b += nsub;
+            int4 r[U];
+            bool c[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const unsigned e = ebase + 32u * k;
+                r[k] = make_int4(0, 0, 0, -1);
+                if (k < nsub && e < n_pt) r[k] = P.pt[e];
             }
-            const unsigned m = __ballot_sync(FULL, is_free);
-            if (is_free) stack[sn + __popc(m & lanemask_lt())] = e;
-            sn += __popc(m);
+            unsigned bu[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                // bit 31: already known to be dominated (cull mode); slab: a triangle below every owned ball is the
+                // lower neighbour's
+                c[k] = r[k].w >= 0 && r[k].z >= P.rank_lo;
+                bu[k] = c[k] ? __ldg(P.adj_off + r[k].x) : 0u;
+            }
+            unsigned long long w[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int j = (r[k].w >> 16) & 0x7fff;
+                w[k] = c[k] ? P.trimask[(size_t)(bu[k] + (r[k].w & 0xffff)) * P.W + (j >> 6)] : ~0ull;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int j = (r[k].w >> 16) & 0x7fff;
+                const bool f = c[k] && !((w[k] >> (j & 63)) & 1ull);     // not inherited from a kept tet
+                const unsigned m = __ballot_sync(FULL, f);
+                if (f) stack[sn + __popc(m & lanemask_lt())] = ebase + 32u * k;
+                sn += __popc(m);
+            }
             __syncwarp();
         }
         if (sn == 0) break;
@@ -444,22 +468,37 @@ __global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_edges(Prune
                 if (lane == 0) chunk_n = atomicAdd(&P.ctr->work_next[2], 1u);
                 b = 0;
             }
-            const unsigned e = chunk * span + (unsigned)(b * 32 + lane);
-            ++b;
-            bool is_free = false;
-            if (e < n_pe) {
-                const int u = __ldg(P.pe_u + e);
-                if (P.eflag[e] != 0u) {                       // inherited: its endpoints are kept
-                    P.vflag[u] = 1;
-                    P.vflag[__ldg(P.pe_v + e)] = 1;
-                } else {
-                    // slab: an edge below every owned ball or generated by the upper halo is a neighbour's business
-                    is_free = u < P.rank_hi && __ldg(P.pe_v + e) >= P.rank_lo;
-                }
+            // PRUNE_SCAN_U sub-steps of the claim at once (see k_prune_tris)
+            constexpr int U = PRUNE_SCAN_U;
+            const unsigned ebase = chunk * span + (unsigned)(b * 32 + lane);
+            const int nsub = min(U, claim - b);
+            b += nsub;
+            int eu[U], ev[U];
+            unsigned ef[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const unsigned e = ebase + 32u * k;
+                const bool valid = k < nsub && e < n_pe;
+                eu[k] = valid ? __ldg(P.pe_u + e) : -1;
+                ev[k] = valid ? __ldg(P.pe_v + e) : -1;
+                ef[k] = valid ? P.eflag[e] : 0u;
             }
-            const unsigned m = __ballot_sync(FULL, is_free);
-            if (is_free) stack[sn + __popc(m & lanemask_lt())] = e;
-            sn += __popc(m);
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                bool is_free = false;
+                if (eu[k] >= 0) {
+                    if (ef[k] != 0u) {                            // inherited: its endpoints are kept
+                        P.vflag[eu[k]] = 1;
+                        P.vflag[ev[k]] = 1;
+                    } else {
+                        // slab: an edge below every owned ball or generated by the upper halo is a neighbour's business
+                        is_free = eu[k] < P.rank_hi && ev[k] >= P.rank_lo;
+                    }
+                }
+                const unsigned m = __ballot_sync(FULL, is_free);
+                if (is_free) stack[sn + __popc(m & lanemask_lt())] = ebase + 32u * k;
+                sn += __popc(m);
+            }
             __syncwarp();
         }
         if (sn == 0) break;
