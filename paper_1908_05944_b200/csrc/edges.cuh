@@ -47,6 +47,9 @@ constexpr int EL_ROWS = 13;
 #ifndef EL_PREF_AHEAD
 #define EL_PREF_AHEAD 1
 #endif
+#ifndef EL_WALK2
+#define EL_WALK2 3           // candidates per lane and walk iteration (0: the one-at-a-time loop)
+#endif
 #ifndef EL_BUDGET_V
 #define EL_BUDGET_V 2400
 #endif
@@ -270,6 +273,53 @@ __global__ void __launch_bounds__(EL_WARPS * 32, EL_MINB) k_edges(EstParams P, i
 #if EL_PREF_ROW
                 if (nr > 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.xyzr + S.u.rows[0][lane].x));
 #endif
+#if EL_WALK2
+                // EL_WALK2 candidates of the row per iteration: a warp issues in order and every iteration ends in a
+                // ballot, so with one record per iteration each of the ~33 candidates of a lane cost a full load latency.
+                constexpr int K = EL_WALK2;
+                for (;;) {
+                    if (pos >= end && r < nr) {             // parked rows are non-empty: one step suffices
+                        const int2 q = S.u.rows[r][lane];
+                        pos = q.x; end = q.y; ++r;
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(P.xyzr + pos));
+                    }
+                    const int have = min(end - pos, K);     // candidates this lane takes in this iteration
+                    if (!__any_sync(FULL, have > 0)) break;
+                    if (pos + K < end) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.xyzr + pos + K));
+                    Atom av[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        av[k].x = av[k].y = av[k].z = 0.0; av[k].r2 = -1.0;
+                        if (k < have) av[k] = load_atom(P.xyzr, pos + k);                       // (x, y, z, reach)
+                    }
+                    unsigned m[K];
+                    unsigned any = 0;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const double dx = av[k].x - ux, dy = av[k].y - uy, dz = av[k].z - uz;
+                        const double lims = av[k].r2 + ureach;
+                        const bool pass = av[k].r2 >= 0.0 && (dx * dx + dy * dy) + dz * dz <= lims * lims;   // pipeline.py:341-344
+                        m[k] = __ballot_sync(FULL, pass);
+                        any |= m[k];
+                    }
+                    if (any) {
+                        if (qn + 32 * K > EL_QCAP) {
+                            settle();
+                            if (qn + 32 * K > EL_QCAP) { crowded = true; break; }
+                        }
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {       // (a lane's candidates stay in ascending rank)
+                            if ((m[k] >> lane) & 1u) {
+                                const int at = qn + __popc(m[k] & lanemask_lt());
+                                S.q_cand[at] = pos + k; S.q_gen[at] = (unsigned char)lane;
+                            }
+                            qn += __popc(m[k]);
+                        }
+                        __syncwarp();
+                    }
+                    pos += max(have, 0);
+                }
+#else
                 for (;;) {
                     if (pos >= end && r < nr) {             // parked rows are non-empty: one step suffices
                         const int2 q = S.u.rows[r][lane];
@@ -307,6 +357,7 @@ __global__ void __launch_bounds__(EL_WARPS * 32, EL_MINB) k_edges(EstParams P, i
                     }
                     if (have) ++pos;
                 }
+#endif
             }
             if (crowded) {
                 // more kept pairs than the queue holds: halve the pass and redo it; a single generator that still does
