@@ -281,7 +281,13 @@ __device__ __forceinline__ Atom load_atom(const Atom *__restrict__ atoms, int t)
 // all rows are walked as ONE flattened sequence with the next AC2_DEPTH + 1 balls prefetched into L1 ahead
 // of the ball being tested.  Same boolean as ac2_pass (same cells, same arithmetic, pipeline.py:286-313).
 #ifndef AC2_DEPTH
-#define AC2_DEPTH 1
+#define AC2_DEPTH 3
+#endif
+#ifndef AC2_WALK_ROWS
+#define AC2_WALK_ROWS 0
+#endif
+#ifndef AC2_PAIR
+#define AC2_PAIR 1           // two balls of the flattened sequence per iteration (a thread issues in order)
 #endif
 __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__restrict__ atoms, double cx, double cy,
                                              double cz, double thr, double r2max, int inc0, int inc1, int inc2, int inc3,
@@ -341,14 +347,50 @@ __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__re
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
         const int k = ORD[q];
-        if (er[k] > sr[k]) { rows[nr * stride] = make_int2(sr[k], er[k]); ++nr; }
+        if (er[k] > sr[k]) {
+            rows[nr * stride] = make_int2(sr[k], er[k]);
+            ++nr;
+#if AC2_WALK_ROWS == 1
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(atoms + sr[k]));
+#endif
+        }
     }
+#if AC2_WALK_ROWS
+    // Row by row, two balls per iteration.  The first line of EVERY parked row was requested while the rows were parked
+    // (a row of the trimmed block holds ~2 balls, i.e. one 128-byte line), so the walk's loads are in flight together;
+    // a thread issues in order, and with one ball per iteration each ball cost a load latency plus the fp64 chain.
+#if AC2_WALK_ROWS == 2
+    if (nr > 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(atoms + rows[0].x));
+#endif
+    for (int r = 0; r < nr; ++r) {
+        const int2 q = rows[r * stride];
+#if AC2_WALK_ROWS == 2
+        if (r + 1 < nr) asm volatile("prefetch.global.L1 [%0];" ::"l"(atoms + rows[(r + 1) * stride].x));
+#endif
+        for (int pos = q.x; pos < q.y; pos += 2) {
+            const bool two = pos + 1 < q.y;
+            if (pos + 4 < q.y) asm volatile("prefetch.global.L1 [%0];" ::"l"(atoms + pos + 4));
+            const Atom a = load_atom(atoms, pos);
+            const Atom b = load_atom(atoms, two ? pos + 1 : pos);
+            const double ax = a.x - cx, ay = a.y - cy, az = a.z - cz;
+            const double bx = b.x - cx, by = b.y - cy, bz = b.z - cz;
+            const double dpa = ((ax * ax + ay * ay) + az * az) - a.r2;
+            const double dpb = ((bx * bx + by * by) + bz * bz) - b.r2;
+            // incident balls are masked (pipeline.py:306-307); they sit at dp == size > thr up to rounding, so the mask is
+            // only consulted in the rare branch
+            if (dpa < thr && !(pos == inc0 || pos == inc1 || pos == inc2 || pos == inc3)) return false;
+            if (two && dpb < thr && !(pos + 1 == inc0 || pos + 1 == inc1 || pos + 1 == inc2 || pos + 1 == inc3)) return false;
+        }
+    }
+    return true;
+#else
     // flattened walk over the balls of all rows
     int r = -1, pos = 0, end = 0;
     auto next = [&]() -> int {
         if (pos >= end) {
-            if (++r >= nr) { r = nr; return -1; }
-            const int2 q = rows[min(r, 8) * stride];      // (clamped: the load may be issued ahead of the test)
+            if (r + 1 >= nr) return -1;                   // exhausted (and stays so: r never leaves the parked rows)
+            ++r;
+            const int2 q = rows[r * stride];
             pos = q.x; end = q.y;
         }
         return pos++;
@@ -367,6 +409,27 @@ __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__re
         tq[d] = next();
         if (tq[d] >= 0) prefetch(tq[d]);
     }
+#if AC2_PAIR
+    // two balls of the flattened sequence per iteration (AC2_DEPTH >= 3: two under test, two requested)
+    static_assert(!AC2_PAIR || AC2_DEPTH >= 3, "AC2_PAIR needs a queue of four");
+    while (tq[0] >= 0) {
+        const int t0 = tq[0], t1 = tq[1];
+        const Atom a = load_atom(atoms, t0);
+        const Atom b = load_atom(atoms, t1 >= 0 ? t1 : t0);
+#pragma unroll
+        for (int d = 0; d + 2 <= AC2_DEPTH; ++d) tq[d] = tq[d + 2];
+        tq[AC2_DEPTH - 1] = next();
+        if (tq[AC2_DEPTH - 1] >= 0) prefetch(tq[AC2_DEPTH - 1]);
+        tq[AC2_DEPTH] = next();
+        if (tq[AC2_DEPTH] >= 0) prefetch(tq[AC2_DEPTH]);
+        const double ax = a.x - cx, ay = a.y - cy, az = a.z - cz;
+        const double bx = b.x - cx, by = b.y - cy, bz = b.z - cz;
+        const double dpa = ((ax * ax + ay * ay) + az * az) - a.r2;
+        const double dpb = ((bx * bx + by * by) + bz * bz) - b.r2;
+        if (dpa < thr && !(t0 == inc0 || t0 == inc1 || t0 == inc2 || t0 == inc3)) return false;   // incident balls are masked (pipeline.py:306-307)
+        if (t1 >= 0 && dpb < thr && !(t1 == inc0 || t1 == inc1 || t1 == inc2 || t1 == inc3)) return false;
+    }
+#else
     while (tq[0] >= 0) {
         const int t = tq[0];
         const Atom a = load_atom(atoms, t);
@@ -378,6 +441,7 @@ __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__re
         const double dp = ((ddx * ddx + ddy * ddy) + ddz * ddz) - a.r2;
         if (dp < thr && !(t == inc0 || t == inc1 || t == inc2 || t == inc3)) return false;   // incident balls are masked (pipeline.py:306-307)
     }
+#endif
 #else
     int tq[AC2_DEPTH];
     Atom aq[AC2_DEPTH];
@@ -399,6 +463,7 @@ __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__re
     }
 #endif
     return true;
+#endif
 }
 #endif
 
