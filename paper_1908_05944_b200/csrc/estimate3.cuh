@@ -76,6 +76,9 @@ constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved 
 #endif
 // cull mode bit 1 (triangles flagged as dominated by a partner, AXB_CULL=2|3) needs a third bit matrix per warp; it
 // never paid, so it is compiled out unless asked for
+#ifndef T3_PAIR2
+#define T3_PAIR2 1
+#endif
 #ifndef T3_STAGE_MLP
 #define T3_STAGE_MLP 1
 #endif
@@ -451,6 +454,27 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                     bool done = false;
                     while (!done) {
                         if (flat) {
+#if T3_PAIR2
+                            // two pairs per lane and iteration (the table look-ups of both are in flight together)
+                            while (p0 < npairs && qn < 32 * 7) {
+                                const int pa = p0 + lane, pb = pa + 32;
+                                p0 += 64;
+                                bool passa = false, passb = false;
+                                int sia = 0, sja = 0, sib = 0, sjb = 0;
+                                if (pa < npairs) sia = S.ptab[pa];
+                                if (pb < npairs) sib = S.ptab[pb];
+                                if (pa < npairs) sja = sia + 1 + (pa - S.rowpre[sia]);
+                                if (pb < npairs) sjb = sib + 1 + (pb - S.rowpre[sib]);
+                                if (pa < npairs) passa = reach_pair(atom_at(S, sia), S.sreach[sia], atom_at(S, sja), S.sreach[sja]);   // pipeline.py:398-401
+                                if (pb < npairs) passb = reach_pair(atom_at(S, sib), S.sreach[sib], atom_at(S, sjb), S.sreach[sjb]);
+                                const unsigned ma = __ballot_sync(FULL, passa), mb = __ballot_sync(FULL, passb);
+                                if (passa) wq[qn + __popc(ma & lanemask_lt())] = (unsigned short)(sia | (sja << 8));
+                                qn += __popc(ma);
+                                if (passb) wq[qn + __popc(mb & lanemask_lt())] = (unsigned short)(sib | (sjb << 8));
+                                qn += __popc(mb);
+                            }
+                            done = p0 >= npairs;
+#else
                             while (p0 < npairs && qn < 32 * 8) {
                                 const int p = p0 + lane;
                                 p0 += 32;
@@ -466,6 +490,7 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                                 qn += __popc(m);
                             }
                             done = p0 >= npairs;
+#endif
                         } else {
                             // lane = slot i of the group, round r pairs it with slot i + r (its record is re-read after a
                             // solve instead of being kept alive across it)
