@@ -1107,7 +1107,7 @@ int run_prune(axb_ctx *c) {
     if ((uint64_t)c->n_pq > (uint64_t)c->n + c->n / 2)
         k_prune_tets<1><<<(unsigned)c->sm_count * (unsigned)TETS_MINB, 256, 0, c->stream>>>(P);
     else
-        k_prune_tets<0><<<(unsigned)c->sm_count * 8u, 256, 0, c->stream>>>(P);
+        k_prune_tets<0><<<(unsigned)c->sm_count * (unsigned)TETS_GRID, 256, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_TETS + 1)) != AXB_OK) return st;
     return run_prune_lower(c);
@@ -2028,7 +2028,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     if ((uint64_t)c->n_pq > (uint64_t)c->n + c->n / 2)
         k_prune_tets<1><<<(unsigned)c->sm_count * (unsigned)TETS_MINB, 256, 0, c->stream>>>(P);
     else
-        k_prune_tets<0><<<(unsigned)c->sm_count * 8u, 256, 0, c->stream>>>(P);
+        k_prune_tets<0><<<(unsigned)c->sm_count * (unsigned)TETS_GRID, 256, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_TETS + 1)) != AXB_OK) return st;
     if ((st = device_scan(c, c->cnt3, n, c->off3)) != AXB_OK) return st;

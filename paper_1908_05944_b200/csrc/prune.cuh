@@ -162,6 +162,9 @@ __device__ __forceinline__ bool lists_overflowed(const PruneParams &P) {
 #ifndef TETS_MINB
 #define TETS_MINB 3
 #endif
+#ifndef TETS_GRID
+#define TETS_GRID 8         // blocks per SM of the static variant (TETS_MINB are resident at a time)
+#endif
 template <int DYN>
 __global__ void __launch_bounds__(256, TETS_MINB) k_prune_tets(PruneParams P) {
     __shared__ int2 s_rows[9][256];
