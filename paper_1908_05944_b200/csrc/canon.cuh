@@ -169,6 +169,42 @@ __global__ void __launch_bounds__(256) k_scatter_tris(CanonParams P, unsigned ca
         if (!canon_emits(P, u)) continue;
         const int ou = __ldg(P.orig + u), ov = __ldg(P.orig + __ldg(P.pe_v + e));
         const unsigned bu = __ldg(P.adj_off + u);
+#if SCATTER_MLP
+        if (P.W == 1) {         // level by level for up to three triangles of the row (see k_scatter_edges_tris)
+            unsigned long long m = any;
+            do {
+                int j[3], pw[3], ow[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    j[k] = -1;
+                    if (m) { j[k] = __ffsll((long long)m) - 1; m &= m - 1; }
+                }
+#pragma unroll
+                for (int k = 0; k < 3; ++k) pw[k] = j[k] >= 0 ? __ldg(P.pe_v + bu + j[k]) : 0;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) ow[k] = j[k] >= 0 ? __ldg(P.orig + pw[k]) : 0;
+                int ta[3], tb[3], tc[3];
+                unsigned tsl[3], to[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    int a = ou, b = ov, c = ow[k], t;
+                    if (a > b) { t = a; a = b; b = t; }
+                    if (b > c) { t = b; b = c; c = t; }
+                    if (a > b) { t = a; a = b; b = t; }
+                    ta[k] = a; tb[k] = b; tc[k] = c;
+                    tsl[k] = 0; to[k] = 0;
+                    if (j[k] >= 0) { to[k] = P.off2[a]; tsl[k] = atomicSub(P.cnt2 + a, 1u); }
+                }
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    if (j[k] >= 0) {
+                        const unsigned pos = to[k] + tsl[k] - 1u;
+                        if (pos < cap) P.tmp2[pos] = make_int4(ta[k], tb[k], tc[k], 0);
+                    }
+            } while (m);
+            continue;
+        }
+#endif
         for (int w = 0; w < P.W; ++w) {
             unsigned long long m = P.trimask[(size_t)e * P.W + w];
             while (m) {
