@@ -76,6 +76,9 @@ constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved 
 #endif
 // cull mode bit 1 (triangles flagged as dominated by a partner, AXB_CULL=2|3) needs a third bit matrix per warp; it
 // never paid, so it is compiled out unless asked for
+#ifndef T3_CULL2
+#define T3_CULL2 1
+#endif
 #ifndef T3_PAIR2
 #define T3_PAIR2 1
 #endif
@@ -216,6 +219,19 @@ __device__ __forceinline__ Ortho ortho_tet_s(const SW &S, int a, int b, int c, i
 template <class SW>
 __device__ __forceinline__ bool dominated_by_partner3(const SW &S, int sb, int se, int s0, int s1, int s2,
                                                       double cx, double cy, double cz, double thr) {
+#if T3_CULL2
+    // two partners per iteration (independent fp64 chains; the simplex' own slots are masked afterwards)
+    for (int s = sb; s < se; s += 2) {
+        const int t = min(s + 1, se - 1);
+        const double ax = S.ax[s] - cx, ay = S.ay[s] - cy, az = S.az[s] - cz;
+        const double bx = S.ax[t] - cx, by = S.ay[t] - cy, bz = S.az[t] - cz;
+        const double dpa = ((ax * ax + ay * ay) + az * az) - S.ar2[s];
+        const double dpb = ((bx * bx + by * by) + bz * bz) - S.ar2[t];
+        if (dpa < thr && !(s == s0 || s == s1 || s == s2)) return true;
+        if (dpb < thr && !(t == s0 || t == s1 || t == s2)) return true;
+    }
+    return false;
+#else
     for (int s = sb; s < se; ++s) {
         if (s == s0 || s == s1 || s == s2) continue;
         const double ddx = S.ax[s] - cx, ddy = S.ay[s] - cy, ddz = S.az[s] - cz;
@@ -223,6 +239,7 @@ __device__ __forceinline__ bool dominated_by_partner3(const SW &S, int sb, int s
         if (dp < thr) return true;
     }
     return false;
+#endif
 }
 
 // ordinal of triangle (s, sj) among its generator's triangles in (i, j) order, from the listed triangles of the tile

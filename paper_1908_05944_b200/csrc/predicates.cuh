@@ -283,9 +283,6 @@ __device__ __forceinline__ Atom load_atom(const Atom *__restrict__ atoms, int t)
 #ifndef AC2_DEPTH
 #define AC2_DEPTH 3
 #endif
-#ifndef AC2_WALK_ROWS
-#define AC2_WALK_ROWS 0
-#endif
 #ifndef AC2_PAIR
 #define AC2_PAIR 1           // two balls of the flattened sequence per iteration (a thread issues in order)
 #endif
@@ -350,40 +347,8 @@ __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__re
         if (er[k] > sr[k]) {
             rows[nr * stride] = make_int2(sr[k], er[k]);
             ++nr;
-#if AC2_WALK_ROWS == 1
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(atoms + sr[k]));
-#endif
         }
     }
-#if AC2_WALK_ROWS
-    // Row by row, two balls per iteration.  The first line of EVERY parked row was requested while the rows were parked
-    // (a row of the trimmed block holds ~2 balls, i.e. one 128-byte line), so the walk's loads are in flight together;
-    // a thread issues in order, and with one ball per iteration each ball cost a load latency plus the fp64 chain.
-#if AC2_WALK_ROWS == 2
-    if (nr > 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(atoms + rows[0].x));
-#endif
-    for (int r = 0; r < nr; ++r) {
-        const int2 q = rows[r * stride];
-#if AC2_WALK_ROWS == 2
-        if (r + 1 < nr) asm volatile("prefetch.global.L1 [%0];" ::"l"(atoms + rows[(r + 1) * stride].x));
-#endif
-        for (int pos = q.x; pos < q.y; pos += 2) {
-            const bool two = pos + 1 < q.y;
-            if (pos + 4 < q.y) asm volatile("prefetch.global.L1 [%0];" ::"l"(atoms + pos + 4));
-            const Atom a = load_atom(atoms, pos);
-            const Atom b = load_atom(atoms, two ? pos + 1 : pos);
-            const double ax = a.x - cx, ay = a.y - cy, az = a.z - cz;
-            const double bx = b.x - cx, by = b.y - cy, bz = b.z - cz;
-            const double dpa = ((ax * ax + ay * ay) + az * az) - a.r2;
-            const double dpb = ((bx * bx + by * by) + bz * bz) - b.r2;
-            // incident balls are masked (pipeline.py:306-307); they sit at dp == size > thr up to rounding, so the mask is
-            // only consulted in the rare branch
-            if (dpa < thr && !(pos == inc0 || pos == inc1 || pos == inc2 || pos == inc3)) return false;
-            if (two && dpb < thr && !(pos + 1 == inc0 || pos + 1 == inc1 || pos + 1 == inc2 || pos + 1 == inc3)) return false;
-        }
-    }
-    return true;
-#else
     // flattened walk over the balls of all rows
     int r = -1, pos = 0, end = 0;
     auto next = [&]() -> int {
@@ -463,7 +428,6 @@ __device__ __forceinline__ bool ac2_pass_mlp(const GridView &g, const Atom *__re
     }
 #endif
     return true;
-#endif
 }
 #endif
 
