@@ -76,8 +76,11 @@ constexpr int T3_WQCAP = 288;             // reach-passing pairs queued (solved 
 #endif
 // cull mode bit 1 (triangles flagged as dominated by a partner, AXB_CULL=2|3) needs a third bit matrix per warp; it
 // never paid, so it is compiled out unless asked for
+#ifndef T3_SPEC3
+#define T3_SPEC3 1
+#endif
 #ifndef T3_CULL2
-#define T3_CULL2 1
+#define T3_CULL2 2
 #endif
 #ifndef T3_PAIR2
 #define T3_PAIR2 1
@@ -220,15 +223,22 @@ template <class SW>
 __device__ __forceinline__ bool dominated_by_partner3(const SW &S, int sb, int se, int s0, int s1, int s2,
                                                       double cx, double cy, double cz, double thr) {
 #if T3_CULL2
-    // two partners per iteration (independent fp64 chains; the simplex' own slots are masked afterwards)
-    for (int s = sb; s < se; s += 2) {
-        const int t = min(s + 1, se - 1);
-        const double ax = S.ax[s] - cx, ay = S.ay[s] - cy, az = S.az[s] - cz;
-        const double bx = S.ax[t] - cx, by = S.ay[t] - cy, bz = S.az[t] - cz;
-        const double dpa = ((ax * ax + ay * ay) + az * az) - S.ar2[s];
-        const double dpb = ((bx * bx + by * by) + bz * bz) - S.ar2[t];
-        if (dpa < thr && !(s == s0 || s == s1 || s == s2)) return true;
-        if (dpb < thr && !(t == s0 || t == s1 || t == s2)) return true;
+    // T3_CULL2 partners per iteration (independent fp64 chains: a thread issues in order; the simplex' own slots are
+    // masked afterwards -- they sit at the simplex' size, above the threshold up to rounding)
+    constexpr int K = T3_CULL2;
+    for (int s = sb; s < se; s += K) {
+        double dp[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int t = min(s + k, se - 1);
+            const double ax = S.ax[t] - cx, ay = S.ay[t] - cy, az = S.az[t] - cz;
+            dp[k] = ((ax * ax + ay * ay) + az * az) - S.ar2[t];
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int t = min(s + k, se - 1);
+            if (dp[k] < thr && !(t == s0 || t == s1 || t == s2)) return true;
+        }
     }
     return false;
 #else
@@ -406,11 +416,19 @@ __global__ void __launch_bounds__(T3_WARPS * 32, (T3Cfg<W, SHAPE>::MINB)) k_tri_
                                 const int d = S.gdeg[g];
                                 const unsigned q = (unsigned)(i * (2 * d - i - 1) / 2 + (j - i - 1));   // triu ordinal
                                 const Ortho e2 = ortho_edge_s(S, si, sj, P.tol.eps_sing);                // pipeline.py:412-414
+#if T3_SPEC3
+                                // (solved beside the edge, not behind it: nearly every pre-filtered pair is a potential edge,
+                                // and two independent fp64 chains fill the issue slots one leaves empty; its result and its
+                                // singular flag only count if the pair passes, as in the reference)
+                                const Ortho e3 = ortho_tri_s(S, SCAP + g, si, sj, P.tol.eps_sing);       // pipeline.py:417-419
+#endif
                                 if (e2.singular) record_singular(P, make_err_key(ST_VW, t, q), S.aorig[si], S.aorig[sj], -1, -1, 2);
                                 if (e2.size <= P.tol.lim_a) {                                            // pipeline.py:415
                                     set_bit(&S.M[si * W], j);
                                     set_bit(&S.M[sj * W], i);
+#if !T3_SPEC3
                                     const Ortho e3 = ortho_tri_s(S, SCAP + g, si, sj, P.tol.eps_sing);   // pipeline.py:417-419
+#endif
                                     if (e3.singular)
                                         record_singular(P, make_err_key(ST_TRI, t, q), S.aorig[SCAP + g], S.aorig[si], S.aorig[sj], -1, 3);
                                     if (e3.size <= P.tol.lim_a) {                                        // pipeline.py:420
