@@ -47,6 +47,9 @@ constexpr int EL_ROWS = 13;
 #ifndef EL_PREF_AHEAD
 #define EL_PREF_AHEAD 1
 #endif
+#ifndef EL_PREF_TILE
+#define EL_PREF_TILE 1
+#endif
 #ifndef EL_WALK2
 #define EL_WALK2 3           // candidates per lane and walk iteration (0: the one-at-a-time loop)
 #endif
@@ -226,6 +229,17 @@ __global__ void __launch_bounds__(EL_WARPS * 32, EL_MINB) k_edges(EstParams P, i
                 }
             }
 
+#if EL_PREF_TILE
+            {   // the next tile's generators (record, reach, cell) are requested now; phase A finds them in L1 / L2
+                const int tnx = __shfl_sync(FULL, tile_n, 0);
+                const int tq = rank_lo + tnx * 32 + lane;
+                if (ts == tile_lo && tnx < ntiles && tq < rank_hi) {
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(P.atoms + tq));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(P.reach + tq));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(P.cell_of_rank + tq));
+                }
+            }
+#endif
             int qn = 0, solved = 0;                         // warp-uniform: queue fill, settled prefix
             // ---- C (defined first): ortho2 over the unsettled part of the queue, kept pairs compacted in place
             auto settle = [&]() {
