@@ -482,12 +482,13 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
     EstParams P = est_params(c, report_key);
     const int ngen = c->rank_hi - c->gen_lo;
 #ifndef TETS_DYN_PAIRS
-#define TETS_DYN_PAIRS 20      // more partner pairs per generator than this: k_prune_tets claims chunks (1M atoms: the static
-                               // loop wins up to alpha 0.4 = 0.36 vs 0.41 ms, a tie at 0.6, claims from alpha 0.8 = 0.67 vs 0.69 ms)
+#define TETS_DYN_PAIRS 25      // more partner pairs per generator than this: k_prune_tets claims chunks (1M atoms, final kernels:
+                               // the static loop wins up to alpha 0.6 = 0.50 vs 0.51 ms (0.4: 0.33 vs 0.38), claims from 0.8 = 0.64 vs 0.70 ms)
 #endif
 #ifndef T3_HEAVY_PAIRS
-#define T3_HEAVY_PAIRS 25     // more partner pairs per generator than this: heavy tile shape (1M atoms: light wins up to
-                              // alpha 0.6 = 0.99 vs 1.09 ms, heavy from alpha 0.8 = 1.32 vs 1.36 ms; tools/gpu_alpha_scan.py)
+#define T3_HEAVY_PAIRS 33     // more partner pairs per generator than this: heavy tile shape (1M atoms, final kernels: light wins up
+                              // to alpha 0.8 = 1.04 vs 1.11 ms (0.6: 0.82 vs 0.91), a tie at 1.0, heavy at 1.4 = 1.97 vs 2.07 ms;
+                              // tools/gpu_alpha_scan.py; ~11 / 23 / 27 / 33 / 45 pairs per generator at alpha 0 / 0.6 / 0.8 / 1.0 / 1.4)
 #endif
     {   // warp-autonomous tiles (estimate3.cuh); the tile shape follows the work per generator
         CUDA_TRY(c, cudaMemsetAsync(&c->ctr->tile_next, 0, 2 * sizeof(unsigned int), c->stream));     // tile_next, n_heavy
