@@ -504,7 +504,10 @@ int launch_tri_tet(axb_ctx *c, unsigned long long report_key) {
         c->many_tets = c->h->ctr.pair_bound > (unsigned long long)TETS_DYN_PAIRS * (unsigned long long)std::max(ngen, 1);   // k_prune_tets variant
         if (c->W != 1) st = launch(k_tri_tet3<4, T3_LIGHT>, sizeof(T3Warp<4, T3_LIGHT>), T3Cfg<4, T3_LIGHT>::GENS, 1);
         else if (heavy) st = launch(k_tri_tet3<1, T3_HEAVY>, sizeof(T3Warp<1, T3_HEAVY>), T3Cfg<1, T3_HEAVY>::GENS, T3Cfg<1, T3_HEAVY>::MINB);
-        else if ((unsigned)ngen <= 16u * T3_WARPS * (unsigned)c->sm_count * (unsigned)T3Cfg<1, T3_LIGHT>::MINB * 2u)    // <= 2 tiles per warp
+#ifndef T3_SMALL_TILES
+#define T3_SMALL_TILES 2      // at most this many tiles per resident warp: the spill-free 16-warp shape
+#endif
+        else if ((unsigned)ngen <= 16u * T3_WARPS * (unsigned)c->sm_count * (unsigned)T3Cfg<1, T3_LIGHT>::MINB * (unsigned)T3_SMALL_TILES)
             st = launch(k_tri_tet3<1, T3_SMALL>, sizeof(T3Warp<1, T3_SMALL>), T3Cfg<1, T3_SMALL>::GENS, T3Cfg<1, T3_SMALL>::MINB);
         else st = launch(k_tri_tet3<1, T3_LIGHT>, sizeof(T3Warp<1, T3_LIGHT>), T3Cfg<1, T3_LIGHT>::GENS, T3Cfg<1, T3_LIGHT>::MINB);
         if (st != AXB_OK) return st;
