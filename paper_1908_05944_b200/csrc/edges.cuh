@@ -317,9 +317,14 @@ __global__ void __launch_bounds__(EL_WARPS * 32, EL_MINB) k_edges(EstParams P, i
                         any |= m[k];
                     }
                     if (any) {
-                        if (qn + 32 * K > EL_QCAP) {
-                            settle();
-                            if (qn + 32 * K > EL_QCAP) { crowded = true; break; }
+                        if (qn + 32 * K > EL_QCAP) {        // nearly full (dense cores): count exactly what this iteration queues,
+                            int add = 0;                    // the queue is used to its last slot before a pass is given up
+#pragma unroll
+                            for (int k = 0; k < K; ++k) add += __popc(m[k]);
+                            if (qn + add > EL_QCAP) {
+                                settle();
+                                if (qn + add > EL_QCAP) { crowded = true; break; }
+                            }
                         }
 #pragma unroll
                         for (int k = 0; k < K; ++k) {       // (a lane's candidates stay in ascending rank)
