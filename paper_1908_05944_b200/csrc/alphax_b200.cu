@@ -461,7 +461,7 @@ PruneParams prune_params(axb_ctx *c) {
     P.k3_cap = c->k3_cap;
     // n_pt may still be the optimistic capacity (axb_compute); the potential triangles are ~0.8 per potential edge
     const unsigned warps = (unsigned)c->sm_count * (unsigned)PRUNE_GRID * (unsigned)PRUNE_WARPS;
-    P.claim_tris = prune_claim(std::min<unsigned long long>(c->n_pt, c->n_pe), warps, PRUNE_CLAIM_TRIS);
+    P.claim_tris = prune_claim(std::min<unsigned long long>(c->n_pt, c->n_pe), (unsigned)c->sm_count * (unsigned)PRUNE_GRID * (unsigned)TRIS_WARPS, PRUNE_CLAIM_TRIS);
     P.claim_edges = prune_claim(c->n_pe, warps, PRUNE_CLAIM_EDGES);
     return P;
 }
@@ -1084,7 +1084,7 @@ int alloc_prune_arrays(axb_ctx *c, bool early) {
 int run_prune_lower(axb_ctx *c) {
     PruneParams P = prune_params(c);
     int st;
-    k_prune_tris<<<(unsigned)c->sm_count * (unsigned)PRUNE_GRID, PRUNE_THREADS, 0, c->stream>>>(P);
+    k_prune_tris<<<(unsigned)c->sm_count * (unsigned)PRUNE_GRID, TRIS_THREADS, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_TRIANGLES + 1)) != AXB_OK) return st;
     k_prune_edges<<<(unsigned)c->sm_count * (unsigned)PRUNE_GRID, PRUNE_THREADS, 0, c->stream>>>(P);
@@ -2044,7 +2044,7 @@ extern "C" int axb_compute_host_finish(axb_ctx *c, int64_t *h_v, int64_t *h_e, i
     LAUNCH_CHECK(c);
     if ((st = mark_ready(3)) != AXB_OK) return st;
     // triangles
-    k_prune_tris<<<(unsigned)c->sm_count * (unsigned)PRUNE_GRID, PRUNE_THREADS, 0, c->stream>>>(P);
+    k_prune_tris<<<(unsigned)c->sm_count * (unsigned)PRUNE_GRID, TRIS_THREADS, 0, c->stream>>>(P);
     LAUNCH_CHECK(c);
     if ((st = mark_event(c, AXB_ST_PRUNE_TRIANGLES + 1)) != AXB_OK) return st;
     if ((st = device_scan(c, c->cnt2, n, c->off2)) != AXB_OK) return st;

@@ -284,7 +284,10 @@ __global__ void __launch_bounds__(256, TETS_MINB) k_prune_tets(PruneParams P) {
     }
 }
 
-constexpr int PRUNE_THREADS = 256;
+#ifndef PRUNE_THREADS_V
+#define PRUNE_THREADS_V 256
+#endif
+constexpr int PRUNE_THREADS = PRUNE_THREADS_V;
 #ifndef PRUNE_MINB
 #define PRUNE_MINB 4      // <= 64 registers: measured best (occupancy beats the few spilled values)
 #endif
@@ -294,6 +297,13 @@ constexpr int PRUNE_THREADS = 256;
 // FREE entries onto its own shared-memory stack and runs the expensive part (ortho solve + AC2) whenever
 // 32 are waiting -- packed lanes, no block barriers, and dense regions do not leave other warps idle.
 constexpr int PRUNE_WARPS = PRUNE_THREADS / 32;
+// the triangle kernel wants a few more registers than four blocks of 256 threads leave (64: 36 B of spills); seven warps
+// per block are 28 warps per SM at 72 registers (0.241 -> 0.229 ms at 1M atoms); the edge kernel is better off at 64
+#ifndef TRIS_THREADS_V
+#define TRIS_THREADS_V 224
+#endif
+constexpr int TRIS_THREADS = TRIS_THREADS_V;
+constexpr int TRIS_WARPS = TRIS_THREADS / 32;
 // List entries per lane and claim: coarse claims keep a warp inside one neighbourhood (L1) and spare the shared
 // counter, fine ones keep every warp busy when the list is short.  Measured on B200 (tools/gpu_autotune.sh):
 // 1M atoms 4 / 6 (triangles / edges) beat 2 by 11 / 20 %, 50k atoms want 1; larger than 8 loses to tail imbalance.
@@ -315,9 +325,9 @@ constexpr int PRUNE_STACK = 32 + 32 * PRUNE_SCAN_U;   // free entries parked per
                                                       // a scan step adds up to 32 * PRUNE_SCAN_U)
 
 // pipeline.py:502-505: AC2 for the triangles no kept tet inherited
-__global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_tris(PruneParams P) {
-    __shared__ unsigned s_stack[PRUNE_WARPS][PRUNE_STACK];
-    __shared__ int2 s_rows[9][PRUNE_THREADS];
+__global__ void __launch_bounds__(TRIS_THREADS, PRUNE_MINB) k_prune_tris(PruneParams P) {
+    __shared__ unsigned s_stack[TRIS_WARPS][PRUNE_STACK];
+    __shared__ int2 s_rows[9][TRIS_THREADS];
     if (lists_overflowed(P)) return;
     const unsigned n_pt = min(P.ctr->n_pt, P.pt_cap);
     const int lane = lane_id();
@@ -342,7 +352,7 @@ __global__ void __launch_bounds__(PRUNE_THREADS, PRUNE_MINB) k_prune_tris(PruneP
 #if PRUNE_EARLY_MARKS
             if (dv > 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.pe_v + bv));     // the row of the look-up
 #endif
-            if (!ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, -1, &s_rows[0][threadIdx.x], PRUNE_THREADS)) return;
+            if (!ac2_check(P, o.cx, o.cy, o.cz, o.size - P.tol.eps_abs, r.x, r.y, r.z, -1, &s_rows[0][threadIdx.x], TRIS_THREADS)) return;
         }
         // kept: mark the triangle and its three edges.  The lookup first, then all four atomics back to back (their
         // round trips overlap), then the owner counters of what was new (no return value needed: fire and forget)
