@@ -260,7 +260,11 @@ int axb_format_complex(const int64_t counts[4], const int64_t *vertices, const i
                        const int64_t *triangles, const int64_t *tets, char *out, int64_t capacity, int64_t *needed);
 
 /* ---- measurement -------------------------------------------------------- */
-/* CUDA-event milliseconds per stage of the last run */
+/* Stage timing is recorded on request only, like the reference's optional `stage_times` dict
+ * (pipeline.py:571, 595): on != 0 brackets every stage of the following runs with CUDA events (about 30
+ * event records, 0.04-0.06 ms per run); off (the default) records nothing and axb_stage_ms reports zeros. */
+int axb_set_stage_timing(axb_ctx *ctx, int on);
+/* CUDA-event milliseconds per stage of the last run (zeros unless axb_set_stage_timing(ctx, 1)) */
 int axb_stage_ms(const axb_ctx *ctx, float out[AXB_ST_COUNT]);
 /* number of kernels this library launched since the context was created */
 int64_t axb_kernel_launches(const axb_ctx *ctx);

@@ -31,7 +31,7 @@ SYMBOLS = (
     "axb_sweep_prepare", "axb_sweep_prune", "axb_sweep_rank", "axb_sweep_select",
     "axb_prune", "axb_canonicalize", "axb_export",
     "axb_sync_check", "axb_compute", "axb_compute_into", "axb_compute_start", "axb_compute_finish_into", "axb_compute_host", "axb_export_host", "axb_compute_host_begin",
-    "axb_compute_host_finish", "axb_last_d2h_bytes", "axb_stage_ms",
+    "axb_compute_host_finish", "axb_last_d2h_bytes", "axb_stage_ms", "axb_set_stage_timing",
     "axb_kernel_launches", "axb_ortho_batch", "axb_format_complex",
 )
 
@@ -114,6 +114,7 @@ def load() -> C.CDLL:
         "axb_compute_host_finish": (C.c_int, [vp, vp, vp, vp, vp, pi64]),
         "axb_last_d2h_bytes": (i64, [vp]),
         "axb_stage_ms": (C.c_int, [vp, C.POINTER(C.c_float)]),
+        "axb_set_stage_timing": (C.c_int, [vp, C.c_int]),
         "axb_kernel_launches": (i64, [vp]),
         "axb_format_complex": (C.c_int, [pi64, vp, vp, vp, vp, vp, i64, pi64]),
         "axb_ortho_batch": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_double, vp, vp, vp]),

@@ -11,6 +11,7 @@ the reference's exceptions.  There is no CPU fallback.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import math
 import os
@@ -188,6 +189,7 @@ class Engine:
         self.arena = None
         self._stage_ms: dict = {}
         self._stage_ms_stale = False
+        self._stage_timing = False
         # identity of what is resident on the device, for the stage API's handles (stages.py): a new token for every
         # run that rebuilds the grid, a new id for every edge level / simplex level computed or imported
         self._remembered_counts: dict = {}     # (n, configuration) -> row counts of the last result (compute_device)
@@ -302,8 +304,30 @@ class Engine:
         self._stage_ms_stale = True
 
     @property
+    def stage_timing(self) -> bool:
+        """Whether the runs of this engine bracket their stages with CUDA events (``last_stage_ms``).  Off by default,
+        like the reference's ``stage_times=None``: the event records cost 0.04-0.06 ms per run."""
+        return self._stage_timing
+
+    @stage_timing.setter
+    def stage_timing(self, on: bool):
+        self._stage_timing = bool(on)
+        self.lib.axb_set_stage_timing(self.handle, int(self._stage_timing))
+
+    @contextlib.contextmanager
+    def timing_stages(self, on: bool = True):
+        """``with eng.timing_stages(): ...`` -- stage timing for the calls inside, the previous setting afterwards."""
+        before = self._stage_timing
+        self.stage_timing = on
+        try:
+            yield self
+        finally:
+            self.stage_timing = before
+
+    @property
     def last_stage_ms(self) -> dict:
-        """Device time per stage of the most recent call (CUDA events; the reference's stage_times keys)."""
+        """Device time per stage of the most recent call (CUDA events; the reference's stage_times keys); zeros
+        unless ``stage_timing`` was on for that call."""
         if self._stage_ms_stale:
             ms = (C.c_float * len(N.STAGE_KEYS))()
             self.lib.axb_stage_ms(self.handle, ms)
@@ -773,8 +797,10 @@ def compute_alpha_complex_arrays(centers, radii, cfg: PipelineConfig, stage_time
                               "the B200 build; use mode='grid'")
     eng = default_engine(device)
     n = int(np.asarray(radii).shape[0])
-    v, e, t, q = eng.compute_host(centers, radii, cfg)
-    _accumulate_stage_times(stage_times, eng.last_stage_ms)
+    with eng.timing_stages(eng.stage_timing or stage_times is not None):      # events only when somebody reads them
+        v, e, t, q = eng.compute_host(centers, radii, cfg)
+    if stage_times is not None:
+        _accumulate_stage_times(stage_times, eng.last_stage_ms)
     k = AlphaComplex(vertices=v, edges=e, triangles=t, tets=q, alpha=cfg.alpha, ball_count=n)
     # The reference re-checks closure on every result (pipeline.py:623-624).  Here closure holds by construction --
     # a kept simplex marks all its faces on the device, and the emit kernels flag anything inconsistent -- so the

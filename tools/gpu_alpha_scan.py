@@ -17,6 +17,7 @@ from paper_1908_05944_b200 import Engine, PipelineConfig, TolerancePolicy, synth
 c, r = synth.jittered_lattice(1_000_000, 0)
 dc, dr = torch.as_tensor(c, device="cuda"), torch.as_tensor(r, device="cuda")
 eng = Engine(0)
+eng.stage_timing = True          # this tool reads eng.last_stage_ms
 out = []
 for alpha in (0.0, 0.2, 0.4, 0.6, 0.8, 1.0, 1.4):
     cfg = PipelineConfig(alpha=alpha, tolerance=TolerancePolicy(1e-9, 1e-300))

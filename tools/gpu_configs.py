@@ -22,6 +22,7 @@ from paper_1908_05944_b200 import synth  # noqa: E402
 def run(name, c, r, alpha, eps_sing, check=True):
     cfg = ax.PipelineConfig(alpha=alpha, tolerance=ax.TolerancePolicy(1e-9, eps_sing))
     eng = ax.default_engine()
+    eng.stage_timing = True          # this tool reads eng.last_stage_ms
     ax.compute_alpha_complex_arrays(c, r, cfg)                       # warm-up (arena growth, pinned buffers)
     t0 = time.perf_counter()
     k = ax.compute_alpha_complex_arrays(c, r, cfg)

@@ -102,6 +102,7 @@ def main():
     big = "--big" in sys.argv
     print("device:", torch.cuda.get_device_name(0))
     eng = Engine(0)
+    eng.stage_timing = True          # this tool reads eng.last_stage_ms
     allok = True
     # 1. predicate arithmetic
     d = np.load(os.path.join(GOLD, "ortho_vectors.npz"))

@@ -22,6 +22,7 @@ for n in [int(a) for a in sys.argv[1:]] or [10_000_000, 17_000_000]:
     c, r = synth.jittered_lattice(n, 0)
     cfg = ax.PipelineConfig(alpha=0.0, tolerance=ax.TolerancePolicy(1e-9, 1e-300))
     eng = ax.default_engine()
+    eng.stage_timing = True          # this tool reads eng.last_stage_ms
     ax.compute_alpha_complex_arrays(c, r, cfg)
     t0 = time.perf_counter()
     k = ax.compute_alpha_complex_arrays(c, r, cfg)

@@ -21,6 +21,7 @@ from paper_1908_05944_b200 import Engine, PipelineConfig, TolerancePolicy, synth
 def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
     eng = Engine(0)
+    eng.stage_timing = True          # this tool reads eng.last_stage_ms
     tol = TolerancePolicy(1e-9, 1e-300)
     work = [("g2_1M_a0", synth.jittered_lattice(1_000_000, 0), 0.0),
             ("g2_1M_a1.4", synth.jittered_lattice(1_000_000, 0), 1.4),

@@ -18,6 +18,7 @@ alpha = float(sys.argv[2]) if len(sys.argv) > 2 else 0.0
 passes = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 c, r = synth.jittered_lattice(n, 0)
 eng = Engine(0)
+eng.stage_timing = True          # this tool reads eng.last_stage_ms
 cfg = PipelineConfig(alpha=alpha, tolerance=TolerancePolicy(1e-9, 1e-300))
 dc, dr = torch.as_tensor(c, device="cuda"), torch.as_tensor(r, device="cuda")
 for _ in range(passes):
