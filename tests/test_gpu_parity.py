@@ -81,6 +81,30 @@ def test_config1_through_ball_boundary(gold_config1):
         assert ax.complex_stats(k).total == sum(m["counts"])
 
 
+def test_stage_times_are_recorded_on_request_only():
+    """The reference fills `stage_times` only for a caller who passes a dict (pipeline.py:571, 595); here the CUDA
+    events behind it are recorded only then (axb_set_stage_timing): same complex either way."""
+    c, r = synth.jittered_lattice(20_000, seed=5)
+    cfg = ax.PipelineConfig(alpha=0.4)
+    eng = ax.default_engine()
+    assert not eng.stage_timing
+    plain = ax.compute_alpha_complex_arrays(c, r, cfg)
+    assert sum(eng.last_stage_ms.values()) == 0.0
+    st = {}
+    timed = ax.compute_alpha_complex_arrays(c, r, cfg, stage_times=st)
+    assert not eng.stage_timing                                   # restored
+    assert st["potential_edges"] > 0.0 and st["prune_triangles"] > 0.0 and st["grid"] > 0.0
+    for a, b in zip(arrays_of(plain), arrays_of(timed)):
+        assert np.array_equal(a, b)
+    import torch
+    dc, dr = torch.as_tensor(c, device="cuda"), torch.as_tensor(r, device="cuda")
+    with eng.timing_stages():
+        eng.compute_device(dc, dr, cfg)
+        assert eng.last_stage_ms["potential_triangles"] > 0.0 and eng.last_stage_ms["canonical"] > 0.0
+    eng.compute_device(dc, dr, cfg)
+    assert sum(eng.last_stage_ms.values()) == 0.0
+
+
 def test_stagewise_against_oracle():
     """grid order, potential levels (rows + cached ortho data bitwise) and the complex, stage by stage."""
     import torch
