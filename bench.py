@@ -596,6 +596,9 @@ def main():
     args = ap.parse_args()
     if args.steps is None:
         args.steps = 3 if args.impl == "reference" else 100      # a pass of the CPU implementation takes seconds
+    if args.gpus > 1 and args.eps_singular == 1e-12:
+        args.eps_singular = 1e-300          # multi-million-atom sets trip the default pivot threshold in BOTH
+                                            # implementations; both arms of an N > 1 run use the same value
     if args.impl == "reference":
         bench_reference(args, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
         return
@@ -609,8 +612,6 @@ def main():
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")            # the communicator's own log (rings, NVLS) goes to stderr
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        if args.eps_singular == 1e-12:
-            args.eps_singular = 1e-300      # large sets trip the default pivot threshold in BOTH implementations
     bench_b200(args, rank, world, local_rank)
 
 
